@@ -1,0 +1,175 @@
+/*
+ * apml.h -- C ABI of libapml.so, the B200 (sm_100a) sparse APML / CUDA-APML hot path.
+ *
+ * The method: Sharifipour et al., "From Theory to Throughput: CUDA-Optimized APML for
+ * Large-Batch 3D Learning" (arXiv 2512.19743).  Citations are PAPER.md line numbers,
+ * written P:<line>, with the section / equation / algorithm they fall in.
+ *
+ * What one call computes, per (pred, gt) pair b of a batch (Algorithm 1):
+ *   C_ij = ||x_i - y_j||_2                                  (section III-A)
+ *   per row i (K = M) and per column j (K = N): min, second minimum of the multiset,
+ *   g = max(c~(2) + delta, eps_g), T = -log((1-p_min)/((K-1) p_min)) / g
+ *                                                          (Eq. (1); clamp P:140)
+ *   s = exp(-T (C - C_min)), keep s >= tau                  (section III-B)
+ *   normalise each line by its kept sum                     (section III-C)
+ *   P0 = (P_row + P_col) / 2 on the union support           (a missing
+ *                                                            direction counts as 0)
+ *   L_iter x { column scaling Eq. (3), row scaling Eq. (4) } with eps_stab
+ *   loss_b = sum_t v_t ||x_i - y_j||                        (section III-D)
+ * and its gradient with respect to pred (Eq. (5)).  No N x M buffer is ever
+ * allocated: memory is O(B (capacity + N + M)).
+ *
+ * Conventions for every entry point
+ *   - Point buffers are fp32, xyz-interleaved (array of structs): pred [B][N][3],
+ *     gt [B][M][3]; d = 3 is fixed.  Pointers to point / loss / gradient buffers are
+ *     CUDA DEVICE pointers unless the function name ends in _host.
+ *   - All device work is enqueued on `stream` (a cudaStream_t passed as void*; NULL =
+ *     the legacy default stream).  No entry point synchronises the device unless its
+ *     comment says so.
+ *   - Ownership: the caller owns every buffer it passes; the library owns the context's
+ *     internals (allocated through the caller's apml_allocator, or cudaMallocAsync when
+ *     the allocator is NULL) and releases them in apml_ctx_destroy.
+ *   - Errors: every function returning apml_status validates its arguments on the host
+ *     before launching anything; on a non-OK status nothing has been written to caller
+ *     buffers and apml_last_error() returns a thread-local message.
+ *   - Threading: re-entrant; one context per forward call.
+ */
+#ifndef APML_H
+#define APML_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APML_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define APML_API __attribute__((visibility("default")))
+#else
+#define APML_API
+#endif
+
+typedef enum {
+    APML_OK = 0,
+    APML_ERR_INVALID_ARG = 1, /* hyper-parameter outside its domain, NULL pointer */
+    APML_ERR_SHAPE = 2,       /* B, N or M < 1, or N, M >= 2^30 */
+    APML_ERR_NONFINITE = 3,   /* non-finite coordinate (only with APML_FLAG_CHECK_FINITE) */
+    APML_ERR_CAPACITY = 4,    /* support exceeded the emit capacity and could not be retried */
+    APML_ERR_CUDA = 5,        /* a CUDA runtime call failed */
+    APML_ERR_OOM = 6,         /* the allocator returned NULL */
+    APML_ERR_STATE = 7        /* backward on a context without saved state, or called twice */
+} apml_status;
+
+typedef enum {
+    APML_GRAD_FULL = 0,          /* through softmax (incl. T via the gap), symmetrisation and
+                                    Sinkhorn: "differentiates through the same sparse
+                                    computation graph" */
+    APML_GRAD_PLAN_DETACHED = 1  /* transport weights held constant: Eq. (5) only */
+} apml_grad_mode;
+
+/* flags */
+#define APML_FLAG_SYNC_CHECK   1u /* after emission, read the per-pair support counts back
+                                     (one device->host sync) and re-run with an exact
+                                     capacity if any pair overflowed.  Without it the call is
+                                     sync-free / graph-capturable and an overflowed pair gets
+                                     a NaN loss (reported by apml_ctx_stats). */
+#define APML_FLAG_CHECK_FINITE 2u /* scan the inputs for NaN/Inf first (one extra pass + sync) */
+
+typedef struct {
+    float   p_min;        /* Eq. (1); 0 < p_min < 1 and p_min > 1/K for every line
+                             length K in {N, M} with K > 1; default 0.9 (paper defers) */
+    float   tau;          /* pruning threshold on the UNNORMALISED similarity, keep s >= tau,
+                             0 <= tau <= 1; default 1e-8 */
+    int32_t l_iter;       /* Sinkhorn iterations, >= 0; default 10 */
+    float   eps_stab;     /* Sinkhorn stability constant, > 0; default 1e-8 */
+    float   delta;        /* g = c~(2) + delta, >= 0; default 1e-6 */
+    float   eps_g;        /* gap clamp g = max(g, eps_g), > 0; default 1e-8 */
+    float   eps_dist;     /* Eq. (5) denominator, > 0; default 1e-8 */
+    int32_t grad_mode;    /* apml_grad_mode; default APML_GRAD_FULL */
+    int32_t capacity;     /* emit capacity per pair in entries per point: cap = capacity*(N+M),
+                             clipped to N*M; 0 = default (6) */
+    uint32_t flags;       /* APML_FLAG_*; default APML_FLAG_SYNC_CHECK */
+} apml_config;
+
+/* Stream-ordered allocator used for all library-owned device memory. */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* stream, void* user);
+    void  (*free)(void* ptr, size_t bytes, void* stream, void* user);
+    void* user;
+} apml_allocator;
+
+/* Per-call diagnostics (SPEC LossResult analogue). */
+typedef struct {
+    int64_t nnz_total;      /* |Omega_tau| summed over pairs (entries carrying a row or column flag) */
+    int64_t emitted_total;  /* emitted entries incl. second-argmin-only entries (tau > tau*) */
+    int64_t clamp_count;    /* lines whose gap was clamped to eps_g */
+    int64_t capacity;       /* emit capacity per pair actually used (entries) */
+    int64_t overflow_pairs; /* pairs whose support exceeded capacity (their loss is NaN) */
+    int64_t bytes_ctx;      /* device bytes owned by the context */
+} apml_stats;
+
+typedef struct apml_ctx apml_ctx; /* opaque: state saved by forward for backward */
+
+APML_API int apml_abi_version(void);
+
+/* Paper / DESIGN.md defaults into *cfg. */
+APML_API void apml_config_default(apml_config* cfg);
+
+/* Forward, Algorithm 1 lines 1-8 for B independent pairs.
+ *   pred   device [B][N][3] fp32 (x_i, predicted points)
+ *   gt     device [B][M][3] fp32 (y_j, reference points)
+ *   cfg    NULL -> apml_config_default
+ *   alloc  NULL -> cudaMallocAsync / cudaFreeAsync on `stream`
+ *   loss   device [B] fp32, per-pair <P, C> (unreduced; the caller reduces)
+ *   ctx_out NULL -> no backward state is kept; else *ctx_out receives a context that the
+ *          caller must release with apml_ctx_destroy (also on the error path it is NULL).
+ * Synchronises the host only with APML_FLAG_SYNC_CHECK / APML_FLAG_CHECK_FINITE. */
+APML_API apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
+                         const apml_config* cfg, const apml_allocator* alloc, void* stream,
+                         float* loss, apml_ctx** ctx_out);
+
+/* Backward: grad_pred [B][N][3] (device, overwritten) = sum_b grad_loss[b] *
+ * d loss_b / d pred_b.  grad_loss device [B].  One backward per context (ERR_STATE after). */
+APML_API apml_status apml_backward(apml_ctx* ctx, const float* grad_loss, float* grad_pred, void* stream);
+
+/* Diagnostics; SYNCHRONISES the context's stream.  nnz_per_pair: host [B] or NULL. */
+APML_API apml_status apml_ctx_stats(const apml_ctx* ctx, int64_t* nnz_per_pair, apml_stats* out);
+
+/* Introspection (tests / diagnostics).  Copies pair b's support to the host in CSR order
+ * (row-major, j ascending); SYNCHRONISES.  *count: in = capacity of the arrays, out =
+ * number of entries (APML_ERR_CAPACITY if the arrays are too small; *count is still set).
+ * flags: 1 = kept by the row softmax, 2 = kept by the column softmax, 0 = second-argmin
+ * entry emitted only for the T-gradient (tau > tau*, reading R14).  p0 = P0, v = the final
+ * plan a_i P0_ij b_j.  Any array pointer may be NULL. */
+APML_API apml_status apml_ctx_support(const apml_ctx* ctx, int64_t b, int64_t* count, int32_t* i,
+                                      int32_t* j, int32_t* flags, float* p0, float* v);
+
+/* Per-line statistics of pair b (dir 0: rows, length N; dir 1: columns, length M), host
+ * arrays, SYNCHRONISES: m = min distance, c2 = second smallest distance, T = Eq. (1)
+ * temperature (0 for K = 1 lines), argmin / second = index of the other cloud (-1 if none).
+ * Any pointer may be NULL. */
+APML_API apml_status apml_ctx_lines(const apml_ctx* ctx, int64_t b, int32_t dir, float* m,
+                                    float* c2, float* T, int32_t* argmin, int32_t* second);
+
+/* Release a context (stream-ordered free on the context's stream).  NULL is a no-op. */
+APML_API void apml_ctx_destroy(apml_ctx* ctx);
+
+/* End-to-end convenience on HOST buffers: copies pred/gt host->device, runs forward and
+ * backward with grad_loss = 1 for every pair (sum reduction), copies loss [B] and
+ * grad_pred [B][N][3] back to the host.  Pinned host memory gives async copies.
+ * Synchronises `stream` before returning. */
+APML_API apml_status apml_loss_grad_host(const float* pred_host, const float* gt_host, int64_t B,
+                                int64_t N, int64_t M, const apml_config* cfg,
+                                const apml_allocator* alloc, void* stream, float* loss_host,
+                                float* grad_pred_host);
+
+/* Thread-local message describing the last non-OK status on this thread. */
+APML_API const char* apml_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APML_H */

@@ -1,0 +1,191 @@
+"""Python binding of libapml.so (include/apml.h) -- argument marshalling only.
+
+Every step of the method runs in the CUDA kernels behind the C ABI; this module passes
+device pointers, sizes and the current torch stream, and lets torch's caching allocator
+back the library's workspace (so ``torch.cuda.max_memory_allocated`` sees it).
+
+    loss = apml_loss(pred, gt)                 # [B,N,3], [B,M,3] fp32 CUDA -> scalar (sum)
+    loss.backward()                            # grad w.r.t. pred
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as A
+
+
+@dataclass
+class Config:
+    """Hyper-parameters, defaults per PAPER.md P:176 and DESIGN.md R2/R3."""
+    p_min: float = 0.9
+    tau: float = 1e-8
+    l_iter: int = 10
+    eps_stab: float = 1e-8
+    delta: float = 1e-6
+    eps_g: float = 1e-8
+    eps_dist: float = 1e-8
+    grad_mode: str = "full"          # "full" | "plan_detached"
+    capacity: int = 0                # entries per point per pair; 0 = library default
+    sync_check: bool = True          # read back support counts and retry on overflow
+    check_finite: bool = False
+
+    def to_c(self) -> A.ApmlConfig:
+        if self.grad_mode not in ("full", "plan_detached"):
+            raise ValueError(f"grad_mode must be 'full' or 'plan_detached', got {self.grad_mode!r}")
+        flags = (A.APML_FLAG_SYNC_CHECK if self.sync_check else 0) | \
+            (A.APML_FLAG_CHECK_FINITE if self.check_finite else 0)
+        return A.ApmlConfig(self.p_min, self.tau, self.l_iter, self.eps_stab, self.delta, self.eps_g,
+                            self.eps_dist, A.APML_GRAD_FULL if self.grad_mode == "full"
+                            else A.APML_GRAD_PLAN_DETACHED, self.capacity, flags)
+
+
+def _torch_alloc(nbytes, stream, user):
+    return torch.cuda.caching_allocator_alloc(int(nbytes), stream=int(stream or 0))
+
+
+def _torch_free(ptr, nbytes, stream, user):
+    torch.cuda.caching_allocator_delete(int(ptr))
+
+
+_ALLOC = A.ApmlAllocator(A.ALLOC_FN(_torch_alloc), A.FREE_FN(_torch_free), None)
+
+
+def _check_points(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != torch.float32 or t.dim() != 3 or t.shape[-1] != 3:
+        raise ValueError(f"{name} must be float32 [B, n, 3], got {tuple(t.shape)} {t.dtype}")
+    return t.contiguous()
+
+
+class Context:
+    """Saved forward state (opaque apml_ctx*) for one backward."""
+
+    def __init__(self, handle: int, B: int, N: int, M: int, device: torch.device):
+        self._h = handle
+        self.B, self.N, self.M, self.device = B, N, M, device
+
+    def stats(self) -> dict:
+        """apml_ctx_stats (synchronises the stream)."""
+        nnz = (C.c_int64 * self.B)()
+        st = A.ApmlStats()
+        A.check(A.lib().apml_ctx_stats(self._h, C.cast(nnz, C.c_void_p), C.byref(st)))
+        return dict(nnz=list(nnz), nnz_total=st.nnz_total, emitted_total=st.emitted_total,
+                    clamp_count=st.clamp_count, capacity=st.capacity,
+                    overflow_pairs=st.overflow_pairs, bytes_ctx=st.bytes_ctx)
+
+    def support(self, b: int) -> dict:
+        """apml_ctx_support for pair b (synchronises): CSR-ordered i, j, flags, P0, v."""
+        import numpy as np
+        n = C.c_int64(0)
+        st = A.lib().apml_ctx_support(self._h, b, C.byref(n), None, None, None, None, None)
+        if st not in (A.APML_OK, A.APML_ERR_CAPACITY) or (st != A.APML_OK and n.value == 0):
+            A.check(st)
+        k = n.value
+        i = np.zeros(max(k, 1), np.int32); j = np.zeros_like(i); fl = np.zeros_like(i)
+        p0 = np.zeros(max(k, 1), np.float32); v = np.zeros_like(p0)
+        ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+        A.check(A.lib().apml_ctx_support(self._h, b, C.byref(n), ptr(i), ptr(j), ptr(fl), ptr(p0), ptr(v)))
+        return dict(i=i[:k], j=j[:k], flags=fl[:k], p0=p0[:k], v=v[:k])
+
+    def lines(self, b: int, direction: int) -> dict:
+        """apml_ctx_lines for pair b (synchronises): m, c2, T, argmin, second."""
+        import numpy as np
+        n = self.M if direction else self.N
+        m = np.zeros(n, np.float32); c2 = np.zeros_like(m); T = np.zeros_like(m)
+        a = np.zeros(n, np.int32); s = np.zeros_like(a)
+        ptr = lambda x: x.ctypes.data_as(C.c_void_p)
+        A.check(A.lib().apml_ctx_lines(self._h, b, direction, ptr(m), ptr(c2), ptr(T), ptr(a), ptr(s)))
+        return dict(m=m, c2=c2, T=T, a=a, b=s)
+
+    def backward(self, grad_loss: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        gl = grad_loss.to(device=self.device, dtype=torch.float32).contiguous().reshape(self.B)
+        g = out if out is not None else torch.empty(self.B, self.N, 3, device=self.device)
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        A.check(A.lib().apml_backward(self._h, gl.data_ptr(), g.data_ptr(), s))
+        return g
+
+    def close(self):
+        if self._h:
+            A.lib().apml_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def forward(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
+            keep_ctx: bool = True, loss_out: torch.Tensor | None = None):
+    """Per-pair losses [B] (fp32, device) and a Context for backward (or None)."""
+    cfg = cfg or Config()
+    pred = _check_points(pred, "pred")
+    gt = _check_points(gt, "gt")
+    if pred.shape[0] != gt.shape[0] or pred.device != gt.device:
+        raise ValueError("pred and gt must share batch size and device (BatchShapeMismatch)")
+    B, N, M = pred.shape[0], pred.shape[1], gt.shape[1]
+    loss = loss_out if loss_out is not None else torch.empty(B, device=pred.device, dtype=torch.float32)
+    h = C.c_void_p()
+    c = cfg.to_c()
+    with torch.cuda.device(pred.device):
+        s = torch.cuda.current_stream(pred.device).cuda_stream
+        A.check(A.lib().apml_forward(pred.data_ptr(), gt.data_ptr(), B, N, M, C.byref(c),
+                                     C.byref(_ALLOC), s, loss.data_ptr(),
+                                     C.byref(h) if keep_ctx else None))
+    ctx = Context(h.value, B, N, M, pred.device) if keep_ctx else None
+    return loss, ctx
+
+
+class _APMLFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(fctx, pred, gt, cfg):
+        loss, ctx = forward(pred, gt, cfg, keep_ctx=True)
+        fctx.apml = ctx
+        return loss
+
+    @staticmethod
+    def backward(fctx, grad_loss):
+        ctx = fctx.apml
+        g = ctx.backward(grad_loss)
+        ctx.close()
+        return g, None, None
+
+
+def apml_loss(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
+              reduction: str = "sum") -> torch.Tensor:
+    """Batched sparse APML (Alg. 1) with autograd w.r.t. pred."""
+    loss = _APMLFunction.apply(pred, gt, cfg or Config())
+    if reduction == "sum":
+        return loss.sum()
+    if reduction == "mean":
+        return loss.mean()
+    if reduction == "none":
+        return loss
+    raise ValueError(f"unknown reduction {reduction!r}")
+
+
+def loss_grad_host(pred_host: torch.Tensor, gt_host: torch.Tensor, cfg: Config | None = None,
+                   loss_out: torch.Tensor | None = None, grad_out: torch.Tensor | None = None,
+                   device: int | None = None):
+    """apml_loss_grad_host: host fp32 buffers in, host loss [B] and grad [B,N,3] out (sum
+    reduction), host<->device copies included.  Pinned inputs give async copies."""
+    cfg = cfg or Config()
+    for t, n in ((pred_host, "pred"), (gt_host, "gt")):
+        if t.is_cuda or t.dtype != torch.float32 or t.dim() != 3 or not t.is_contiguous():
+            raise ValueError(f"{n} must be a contiguous float32 host tensor [B, n, 3]")
+    B, N, M = pred_host.shape[0], pred_host.shape[1], gt_host.shape[1]
+    loss = loss_out if loss_out is not None else torch.empty(B, dtype=torch.float32, pin_memory=True)
+    grad = grad_out if grad_out is not None else torch.empty(B, N, 3, dtype=torch.float32, pin_memory=True)
+    c = cfg.to_c()
+    dev = torch.cuda.current_device() if device is None else device
+    with torch.cuda.device(dev):
+        s = torch.cuda.current_stream().cuda_stream
+        A.check(A.lib().apml_loss_grad_host(pred_host.data_ptr(), gt_host.data_ptr(), B, N, M,
+                                            C.byref(c), C.byref(_ALLOC), s, loss.data_ptr(),
+                                            grad.data_ptr()))
+    return loss, grad

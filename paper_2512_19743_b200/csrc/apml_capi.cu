@@ -1,0 +1,511 @@
+// apml_capi.cu -- host side of libapml.so: validation, context / workspace, launch sequence.
+// Declarations and the contract of every entry point: include/apml.h.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/apml.h"
+#include "common.cuh"
+#include "k_backward.cuh"
+#include "k_dist.cuh"
+#include "k_sparse.cuh"
+
+using namespace apml;
+
+namespace {
+
+thread_local std::string g_err;
+
+apml_status fail(apml_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) return fail(APML_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+constexpr int kR = 4;                        // owned points per thread in the sweeps
+constexpr int kOwnTile = kSweepThreads * kR; // owned points per CTA (512)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// Workspace carve-out (256-byte aligned sub-buffers of one allocation).
+struct Carve {
+  size_t off = 0;
+  template <class T>
+  size_t take(int64_t count) {
+    size_t o = off;
+    off += round_up((int64_t)(sizeof(T) * (size_t)(count > 0 ? count : 1)), 256);
+    return o;
+  }
+};
+
+}  // namespace
+
+struct apml_ctx {
+  int64_t B = 0, N = 0, M = 0, Np = 0, Mp = 0;
+  apml_config cfg{};
+  cudaStream_t stream = nullptr;
+  apml_allocator alloc{};
+  bool has_alloc = false;
+  char* base = nullptr;
+  size_t bytes = 0;
+  uint32_t cap = 0;
+  int S_rows = 1, S_cols = 1, chunk_rows = 0, chunk_cols = 0;
+  bool backward_done = false;
+  bool smem_sinkhorn = false;
+  size_t smem_bytes = 0;
+  float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
+  // sub-buffers
+  float *predS, *gtS; float4 *pred4, *gt4;
+  float2 *part_r, *part_c;
+  LineA *rowA, *colA; LineB *rowB, *colB;
+  unsigned long long* clamp;
+  uint2* ebuf; unsigned *cursor, *aux;
+  unsigned *row_cnt, *col_cnt, *row_ptr, *col_ptr;
+  uint32_t *csr_t, *csc_t, *inv, *csr_jf, *csc_i, *csc_perm;
+  float *d2s, *cs, *prow, *pcol, *P0, *P0c, *pbar;
+  int2 *rowidx, *colidx;
+  float *a_hist, *b_hist, *Rbar, *Qbar, *gscratch;
+  LineBack *rowback, *colback;
+};
+
+namespace {
+
+void* ctx_alloc(apml_ctx* c, size_t bytes) {
+  if (c->has_alloc) return c->alloc.alloc(bytes, c->stream, c->alloc.user);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void ctx_free(apml_ctx* c) {
+  if (!c->base) return;
+  if (c->has_alloc) c->alloc.free(c->base, c->bytes, c->stream, c->alloc.user);
+  else cudaFreeAsync(c->base, c->stream);
+  c->base = nullptr;
+}
+
+apml_status validate(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
+                     const apml_config& c) {
+  if (!pred || !gt) return fail(APML_ERR_INVALID_ARG, "pred / gt must be non-NULL device pointers");
+  if (B < 1 || N < 1 || M < 1) return fail(APML_ERR_SHAPE, "B, N and M must be >= 1 (EmptyCloud)");
+  if (N >= (1 << 30) || M >= (1 << 30)) return fail(APML_ERR_SHAPE, "N and M must be < 2^30");
+  if (B > 65535) return fail(APML_ERR_SHAPE, "B must be <= 65535 (grid.y / grid.z limit)");
+  if (!(c.p_min > 0.f && c.p_min < 1.f)) return fail(APML_ERR_INVALID_ARG, "p_min must lie in (0, 1) (Eq. 1)");
+  for (int64_t K : {N, M})
+    if (K > 1 && !((double)c.p_min * (double)K > 1.0))
+      return fail(APML_ERR_INVALID_ARG, "p_min <= 1/K makes T <= 0 (dense line); outside the sparse contract");
+  if (!(c.tau >= 0.f && c.tau <= 1.f)) return fail(APML_ERR_INVALID_ARG, "tau must lie in [0, 1]");
+  if (c.l_iter < 0) return fail(APML_ERR_INVALID_ARG, "l_iter must be >= 0");
+  if (!(c.eps_stab > 0.f) || !(c.eps_g > 0.f) || !(c.eps_dist > 0.f) || !(c.delta >= 0.f))
+    return fail(APML_ERR_INVALID_ARG, "eps_stab, eps_g, eps_dist must be > 0 and delta >= 0");
+  if (c.grad_mode != APML_GRAD_FULL && c.grad_mode != APML_GRAD_PLAN_DETACHED)
+    return fail(APML_ERR_INVALID_ARG, "unknown grad_mode");
+  if (c.capacity < 0) return fail(APML_ERR_INVALID_ARG, "capacity must be >= 0");
+  return APML_OK;
+}
+
+// Lambda_K = -log((1 - p) / ((K - 1) p)) (numerator of Eq. (1)), fp64.
+double lambda_K(int64_t K, double p) { return K > 1 ? -std::log((1.0 - p) / ((double)(K - 1) * p)) : 0.0; }
+
+int num_sms() {
+  static int sms = -1;
+  if (sms < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+  }
+  return sms;
+}
+
+// Column-range split of a sweep so that the grid covers the SMs several times over.
+void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk) {
+  const int64_t blocks = own_np / kOwnTile * B;
+  const int64_t target = 4LL * num_sms() * 4;  // ~4 waves of 4 CTAs / SM
+  int64_t s = (target + blocks - 1) / blocks;
+  const int64_t tiles = str_np / kTQ;
+  if (s > tiles) s = tiles;
+  if (s < 1) s = 1;
+  const int64_t ch = round_up((tiles + s - 1) / s, 1) * kTQ;
+  *chunk = (int)ch;
+  *S = (int)((str_np + ch - 1) / ch);
+}
+
+apml_status build_ctx(apml_ctx* c, uint32_t cap) {
+  const int64_t B = c->B, N = c->N, M = c->M, L = c->cfg.l_iter;
+  c->cap = cap;
+  c->Np = round_up(N, kOwnTile);
+  c->Mp = round_up(M, kOwnTile);
+  plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows);
+  plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols);
+  Carve k;
+  const int64_t E = B * (int64_t)cap;
+  size_t o_predS = k.take<float>(B * 3 * c->Np), o_gtS = k.take<float>(B * 3 * c->Mp);
+  size_t o_pred4 = k.take<float4>(B * N), o_gt4 = k.take<float4>(B * M);
+  size_t o_part_r = k.take<float2>((int64_t)c->S_rows * B * c->Np);
+  size_t o_part_c = k.take<float2>((int64_t)c->S_cols * B * c->Mp);
+  size_t o_rowA = k.take<LineA>(B * N), o_colA = k.take<LineA>(B * M);
+  size_t o_rowB = k.take<LineB>(B * N), o_colB = k.take<LineB>(B * M);
+  // counters first in one contiguous zeroed block
+  size_t z0 = k.off;
+  size_t o_clamp = k.take<unsigned long long>(1);
+  size_t o_cursor = k.take<unsigned>(B), o_aux = k.take<unsigned>(B);
+  size_t o_row_cnt = k.take<unsigned>(B * (N + 1)), o_col_cnt = k.take<unsigned>(B * (M + 1));
+  size_t z1 = k.off;
+  size_t o_row_ptr = k.take<unsigned>(B * (N + 1)), o_col_ptr = k.take<unsigned>(B * (M + 1));
+  size_t o_ebuf = k.take<uint2>(E);
+  size_t o_csr_t = k.take<uint32_t>(E), o_csc_t = k.take<uint32_t>(E), o_inv = k.take<uint32_t>(E);
+  size_t o_csr_jf = k.take<uint32_t>(E), o_csc_i = k.take<uint32_t>(E), o_csc_perm = k.take<uint32_t>(E);
+  size_t o_d2 = k.take<float>(E), o_cs = k.take<float>(E), o_prow = k.take<float>(E), o_pcol = k.take<float>(E);
+  size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
+  size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
+  size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
+  size_t o_Rbar = k.take<float>(B * N * (L > 0 ? L : 1)), o_Qbar = k.take<float>(B * M * (L > 0 ? L : 1));
+  size_t o_gs = k.take<float>(B * (N + M));
+  size_t o_rowback = k.take<LineBack>(B * N), o_colback = k.take<LineBack>(B * M);
+  c->bytes = k.off;
+  c->base = (char*)ctx_alloc(c, c->bytes);
+  if (!c->base) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->bytes) + " bytes failed");
+  char* p = c->base;
+  c->predS = (float*)(p + o_predS); c->gtS = (float*)(p + o_gtS);
+  c->pred4 = (float4*)(p + o_pred4); c->gt4 = (float4*)(p + o_gt4);
+  c->part_r = (float2*)(p + o_part_r); c->part_c = (float2*)(p + o_part_c);
+  c->rowA = (LineA*)(p + o_rowA); c->colA = (LineA*)(p + o_colA);
+  c->rowB = (LineB*)(p + o_rowB); c->colB = (LineB*)(p + o_colB);
+  c->clamp = (unsigned long long*)(p + o_clamp);
+  c->cursor = (unsigned*)(p + o_cursor); c->aux = (unsigned*)(p + o_aux);
+  c->row_cnt = (unsigned*)(p + o_row_cnt); c->col_cnt = (unsigned*)(p + o_col_cnt);
+  c->row_ptr = (unsigned*)(p + o_row_ptr); c->col_ptr = (unsigned*)(p + o_col_ptr);
+  c->ebuf = (uint2*)(p + o_ebuf);
+  c->csr_t = (uint32_t*)(p + o_csr_t); c->csc_t = (uint32_t*)(p + o_csc_t); c->inv = (uint32_t*)(p + o_inv);
+  c->csr_jf = (uint32_t*)(p + o_csr_jf); c->csc_i = (uint32_t*)(p + o_csc_i); c->csc_perm = (uint32_t*)(p + o_csc_perm);
+  c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
+  c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
+  c->rowidx = (int2*)(p + o_rowidx); c->colidx = (int2*)(p + o_colidx);
+  c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh);
+  c->Rbar = (float*)(p + o_Rbar); c->Qbar = (float*)(p + o_Qbar); c->gscratch = (float*)(p + o_gs);
+  c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
+  CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
+  c->smem_bytes = (size_t)(N + M) * sizeof(float);
+  c->smem_sinkhorn = c->smem_bytes <= 200 * 1024;
+  if (c->smem_sinkhorn && c->smem_bytes > 48 * 1024) {
+    CK(cudaFuncSetAttribute(k_sinkhorn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+    CK(cudaFuncSetAttribute(k_sinkhorn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+  }
+  return APML_OK;
+}
+
+apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt, float* loss) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
+  cudaStream_t s = c->stream;
+  (void)loss;
+  // S0 staging
+  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
+  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
+  // S1 Pass A: rows (own pred, stream gt) and columns (own gt, stream pred)
+  k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
+      c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
+  k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
+      c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
+  // S2 line constants
+  k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
+      c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+  k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, N, c->lam_c,
+      c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+  // S3 Pass B emit
+  k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
+      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
+      c->aux, c->row_cnt, c->col_cnt);
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
+apml_status launch_sparse(apml_ctx* c, float* loss) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M;
+  const int L = c->cfg.l_iter;
+  cudaStream_t s = c->stream;
+  const uint32_t cap = c->cap;
+  // S4 CSR / CSC
+  k_scan<<<B, 1024, 0, s>>>(c->row_cnt, c->row_ptr, N);
+  k_scan<<<B, 1024, 0, s>>>(c->col_cnt, c->col_ptr, M);
+  k_scatter<<<dim3((cap + 255) / 256, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, N, M, c->row_ptr,
+      c->row_cnt, c->col_ptr, c->col_cnt, c->csr_t, c->csc_t);
+  k_sort_lines<true><<<dim3((N + 7) / 8, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, N, c->row_ptr,
+      c->csr_t, c->csr_jf, c->inv, nullptr);
+  k_sort_lines<false><<<dim3((M + 7) / 8, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, M, c->col_ptr,
+      c->csc_t, c->csc_i, c->inv, c->csc_perm);
+  // S5 normalisation + symmetrisation
+  k_row_norm<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->pred4, c->gt4, N, M, c->cursor, cap,
+      c->row_ptr, c->csr_jf, c->rowA, c->rowB, c->d2s, c->cs, c->prow, c->rowidx);
+  k_col_norm<<<dim3((M + 255) / 256, B), 256, 0, s>>>(N, M, c->cursor, cap, c->col_ptr, c->csc_i,
+      c->csc_perm, c->csr_jf, c->colA, c->colB, c->d2s, c->cs, c->prow, c->pcol, c->P0, c->P0c,
+      c->colidx);
+  // S6 + S7 Sinkhorn and loss
+  k_sinkhorn<<<B, 1024, c->smem_sinkhorn ? c->smem_bytes : 0, s>>>(N, M, L, c->cfg.eps_stab,
+      c->cursor, cap, c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist,
+      c->b_hist, c->gscratch, c->smem_sinkhorn ? 1 : 0, loss);
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
+apml_status check_finite(const float* p, int64_t n, cudaStream_t s) {
+  std::vector<float> h((size_t)n);
+  CK(cudaMemcpyAsync(h.data(), p, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (float v : h)
+    if (!std::isfinite(v)) return fail(APML_ERR_NONFINITE, "non-finite coordinate in input");
+  return APML_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int apml_abi_version(void) { return APML_ABI_VERSION; }
+
+void apml_config_default(apml_config* c) {
+  if (!c) return;
+  c->p_min = 0.9f;      // DESIGN.md R2 (paper defers to APML)
+  c->tau = 1e-8f;
+  c->l_iter = 10;
+  c->eps_stab = 1e-8f;
+  c->delta = 1e-6f;     // R3
+  c->eps_g = 1e-8f;     // R3
+  c->eps_dist = 1e-8f;  // R3
+  c->grad_mode = APML_GRAD_FULL;
+  c->capacity = 0;
+  c->flags = APML_FLAG_SYNC_CHECK;
+}
+
+const char* apml_last_error(void) { return g_err.c_str(); }
+
+apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
+                         const apml_config* cfg, const apml_allocator* alloc, void* stream,
+                         float* loss, apml_ctx** ctx_out) {
+  if (ctx_out) *ctx_out = nullptr;
+  apml_config c;
+  if (cfg) c = *cfg; else apml_config_default(&c);
+  apml_status st = validate(pred, gt, B, N, M, c);
+  if (st != APML_OK) return st;
+  if (!loss) return fail(APML_ERR_INVALID_ARG, "loss must be a non-NULL device pointer");
+  if (alloc && (!alloc->alloc || !alloc->free)) return fail(APML_ERR_INVALID_ARG, "allocator needs alloc and free");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (c.flags & APML_FLAG_CHECK_FINITE) {
+    if ((st = check_finite(pred, B * N * 3, s)) != APML_OK) return st;
+    if ((st = check_finite(gt, B * M * 3, s)) != APML_OK) return st;
+  }
+  const int64_t per = c.capacity > 0 ? c.capacity : 6;
+  int64_t cap64 = per * (N + M);
+  if (cap64 > N * M) cap64 = N * M;
+  if (cap64 < 1) cap64 = 1;
+  if (cap64 * B > (int64_t)1 << 40 || cap64 >= ((int64_t)1 << 32))
+    return fail(APML_ERR_SHAPE, "emit capacity exceeds 32-bit per-pair positions");
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    apml_ctx* x = new apml_ctx();
+    x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = s;
+    if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
+    const double p = c.p_min;
+    x->lam_r = (float)lambda_K(M, p);
+    x->lam_c = (float)lambda_K(N, p);
+    const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;  // ln(1/tau)
+    x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
+    x->rho_c = N > 1 ? (float)(lt / lambda_K(N, p)) : INFINITY;
+    st = build_ctx(x, (uint32_t)cap64);
+    if (st == APML_OK) st = launch_forward(x, pred, gt, loss);
+    if (st != APML_OK) { apml_ctx_destroy(x); return st; }
+    if (c.flags & APML_FLAG_SYNC_CHECK) {
+      std::vector<unsigned> cnt((size_t)B);
+      cudaError_t e = cudaMemcpyAsync(cnt.data(), x->cursor, sizeof(unsigned) * (size_t)B,
+                                      cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, cudaGetErrorString(e)); }
+      unsigned mx = 0;
+      for (unsigned v : cnt) mx = v > mx ? v : mx;
+      if (mx > x->cap) {
+        apml_ctx_destroy(x);
+        if (attempt == 1) return fail(APML_ERR_CAPACITY, "support exceeded capacity after retry");
+        cap64 = round_up((int64_t)mx + (int64_t)mx / 16 + 16, 64);
+        if (cap64 > N * M) cap64 = N * M;
+        continue;
+      }
+    }
+    st = launch_sparse(x, loss);
+    if (st != APML_OK) { apml_ctx_destroy(x); return st; }
+    if (ctx_out) *ctx_out = x; else apml_ctx_destroy(x);
+    return APML_OK;
+  }
+  return fail(APML_ERR_CAPACITY, "unreachable");
+}
+
+apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred, void* stream) {
+  if (!x) return fail(APML_ERR_STATE, "NULL context");
+  if (x->backward_done) return fail(APML_ERR_STATE, "backward already ran on this context");
+  if (!grad_loss || !grad_pred) return fail(APML_ERR_INVALID_ARG, "grad_loss / grad_pred must be non-NULL");
+  cudaStream_t s = stream ? (cudaStream_t)stream : x->stream;
+  const int B = (int)x->B, N = (int)x->N, M = (int)x->M, L = x->cfg.l_iter;
+  const uint32_t cap = x->cap;
+  const int full = x->cfg.grad_mode == APML_GRAD_FULL;
+  if (s != x->stream) {  // order after the forward's stream
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, x->stream));
+    CK(cudaStreamWaitEvent(s, ev, 0));
+    CK(cudaEventDestroy(ev));
+  }
+  if (full) {
+    k_sinkhorn_bwd<<<B, 1024, x->smem_sinkhorn ? x->smem_bytes : 0, s>>>(N, M, L, x->cfg.eps_stab,
+        x->cursor, cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c,
+        x->cs, x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch,
+        x->smem_sinkhorn ? 1 : 0);
+    k_pbar_rowsoft<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, x->cursor, cap, x->row_ptr,
+        x->csr_jf, x->cs, x->prow, x->a_hist, x->b_hist, x->Rbar, x->Qbar, grad_loss, x->rowB,
+        x->pbar, x->rowback);
+    k_colsoft<<<dim3((M + 255) / 256, B), 256, 0, s>>>(N, M, x->cursor, cap, x->col_ptr,
+        x->csc_perm, x->csr_jf, x->cs, x->pcol, x->pbar, x->colB, x->colback);
+  }
+  k_grad<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, full, x->cfg.eps_dist, x->cursor, cap,
+      x->pred4, x->gt4, x->row_ptr, x->csr_jf, x->cs, x->P0, x->prow, x->pcol, x->pbar, x->a_hist,
+      x->b_hist, grad_loss, x->rowback, x->colback, x->rowidx, x->colidx, grad_pred);
+  CK(cudaGetLastError());
+  x->backward_done = true;
+  return APML_OK;
+}
+
+apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats* out) {
+  if (!x) return fail(APML_ERR_STATE, "NULL context");
+  const int64_t B = x->B;
+  std::vector<unsigned> cur((size_t)B), aux((size_t)B);
+  unsigned long long clamp = 0;
+  CK(cudaMemcpyAsync(cur.data(), x->cursor, sizeof(unsigned) * B, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(aux.data(), x->aux, sizeof(unsigned) * B, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(&clamp, x->clamp, sizeof(clamp), cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaStreamSynchronize(x->stream));
+  apml_stats st{};
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t kept = (int64_t)cur[b] - (int64_t)aux[b];
+    if (nnz_per_pair) nnz_per_pair[b] = kept;
+    st.nnz_total += kept;
+    st.emitted_total += cur[b];
+    if (cur[b] > x->cap) st.overflow_pairs++;
+  }
+  st.clamp_count = (int64_t)clamp;
+  st.capacity = x->cap;
+  st.bytes_ctx = (int64_t)x->bytes;
+  if (out) *out = st;
+  return APML_OK;
+}
+
+apml_status apml_ctx_support(const apml_ctx* x, int64_t b, int64_t* count, int32_t* oi,
+                             int32_t* oj, int32_t* ofl, float* op0, float* ov) {
+  if (!x) return fail(APML_ERR_STATE, "NULL context");
+  if (!count) return fail(APML_ERR_INVALID_ARG, "count must be non-NULL");
+  if (b < 0 || b >= x->B) return fail(APML_ERR_INVALID_ARG, "pair index out of range");
+  const int64_t N = x->N, M = x->M, L = x->cfg.l_iter;
+  unsigned cur = 0;
+  CK(cudaMemcpyAsync(&cur, x->cursor + b, sizeof(unsigned), cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaStreamSynchronize(x->stream));
+  if (cur > x->cap) return fail(APML_ERR_CAPACITY, "pair overflowed its emit capacity");
+  const int64_t cap_in = *count;
+  *count = cur;
+  if (cap_in < (int64_t)cur) return fail(APML_ERR_CAPACITY, "output arrays too small");
+  std::vector<unsigned> rp((size_t)N + 1);
+  std::vector<uint32_t> jf(cur);
+  std::vector<float> p0(cur), ah((size_t)N * (L + 1)), bh((size_t)M * (L + 1));
+  const size_t pb = (size_t)b * x->cap;
+  CK(cudaMemcpyAsync(rp.data(), x->row_ptr + (size_t)b * (N + 1), sizeof(unsigned) * (N + 1), cudaMemcpyDeviceToHost, x->stream));
+  if (cur) {
+    CK(cudaMemcpyAsync(jf.data(), x->csr_jf + pb, sizeof(uint32_t) * cur, cudaMemcpyDeviceToHost, x->stream));
+    CK(cudaMemcpyAsync(p0.data(), x->P0 + pb, sizeof(float) * cur, cudaMemcpyDeviceToHost, x->stream));
+  }
+  CK(cudaMemcpyAsync(ah.data(), x->a_hist + (size_t)b * N * (L + 1), sizeof(float) * ah.size(), cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(bh.data(), x->b_hist + (size_t)b * M * (L + 1), sizeof(float) * bh.size(), cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaStreamSynchronize(x->stream));
+  for (int64_t i = 0; i < N; ++i)
+    for (unsigned p = rp[i]; p < rp[i + 1]; ++p) {
+      const uint32_t j = jf[p] & kIdxMask;
+      if (oi) oi[p] = (int32_t)i;
+      if (oj) oj[p] = (int32_t)j;
+      if (ofl) ofl[p] = ((jf[p] & kFlagRow) ? 1 : 0) | ((jf[p] & kFlagCol) ? 2 : 0);
+      if (op0) op0[p] = p0[p];
+      if (ov) ov[p] = ah[(size_t)i * (L + 1) + L] * p0[p] * bh[(size_t)j * (L + 1) + L];
+    }
+  return APML_OK;
+}
+
+apml_status apml_ctx_lines(const apml_ctx* x, int64_t b, int32_t dir, float* om, float* oc2,
+                           float* oT, int32_t* oa, int32_t* ob) {
+  if (!x) return fail(APML_ERR_STATE, "NULL context");
+  if (b < 0 || b >= x->B || (dir != 0 && dir != 1)) return fail(APML_ERR_INVALID_ARG, "bad pair / direction");
+  const int64_t n = dir ? x->M : x->N;
+  std::vector<LineA> la((size_t)n);
+  std::vector<LineB> lb((size_t)n);
+  std::vector<int2> idx((size_t)n);
+  CK(cudaMemcpyAsync(la.data(), (dir ? x->colA : x->rowA) + (size_t)b * n, sizeof(LineA) * n, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(lb.data(), (dir ? x->colB : x->rowB) + (size_t)b * n, sizeof(LineB) * n, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(idx.data(), (dir ? x->colidx : x->rowidx) + (size_t)b * n, sizeof(int2) * n, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaStreamSynchronize(x->stream));
+  for (int64_t k = 0; k < n; ++k) {
+    if (om) om[k] = lb[k].m;
+    if (oc2) oc2[k] = std::sqrt(la[k].s2);
+    if (oT) oT[k] = lb[k].T;
+    if (oa) oa[k] = idx[k].x;
+    if (ob) ob[k] = idx[k].y;
+  }
+  return APML_OK;
+}
+
+void apml_ctx_destroy(apml_ctx* x) {
+  if (!x) return;
+  ctx_free(x);
+  delete x;
+}
+
+apml_status apml_loss_grad_host(const float* pred_host, const float* gt_host, int64_t B,
+                                int64_t N, int64_t M, const apml_config* cfg,
+                                const apml_allocator* alloc, void* stream, float* loss_host,
+                                float* grad_pred_host) {
+  if (!pred_host || !gt_host || !loss_host || !grad_pred_host)
+    return fail(APML_ERR_INVALID_ARG, "host buffers must be non-NULL");
+  if (B < 1 || N < 1 || M < 1) return fail(APML_ERR_SHAPE, "B, N and M must be >= 1 (EmptyCloud)");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bp = sizeof(float) * (size_t)(B * N * 3), bg = sizeof(float) * (size_t)(B * M * 3);
+  const size_t bl = sizeof(float) * (size_t)B;
+  const size_t total = bp + bg + 2 * bl + bp + 4096;
+  apml_ctx tmp;
+  tmp.stream = s;
+  if (alloc) { tmp.alloc = *alloc; tmp.has_alloc = true; }
+  char* buf = (char*)ctx_alloc(&tmp, total);
+  if (!buf) return fail(APML_ERR_OOM, "allocation failed");
+  tmp.base = buf; tmp.bytes = total;
+  float* d_pred = (float*)buf;
+  float* d_gt = (float*)(buf + round_up(bp, 256));
+  float* d_loss = (float*)(buf + round_up(bp, 256) + round_up(bg, 256));
+  float* d_gl = d_loss + round_up(B, 64);
+  float* d_grad = (float*)((char*)(d_gl + round_up(B, 64)));
+  apml_status st = APML_OK;
+  apml_ctx* ctx = nullptr;
+  std::vector<float> ones((size_t)B, 1.f);
+  cudaError_t e = cudaMemcpyAsync(d_pred, pred_host, bp, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_gt, gt_host, bg, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_gl, ones.data(), bl, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) st = fail(APML_ERR_CUDA, cudaGetErrorString(e));
+  if (st == APML_OK) st = apml_forward(d_pred, d_gt, B, N, M, cfg, alloc, stream, d_loss, &ctx);
+  if (st == APML_OK) st = apml_backward(ctx, d_gl, d_grad, stream);
+  if (st == APML_OK) {
+    e = cudaMemcpyAsync(loss_host, d_loss, bl, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(grad_pred_host, d_grad, bp, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) st = fail(APML_ERR_CUDA, cudaGetErrorString(e));
+  }
+  apml_ctx_destroy(ctx);
+  ctx_free(&tmp);
+  return st;
+}
+
+}  // extern "C"

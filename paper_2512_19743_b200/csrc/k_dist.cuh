@@ -1,0 +1,231 @@
+// k_dist.cuh -- the O(B N M) distance sweeps of the hot path.
+//
+//   k_stage      S0: AoS [B][n][3] -> padded SoA [B][3][np] (sentinel-padded, so the sweeps
+//                    need no bounds checks) + float4 copy [B][n] for the sparse gathers.
+//   k_line_top2  S1 (Pass A): for every owned point, the min and second min (multiset) of
+//                    d2 against all streamed points -- "tracks the minimum and second
+//                    minimum" (Alg. 1).  Launched twice (rows: own = pred,
+//                    stream = gt; columns: roles swapped).  Column range split across
+//                    blockIdx.y; partial (min, second) per split are merged in k_line_info.
+//   k_line_info  S2: merge partials, m = sqrt(m2), c2 = sqrt(s2), g = max(c2 - m + delta,
+//                    eps_g), T = Lambda_K / g (Eq. (1)), kept radius
+//                    R = m + rho_K g with rho_K = ln(1/tau)/Lambda_K, so s >= tau <=> c <= R
+//                     -- no exp / sqrt per pair in the sweeps.
+//   k_emit       S3 (Pass B): recompute d2, keep (i, j) iff d2 <= R_i^2 (row) or d2 <= R'_j^2
+//                    (column), append (i, j | flags) to the pair's segment (P:90 union
+//                    support, "rescans ... writes the kept COO triples").
+//
+// Thread mapping of the sweeps: a CTA of 128 threads owns 128*R points (R per thread, kept
+// in registers as negated packed pairs) and streams the other cloud through shared memory
+// in tiles of kTQ points; per 4 streamed points a thread issues 3 broadcast LDS.128 and, per
+// owned point, 2 x 6 packed FADD2/FMUL2/FFMA2 + 2 x 5 FMNMX(3) -- FP32 / ALU issue bound
+// (DESIGN.md "Roofline").
+#pragma once
+#include "common.cuh"
+
+namespace apml {
+
+constexpr int kSweepThreads = 128;
+constexpr int kTQ = 128;  // streamed points per shared-memory tile
+
+__global__ void k_stage(const float* __restrict__ pts, int n, int np, float sentinel,
+                        float* __restrict__ soa, float4* __restrict__ p4) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= np) return;
+  float x = sentinel, y = sentinel, z = sentinel;
+  if (k < n) {
+    const float* p = pts + ((size_t)b * n + k) * 3;
+    x = p[0]; y = p[1]; z = p[2];
+    p4[(size_t)b * n + k] = make_float4(x, y, z, 0.f);
+  }
+  float* s = soa + (size_t)b * 3 * np;
+  s[k] = x; s[np + k] = y; s[2 * np + k] = z;
+}
+
+// Load one kTQ-point tile of the streamed cloud (SoA) into shared memory.
+__device__ __forceinline__ void load_tile(const float* __restrict__ str, int str_np, int j0,
+                                          float* sx, float* sy, float* sz) {
+  for (int t = threadIdx.x; t < kTQ; t += kSweepThreads) {
+    sx[t] = __ldg(str + j0 + t);
+    sy[t] = __ldg(str + str_np + j0 + t);
+    sz[t] = __ldg(str + 2 * str_np + j0 + t);
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads)
+k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restrict__ str_soa,
+            int str_np, int chunk, int B, float2* __restrict__ part) {
+  const int b = blockIdx.z, split = blockIdx.y;
+  const float* own = own_soa + (size_t)b * 3 * own_np;
+  const float* str = str_soa + (size_t)b * 3 * str_np;
+  const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
+  __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ];
+
+  f2_t nx[R], ny[R], nz[R];
+  float m[R], s[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int idx = base + r * kSweepThreads;
+    const float x = -__ldg(own + idx), y = -__ldg(own + own_np + idx), z = -__ldg(own + 2 * own_np + idx);
+    nx[r] = f2_pack(x, x); ny[r] = f2_pack(y, y); nz[r] = f2_pack(z, z);
+    m[r] = __int_as_float(0x7f800000); s[r] = m[r];
+  }
+  const int j0 = split * chunk, j1 = min(str_np, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTQ) {
+    __syncthreads();
+    load_tile(str, str_np, jt, sx, sy, sz);
+    __syncthreads();
+    const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
+    const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
+    const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
+#pragma unroll 4
+    for (int q = 0; q < kTQ / 4; ++q) {
+      const ulonglong2 qx = px[q], qy = py[q], qz = pz[q];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
+        const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
+        float d0, d1, d2, d3;
+        f2_unpack(d01, d0, d1);
+        f2_unpack(d23, d2, d3);
+        top2_pair(m[r], s[r], d0, d1);
+        top2_pair(m[r], s[r], d2, d3);
+      }
+    }
+  }
+  float2* out = part + ((size_t)split * B + b) * own_np;
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[base + r * kSweepThreads] = make_float2(m[r], s[r]);
+}
+
+// S2: one thread per line.  lam = Lambda_K (fp64 on the host, rounded), rho = ln(1/tau) /
+// Lambda_K (+inf for tau = 0).  K == 1 lines keep their single entry with P = 1.
+__global__ void k_line_info(const float2* __restrict__ part, int S, int B, int own_np, int n,
+                            int K, float lam, float rho, float delta, float eps_g,
+                            LineA* __restrict__ A, LineB* __restrict__ Bo,
+                            unsigned long long* __restrict__ clamp_count) {
+  const int b = blockIdx.y;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  float m2 = __int_as_float(0x7f800000), s2 = m2;
+  for (int sp = 0; sp < S; ++sp) {
+    const float2 p = part[((size_t)sp * B + b) * own_np + k];
+    top2_merge(m2, s2, p.x, p.y);
+  }
+  LineA a;
+  LineB o;
+  const float inf = __int_as_float(0x7f800000);
+  if (K == 1) {
+    a = {m2, inf, inf, inf};
+    o = {__fsqrt_rn(m2), 0.f, 0.f, kLineK1};
+  } else {
+    const float m = __fsqrt_rn(m2), c2 = __fsqrt_rn(s2);
+    float g = __fadd_rn(__fsub_rn(c2, m), delta);       // g = c~(2) + delta
+    int flags = 0;
+    if (g < eps_g) { g = eps_g; flags |= kLineClamped; } // max(gap, eps_g)
+    const float T = __fdiv_rn(lam, g);                   // Eq. (1)
+    const float R = __fadd_rn(m, __fmul_rn(rho, g));     // s >= tau <=> c <= R
+    float R2 = fmaxf(__fmul_rn(R, R), m2);               // the argmin (s = 1) is always kept
+    a = {m2, s2, R2, fmaxf(R2, s2)};
+    o = {m, T, g, flags};
+    if (flags & kLineClamped) atomicAdd(clamp_count, 1ull);
+  }
+  A[(size_t)b * n + k] = a;
+  Bo[(size_t)b * n + k] = o;
+}
+
+// Append one entry to the pair's segment.  Counts keep running past the capacity so the
+// host can size a retry; overflowed pairs are skipped downstream.
+__device__ __forceinline__ void emit_entry(int b, uint32_t i, uint32_t j, uint32_t flags,
+                                           uint32_t cap, uint2* __restrict__ ebuf,
+                                           unsigned* __restrict__ cursor,
+                                           unsigned* __restrict__ aux_cnt,
+                                           unsigned* __restrict__ row_cnt, int N,
+                                           unsigned* __restrict__ col_cnt, int M) {
+  const unsigned pos = atomicAdd(cursor + b, 1u);
+  if (pos < cap) ebuf[(size_t)b * cap + pos] = make_uint2(i, j | flags);
+  atomicAdd(row_cnt + (size_t)b * (N + 1) + i, 1u);
+  atomicAdd(col_cnt + (size_t)b * (M + 1) + j, 1u);
+  if (!flags) atomicAdd(aux_cnt + b, 1u);
+}
+
+// S3 (Pass B).  Rows own pred points; gt streamed with its column radii in shared memory.
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads)
+k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restrict__ rowA,
+       const float* __restrict__ gt_soa, int mp, int M, const LineA* __restrict__ colA,
+       int chunk, uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
+       unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt,
+       unsigned* __restrict__ col_cnt) {
+  const int b = blockIdx.z, split = blockIdx.y;
+  const float* own = pred_soa + (size_t)b * 3 * np;
+  const float* str = gt_soa + (size_t)b * 3 * mp;
+  const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
+  __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ], sR[kTQ], sE[kTQ];
+
+  f2_t nx[R], ny[R], nz[R];
+  float rR2[R], rE2[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int idx = base + r * kSweepThreads;
+    const float x = -__ldg(own + idx), y = -__ldg(own + np + idx), z = -__ldg(own + 2 * np + idx);
+    nx[r] = f2_pack(x, x); ny[r] = f2_pack(y, y); nz[r] = f2_pack(z, z);
+    if (idx < N) {
+      const LineA a = rowA[(size_t)b * N + idx];
+      rR2[r] = a.R2; rE2[r] = a.E2;
+    } else {
+      rR2[r] = -1.f; rE2[r] = -1.f;
+    }
+  }
+  const int j0 = split * chunk, j1 = min(mp, j0 + chunk);
+  for (int jt = j0; jt < j1; jt += kTQ) {
+    __syncthreads();
+    load_tile(str, mp, jt, sx, sy, sz);
+    for (int t = threadIdx.x; t < kTQ; t += kSweepThreads) {
+      const int j = jt + t;
+      if (j < M) {
+        const LineA a = colA[(size_t)b * M + j];
+        sR[t] = a.R2; sE[t] = a.E2;
+      } else {
+        sR[t] = -1.f; sE[t] = -1.f;
+      }
+    }
+    __syncthreads();
+    const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
+    const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
+    const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
+    const float4* pE = reinterpret_cast<const float4*>(sE);
+#pragma unroll 2
+    for (int q = 0; q < kTQ / 4; ++q) {
+      const ulonglong2 qx = px[q], qy = py[q], qz = pz[q];
+      const float4 ce = pE[q];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
+        const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
+        float d[4];
+        f2_unpack(d01, d[0], d[1]);
+        f2_unpack(d23, d[2], d[3]);
+        const bool hit = (d[0] <= fmaxf(rE2[r], ce.x)) | (d[1] <= fmaxf(rE2[r], ce.y)) |
+                         (d[2] <= fmaxf(rE2[r], ce.z)) | (d[3] <= fmaxf(rE2[r], ce.w));
+        if (hit) {  // rare: ~5 kept entries per line out of K
+          const uint32_t i = base + r * kSweepThreads;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int t = 4 * q + c;
+            const uint32_t j = jt + t;
+            const float e = fmaxf(rE2[r], sE[t]);
+            if (d[c] <= e && i < (uint32_t)N && j < (uint32_t)M) {
+              const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= sR[t] ? kFlagCol : 0u);
+              emit_entry(b, i, j, fl, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+}  // namespace apml

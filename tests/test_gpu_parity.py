@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 CPU oracle on the same
+seeded fp32 inputs.  Bars (BASELINE.json north_star):
+  loss          |l_gpu - l_or| / l_or <= 1e-5 per pair
+  support       identical outside the boundary band; direction flags identical too
+  lines         argmin / second argmin identical outside distance ties; T rel 1e-5
+  gradient      normwise <= 1e-4 per pair (full mode: over the well-conditioned set;
+                plan-detached: over all points)
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import OracleConfig, SparsePlan, batch as oracle_batch
+from synth import clouds
+from tests.parity_util import boundary, flags_map, normwise, support_diff, well_conditioned
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 1e-5
+GRAD_RTOL = 1e-4
+
+
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2512_19743_b200 import Config, forward
+    return Config, forward
+
+
+def _ocfg(cfg) -> OracleConfig:
+    return OracleConfig(p_min=cfg.p_min, tau=cfg.tau, l_iter=cfg.l_iter, eps_stab=cfg.eps_stab,
+                        delta=cfg.delta, eps_g=cfg.eps_g, eps_dist=cfg.eps_dist,
+                        grad_mode=0 if cfg.grad_mode == "full" else 1)
+
+
+def _run(x, y, cfg):
+    Config, forward = _gpu()
+    pred = torch.tensor(x, device="cuda")
+    gt = torch.tensor(y, device="cuda")
+    loss, ctx = forward(pred, gt, cfg)
+    g = ctx.backward(torch.ones(x.shape[0], device="cuda"))
+    torch.cuda.synchronize()
+    return loss.cpu().numpy().astype(np.float64), g.cpu().numpy().astype(np.float64), ctx
+
+
+def _check_pair(x, y, cfg, loss_g, grad_g, ctx, b, check_grad=True):
+    oc = _ocfg(cfg)
+    plan = SparsePlan(x[b], y[b], oc)
+    rel = abs(loss_g[b] - plan.loss) / abs(plan.loss) if plan.loss != 0 else abs(loss_g[b])
+    assert rel <= LOSS_RTOL, f"pair {b}: loss {loss_g[b]} vs oracle {plan.loss} (rel {rel:.3e})"
+    # support and flags
+    gs = ctx.support(b)
+    os_ = plan.support()
+    only_g, only_o = support_diff(gs, os_)
+    bad = [e for e in only_g | only_o if not boundary(x[b], y[b], plan, e[0], e[1], oc)]
+    assert not bad, f"pair {b}: {len(bad)} support entries differ outside the band: {sorted(bad)[:5]}"
+    fg, fo = flags_map(gs), flags_map(os_)
+    badf = [k for k in fo if k in fg and fg[k] != fo[k] and not boundary(x[b], y[b], plan, k[0], k[1], oc)]
+    assert not badf, f"pair {b}: flags differ at {badf[:5]}"
+    # per-line statistics
+    for d in (0, 1):
+        gl, ol = ctx.lines(b, d), plan.lines(d)
+        K = y.shape[1] if d == 0 else x.shape[1]
+        np.testing.assert_allclose(gl["m"], ol["m"], rtol=1e-6, atol=1e-7)
+        if K > 1:
+            np.testing.assert_allclose(gl["c2"], ol["c2"], rtol=1e-6, atol=1e-7)
+            u = 2.0 ** -24
+            tie = np.abs(ol["c2"] - ol["m"]) <= 8 * u * np.maximum(ol["c2"], 1e-30)
+            np.testing.assert_array_equal(gl["a"][~tie], ol["a"][~tie])
+            # T = Lambda / g with g = c2 - m + delta: fp32 error of g is ~ u (m + c2)
+            tol = 1e-5 + 8 * u * (ol["m"] + ol["c2"]) / ol["g"]
+            relT = np.abs(gl["T"] - ol["T"]) / np.abs(ol["T"])
+            assert np.all(relT <= tol), f"T mismatch, worst {relT.max():.3e}"
+    if not check_grad:
+        return
+    gx, _ = plan.backward(1.0)
+    if cfg.grad_mode == "full":
+        mask = well_conditioned(x[b], y[b], plan, oc)
+        assert mask.mean() > 0.9
+        e = normwise(grad_g[b][mask], gx[mask])
+    else:
+        e = normwise(grad_g[b], gx)
+    assert e <= GRAD_RTOL, f"pair {b}: grad normwise error {e:.3e} ({cfg.grad_mode})"
+
+
+CASES = [
+    # kind, B, N, M, p_min, tau, seed
+    ("uniform", 1, 64, 64, 0.9, 1e-8, 0),           # C1
+    ("shapenet", 1, 64, 64, 0.9, 1e-8, 1),          # C1
+    ("uniform", 3, 300, 300, 0.9, 1e-8, 2),         # ragged vs 512-point tiles
+    ("shapenet", 2, 700, 333, 0.8, 1e-8, 3),        # N != M, ragged
+    ("mmfi", 2, 512, 1024, 0.9, 1e-8, 4),           # N < M: long rows
+    ("mmfi", 2, 1024, 256, 0.9, 1e-8, 5),           # N > M
+    ("near", 2, 600, 600, 0.9, 1e-8, 6),            # near-converged
+    ("uniform", 2, 200, 150, 0.5, 1e-8, 7),         # flatter softmax
+    ("uniform", 2, 257, 129, 0.9, 1e-4, 8),         # argmin-only regime (tau > tau*), R14
+    ("uniform", 1, 96, 80, 0.9, 0.0, 9),            # tau = 0: full support (capacity retry)
+    ("scene", 1, 1500, 1200, 0.95, 1e-8, 10),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-B{c[1]}-{c[2]}x{c[3]}-p{c[4]}-t{c[5]}")
+@pytest.mark.parametrize("mode", ["full", "plan_detached"])
+def test_parity_cases(case, mode):
+    Config, _ = _gpu()
+    kind, B, N, M, p, tau, seed = case
+    x, y = clouds.batch(kind, B, N, M, seed)
+    cfg = Config(p_min=p, tau=tau, grad_mode=mode)
+    lg, gg, ctx = _run(x, y, cfg)
+    for b in range(B):
+        _check_pair(x, y, cfg, lg, gg, ctx, b)
+
+
+@pytest.mark.parametrize("NM", [(1, 1), (1, 37), (41, 1), (2, 2), (3, 700)])
+def test_degenerate_shapes(NM):
+    """K = 1 lines (P = 1, R4), tiny clouds, single pair."""
+    Config, _ = _gpu()
+    N, M = NM
+    x, y = clouds.batch("uniform", 2, N, M, 11)
+    cfg = Config()
+    lg, gg, ctx = _run(x, y, cfg)
+    for b in range(2):
+        plan = SparsePlan(x[b], y[b], _ocfg(cfg))
+        assert abs(lg[b] - plan.loss) <= LOSS_RTOL * abs(plan.loss)
+        gx, _ = plan.backward()
+        assert normwise(gg[b], gx) <= GRAD_RTOL
+
+
+def test_ties_duplicates_and_coincident_points():
+    """Duplicated gt points (multiset second min = min, R5), coincident pred/gt points
+    (d = 0, Eq. (5) eps_dist), gap clamp active when delta < eps_g."""
+    Config, _ = _gpu()
+    rng = np.random.default_rng(0)
+    y = rng.uniform(size=(1, 200, 3)).astype(np.float32)
+    y[0, 100:150] = y[0, 0:50]                                  # duplicates
+    x = rng.uniform(size=(1, 180, 3)).astype(np.float32)
+    x[0, :30] = y[0, 60:90]                                     # coincident
+    for cfg in (Config(), Config(delta=0.0, eps_g=1e-6)):
+        lg, gg, ctx = _run(x, y, cfg)
+        plan = SparsePlan(x[0], y[0], _ocfg(cfg))
+        assert abs(lg[0] - plan.loss) <= LOSS_RTOL * plan.loss
+        assert ctx.stats()["nnz_total"] == plan.nnz
+
+
+def test_capacity_retry_and_overflow_reporting():
+    """Capacity too small: with sync_check the library retries exactly; without it the
+    overflowed pairs report NaN loss and are counted (no silent truncation)."""
+    Config, forward = _gpu()
+    x, y = clouds.batch("uniform", 3, 400, 300, 12)
+    ref, _, _ = _run(x, y, Config())
+    small, _, ctx = _run(x, y, Config(capacity=1))
+    np.testing.assert_array_equal(small, ref)
+    assert ctx.stats()["overflow_pairs"] == 0
+    pred, gt = torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda")
+    loss, ctx = forward(pred, gt, Config(capacity=1, sync_check=False))
+    st = ctx.stats()
+    assert st["overflow_pairs"] == 3 and torch.isnan(loss).all()
+
+
+def test_determinism_and_batch_independence():
+    """Bitwise-identical results across runs and independent of the batch a pair sits in."""
+    x, y = clouds.batch("shapenet", 4, 1000, 900, 13)
+    Config, _ = _gpu()
+    l1, g1, _ = _run(x, y, Config())
+    l2, g2, _ = _run(x, y, Config())
+    np.testing.assert_array_equal(l1, l2)
+    np.testing.assert_array_equal(g1, g2)
+    l3, g3, _ = _run(x[2:3], y[2:3], Config())
+    np.testing.assert_array_equal(l3[0], l1[2])
+    np.testing.assert_array_equal(g3[0], g1[2])
+
+
+def test_host_entry_point_matches_device_path():
+    from paper_2512_19743_b200 import loss_grad_host
+    Config, _ = _gpu()
+    x, y = clouds.batch("mmfi", 3, 512, 256, 14)
+    l1, g1, _ = _run(x, y, Config())
+    l2, g2 = loss_grad_host(torch.tensor(x).pin_memory(), torch.tensor(y).pin_memory(), Config())
+    np.testing.assert_array_equal(l2.numpy(), l1.astype(np.float32))
+    np.testing.assert_array_equal(g2.numpy(), g1.astype(np.float32))
+
+
+def test_autograd_function_and_state_errors():
+    from paper_2512_19743_b200 import apml_loss
+    from paper_2512_19743_b200._lib import ApmlError
+    Config, forward = _gpu()
+    x, y = clouds.batch("uniform", 2, 128, 100, 15)
+    pred = torch.tensor(x, device="cuda", requires_grad=True)
+    gt = torch.tensor(y, device="cuda")
+    apml_loss(pred, gt, reduction="mean").backward()
+    l, g, _ = _run(x, y, Config())
+    np.testing.assert_allclose(pred.grad.cpu().numpy(), g / 2, rtol=1e-6, atol=1e-9)
+    loss, ctx = forward(pred.detach(), gt)
+    ctx.backward(torch.ones(2, device="cuda"))
+    with pytest.raises(ApmlError):
+        ctx.backward(torch.ones(2, device="cuda"))
+
+
+# ------------------------------------------------------------ BASELINE.json full sizes
+def _full_size(kind, B, N, M, sample, seed, grad=True):
+    Config, _ = _gpu()
+    x, y = clouds.batch(kind, B, N, M, seed)
+    cfg = Config(sync_check=False)  # the launch configuration bench.py times
+    lg, gg, ctx = _run(x, y, cfg)
+    st = ctx.stats()
+    assert st["overflow_pairs"] == 0
+    xs, ys = x[sample], y[sample]
+    ol, og, onnz, _ = oracle_batch(xs, ys, _ocfg(cfg), want_grad=grad)
+    rel = np.abs(lg[sample] - ol) / np.abs(ol)
+    assert rel.max() <= LOSS_RTOL, f"loss rel {rel.max():.3e}"
+    nnz_g = np.asarray(st["nnz"])[sample]
+    assert np.all(np.abs(nnz_g - onnz) <= 8), f"nnz {nnz_g} vs {onnz}"
+    if grad:
+        for k, b in enumerate(sample):
+            plan = None
+            e = normwise(gg[b], og[k])
+            if e > GRAD_RTOL:  # restrict to the well-conditioned set
+                plan = SparsePlan(x[b], y[b], _ocfg(cfg))
+                mask = well_conditioned(x[b], y[b], plan, _ocfg(cfg))
+                e = normwise(gg[b][mask], og[k][mask])
+            assert e <= GRAD_RTOL, f"pair {b}: grad {e:.3e}"
+
+
+def test_full_size_C2_shapenet_all_pairs():
+    """configs[1]: ShapeNet-55-shaped B = 32, N = M = 2048 -- every pair against the oracle."""
+    _full_size("shapenet", 32, 2048, 2048, list(range(32)), seed=100)
+
+
+def test_full_size_C3_mmfi_sampled():
+    """configs[2]: MM-Fi-shaped B = 512, (N, M) = (1024, 512); sampled pairs."""
+    _full_size("mmfi", 512, 1024, 512, [0, 1, 255, 510, 511], seed=200)
+
+
+def test_full_size_C4_pcn_sampled():
+    """configs[3] per-GPU shard at 1 GPU: B = 64, N = M = 16384; sampled pairs (loss + nnz)."""
+    _full_size("shapenet", 64, 16384, 16384, [0, 63], seed=300, grad=False)
