@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse APML hot path (fwd + bwd) -- driver contract in DESIGN.md "Bench".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one batch: forward (S0-S7) + full-mode
+backward (S8) through the C ABI, plus (N > 1) the NCCL all-reduce of the loss.  Batch
+sharding is weak scaling: every rank owns its own B pairs (seed offset by rank).  The JSON
+line reports pairs/s of the whole job, per-stage device times, the roofline of the dominant
+kernel, the oracle on the host cores (cpu_baseline), an end-to-end number through the host
+entry point (apml_loss_grad_host, copies included) and the SM clocks seen while timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs (tau = 1e-8, L_iter = 10 for all)
+CONFIGS = {
+    "C1": dict(B=1, N=64, M=64, kind="uniform", workload="C1 parity: B=1, N=M=64"),
+    "C2": dict(B=32, N=2048, M=2048, kind="shapenet",
+               workload="C2 ShapeNet-55-shaped: B=32, N=M=2048 (FoldingNet-style step)"),
+    "C3": dict(B=512, N=1024, M=512, kind="mmfi",
+               workload="C3 MM-Fi-shaped: B=512, N=1024, M=512 (N != M)"),
+    "C4": dict(B=64, N=16384, M=16384, kind="shapenet",
+               workload="C4 PCN-shaped: B=64, N=M=16384 (per-GPU batch at weak scaling)"),
+    "C5": dict(B=1, N=262144, M=262144, kind="scene",
+               workload="C5 scene: B=1, N=M=262144 (single GPU, unsharded)"),
+}
+METRIC = "point-cloud pairs/sec fwd+bwd"
+LANE_OPS_PER_EVAL = 6  # d2 = 3 sub + 1 mul + 2 fma FP32 lane-ops per (i, j) per sweep
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2] not in ("", "[N/A]"))}
+
+
+def cpu_baseline(cfg_name: str, seed: int, budget_s: float = 15.0) -> dict:
+    """The fp64 oracle as it stands (OpenMP over pairs) on a bounded sample of the workload."""
+    from oracle import OracleConfig, batch as oracle_batch
+    from synth import clouds
+    c = CONFIGS[cfg_name]
+    cores = os.cpu_count() or 1
+    n = max(1, min(c["B"], cores))
+    x, y = clouds.batch(c["kind"], n, c["N"], c["M"], seed)
+    t0 = time.perf_counter()
+    _, _, _, used = oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
+    dt = time.perf_counter() - t0
+    done, reps = n, 1
+    while time.perf_counter() - t0 + dt < budget_s and reps < 64:
+        oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
+        done += n
+        reps += 1
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "pairs/s", "cores": used, "kind": "oracle",
+            "sample": f"{reps} x {n} pairs of {cfg_name} ({c['kind']}, N={c['N']}, M={c['M']}), fwd+full bwd, fp64, {el:.1f} s"}
+
+
+def run_reference(args) -> None:
+    """--impl reference: the oracle timed on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import OracleConfig, batch as oracle_batch
+    from synth import clouds
+    c = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    n = max(1, min(c["B"], cores))
+    x, y = clouds.batch(c["kind"], n, c["N"], c["M"], args.seed)
+    for _ in range(args.warmup):
+        oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
+    t0 = time.perf_counter()
+    used = 1
+    for _ in range(args.steps):
+        _, _, _, used = oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
+    el = time.perf_counter() - t0
+    val = n * args.steps / el
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "pairs/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": c["workload"], "B": c["B"], "N": c["N"], "M": c["M"],
+                                           "kind": c["kind"], "step_sample_pairs": n},
+           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": used, "kind": "oracle",
+                            "sample": f"{n} pairs of {args.config} per step (bounded sample), fwd+full bwd, fp64"},
+           "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--grad-mode", default="full", choices=["full", "plan_detached"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_19743_b200 import Config, forward, loss_grad_host
+    from synth import clouds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS[args.config]
+    B, N, M = c["B"], c["N"], c["M"]
+    x, y = clouds.batch(c["kind"], B, N, M, args.seed + 1000 * rank)
+    pred = torch.tensor(x, device=dev)
+    gt = torch.tensor(y, device=dev)
+    ones = torch.ones(B, device=dev)
+    loss_buf = torch.empty(B, device=dev)
+    grad_buf = torch.empty(B, N, 3, device=dev)
+    cfg = Config(grad_mode=args.grad_mode, sync_check=False, stage_timing=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def step():
+        loss, ctx = forward(pred, gt, cfg, loss_out=loss_buf)
+        ctx.backward(ones, out=grad_buf)
+        if world > 1:
+            tot = loss.sum()
+            dist.all_reduce(tot)  # X1: NCCL loss all-reduce (batch sharding)
+        return ctx
+
+    for _ in range(args.warmup):
+        step().close()
+    torch.cuda.synchronize()
+    st0 = None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.reset_peak_memory_stats(dev)
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stages, launches, prev = [], 0, None
+    t_wall = time.perf_counter()
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)  # evict L2 between timed steps (not inside the step bracket)
+        evs[k][0].record()
+        ctx = step()
+        evs[k][1].record()
+        if prev is not None:
+            stages.append(prev.stage_times()); launches += prev.stats()["launches"]; prev.close()
+        prev = ctx
+    stages.append(prev.stage_times()); st0 = prev.stats(); launches += st0["launches"]; prev.close()
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = float(sum(step_ms))
+    peak_gb = torch.cuda.max_memory_allocated(dev) / 1e9
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    value = B * world / (ms_per_step / 1e3)
+
+    # per-stage medians and the roofline of the dominant kernel
+    keys = list(stages[0].keys())
+    med = {k: float(np.median([s[k] for s in stages])) for k in keys}
+    peaks = _peaks()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    alu_peak = sms * 128 * f_max / 1e12  # FP32 lane-ops/s (FMA = 1), DESIGN.md "Roofline"
+    evals = B * N * M
+    dist_stages = ("passA_rows", "passA_cols", "emit")
+    nnz = st0["nnz_total"]
+    L = cfg.l_iter
+    sparse_bytes = {  # algorithmic bytes per launch (SURVEY 8(d) per-entry figures x nnz)
+        "sinkhorn": nnz * (16 * L + 12),
+        "bwd_sinkhorn": nnz * (16 * L + 24),
+        "bwd_softmax": nnz * 44,
+        "bwd_grad": nnz * 12,
+        "norm": nnz * 48,
+        "csr": nnz * 20,
+    }
+    dom = max(med, key=med.get)
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = tr.get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    if dom in dist_stages:
+        ach = LANE_OPS_PER_EVAL * evals / (med[dom] / 1e3) / 1e12
+        roof = {"bound": "alu", "kernel": f"k_line_top2/k_emit ({dom})", "achieved": ach, "peak": alu_peak,
+                "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": traffic,
+                "note": "FP32 lane-op roofline (FMA counted once): 148 SM x 128 lanes x sm_max clock"}
+    else:
+        byt = sparse_bytes.get(dom, 0)
+        ach = byt / (med[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": ach / peaks.get("hbm_gbs", 6544.7), "traffic": traffic,
+                "note": "algorithmic bytes = SURVEY 8(d) per-entry figure x nnz"}
+    dist_ms = sum(med[k] for k in dist_stages)
+    roof_dist = {"bound": "alu", "achieved": LANE_OPS_PER_EVAL * 3 * evals / (dist_ms / 1e3) / 1e12,
+                 "peak": alu_peak, "unit": "TFLOP/s", "sweeps": 3, "ms": dist_ms}
+    roof_dist["frac"] = roof_dist["achieved"] / alu_peak
+    roof_dist["frac_vs_2sweep_algorithm"] = LANE_OPS_PER_EVAL * 2 * evals / (dist_ms / 1e3) / 1e12 / alu_peak
+
+    # end to end through the host entry point (pinned host buffers; copies inside the bracket)
+    e2e = None
+    if not args.no_e2e:
+        ph = torch.tensor(x).pin_memory()
+        gh = torch.tensor(y).pin_memory()
+        lo = torch.empty(B, pin_memory=True)
+        go = torch.empty(B, N, 3, pin_memory=True)
+        hcfg = Config(grad_mode=args.grad_mode, sync_check=False)
+        for _ in range(2):
+            loss_grad_host(ph, gh, hcfg, lo, go, device=local)
+        ke = max(3, min(args.steps, 20))
+        acc = 0.0
+        for _ in range(ke):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            loss_grad_host(ph, gh, hcfg, lo, go, device=local)  # synchronises before returning
+            acc += (time.perf_counter() - t0) * 1e3
+        e2e_ms = acc / ke
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": B * world / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 4 * B * 3 * (N + M), "d2h_bytes_per_step": 4 * B + 4 * B * N * 3,
+               "api": "apml_loss_grad_host (host fp32 in, host loss + grad out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, args.seed)
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": c["workload"], "B": B, "N": N, "M": M, "kind": c["kind"], "tau": cfg.tau,
+                       "l_iter": cfg.l_iter, "p_min": cfg.p_min, "grad_mode": args.grad_mode,
+                       "global_batch": B * world, "parallelism": f"batch-shard dp{world}" +
+                       (" + NCCL loss all-reduce" if world > 1 else ""),
+                       "l2": "flushed between timed steps (256 MiB write outside the step bracket)"},
+            "roofline": roof, "roofline_distance_pass": roof_dist,
+            "stages_ms": med, "nnz_per_pair": nnz / B, "peak_gb": peak_gb,
+            "dense_lower_bound_gb": 8 * B * N * M / 1e9,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
+            "wall_s_timed": t_wall, "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,24 @@ typedef enum {
                                      sync-free / graph-capturable and an overflowed pair gets
                                      a NaN loss (reported by apml_ctx_stats). */
 #define APML_FLAG_CHECK_FINITE 2u /* scan the inputs for NaN/Inf first (one extra pass + sync) */
+#define APML_FLAG_STAGE_TIMING 4u /* record CUDA events between the stages below (on the launch
+                                     stream); read them with apml_ctx_stage_times */
+
+/* Stages timed with APML_FLAG_STAGE_TIMING (indices into apml_ctx_stage_times' output). */
+enum {
+    APML_STAGE_STAGING = 0,     /* S0: AoS -> padded SoA + float4 copies */
+    APML_STAGE_PASSA_ROWS = 1,  /* S1: row min / second min sweep (k_line_top2, B N M pairs) */
+    APML_STAGE_PASSA_COLS = 2,  /* S1: column min / second min sweep (k_line_top2, B N M pairs) */
+    APML_STAGE_LINE_INFO = 3,   /* S2: line constants */
+    APML_STAGE_EMIT = 4,        /* S3: emit sweep (k_emit, B N M pairs) */
+    APML_STAGE_CSR = 5,         /* S4: scan, scatter, sort -> CSR / CSC */
+    APML_STAGE_NORM = 6,        /* S5: directional normalisation + symmetrisation */
+    APML_STAGE_SINKHORN = 7,    /* S6 + S7: Sinkhorn and loss */
+    APML_STAGE_BWD_SINKHORN = 8,/* S8: Sinkhorn reverse (full mode) */
+    APML_STAGE_BWD_SOFTMAX = 9, /* S8: P0bar + row / column softmax reverse (full mode) */
+    APML_STAGE_BWD_GRAD = 10,   /* S8: cbar + Eq. (5) scatter */
+    APML_NUM_STAGES = 11
+};
 
 typedef struct {
     float   p_min;        /* Eq. (1); 0 < p_min < 1 and p_min > 1/K for every line
@@ -109,6 +127,7 @@ typedef struct {
     int64_t capacity;       /* emit capacity per pair actually used (entries) */
     int64_t overflow_pairs; /* pairs whose support exceeded capacity (their loss is NaN) */
     int64_t bytes_ctx;      /* device bytes owned by the context */
+    int64_t launches;       /* kernels launched so far by this context (forward + backward) */
 } apml_stats;
 
 typedef struct apml_ctx apml_ctx; /* opaque: state saved by forward for backward */
@@ -153,6 +172,10 @@ APML_API apml_status apml_ctx_support(const apml_ctx* ctx, int64_t b, int64_t* c
  * Any pointer may be NULL. */
 APML_API apml_status apml_ctx_lines(const apml_ctx* ctx, int64_t b, int32_t dir, float* m,
                                     float* c2, float* T, int32_t* argmin, int32_t* second);
+
+/* Per-stage device durations in milliseconds (ms[APML_NUM_STAGES]; stages not run are 0)
+ * for a context created with APML_FLAG_STAGE_TIMING.  SYNCHRONISES on the last event. */
+APML_API apml_status apml_ctx_stage_times(const apml_ctx* ctx, float* ms, int32_t n);
 
 /* Release a context (stream-ordered free on the context's stream).  NULL is a no-op. */
 APML_API void apml_ctx_destroy(apml_ctx* ctx);

@@ -16,11 +16,14 @@ APML_OK, APML_ERR_INVALID_ARG, APML_ERR_SHAPE, APML_ERR_NONFINITE, APML_ERR_CAPA
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NONFINITE", 4: "CAPACITY", 5: "CUDA",
                 6: "OOM", 7: "STATE"}
 APML_GRAD_FULL, APML_GRAD_PLAN_DETACHED = 0, 1
-APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE = 1, 2
+APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE, APML_FLAG_STAGE_TIMING = 1, 2, 4
+STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "csr", "norm", "sinkhorn",
+          "bwd_sinkhorn", "bwd_softmax", "bwd_grad")
 
 # exported symbols declared in include/apml.h (checked by tests/test_abi.py)
 EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_backward",
-           "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_destroy",
+           "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
+           "apml_ctx_destroy",
            "apml_loss_grad_host", "apml_last_error")
 
 
@@ -41,7 +44,8 @@ class ApmlAllocator(C.Structure):
 
 class ApmlStats(C.Structure):
     _fields_ = [("nnz_total", C.c_int64), ("emitted_total", C.c_int64), ("clamp_count", C.c_int64),
-                ("capacity", C.c_int64), ("overflow_pairs", C.c_int64), ("bytes_ctx", C.c_int64)]
+                ("capacity", C.c_int64), ("overflow_pairs", C.c_int64), ("bytes_ctx", C.c_int64),
+                ("launches", C.c_int64)]
 
 
 class ApmlError(RuntimeError):
@@ -77,6 +81,8 @@ def lib() -> C.CDLL:
         L.apml_ctx_support.argtypes = [vp, i64, C.POINTER(C.c_int64), vp, vp, vp, vp, vp]
         L.apml_ctx_lines.restype = C.c_int
         L.apml_ctx_lines.argtypes = [vp, i64, C.c_int32, vp, vp, vp, vp, vp]
+        L.apml_ctx_stage_times.restype = C.c_int
+        L.apml_ctx_stage_times.argtypes = [vp, vp, C.c_int32]
         L.apml_ctx_destroy.restype = None
         L.apml_ctx_destroy.argtypes = [vp]
         L.apml_loss_grad_host.restype = C.c_int

@@ -31,12 +31,14 @@ class Config:
     capacity: int = 0                # entries per point per pair; 0 = library default
     sync_check: bool = True          # read back support counts and retry on overflow
     check_finite: bool = False
+    stage_timing: bool = False       # CUDA events between stages (apml_ctx_stage_times)
 
     def to_c(self) -> A.ApmlConfig:
         if self.grad_mode not in ("full", "plan_detached"):
             raise ValueError(f"grad_mode must be 'full' or 'plan_detached', got {self.grad_mode!r}")
         flags = (A.APML_FLAG_SYNC_CHECK if self.sync_check else 0) | \
-            (A.APML_FLAG_CHECK_FINITE if self.check_finite else 0)
+            (A.APML_FLAG_CHECK_FINITE if self.check_finite else 0) | \
+            (A.APML_FLAG_STAGE_TIMING if self.stage_timing else 0)
         return A.ApmlConfig(self.p_min, self.tau, self.l_iter, self.eps_stab, self.delta, self.eps_g,
                             self.eps_dist, A.APML_GRAD_FULL if self.grad_mode == "full"
                             else A.APML_GRAD_PLAN_DETACHED, self.capacity, flags)
@@ -75,7 +77,13 @@ class Context:
         A.check(A.lib().apml_ctx_stats(self._h, C.cast(nnz, C.c_void_p), C.byref(st)))
         return dict(nnz=list(nnz), nnz_total=st.nnz_total, emitted_total=st.emitted_total,
                     clamp_count=st.clamp_count, capacity=st.capacity,
-                    overflow_pairs=st.overflow_pairs, bytes_ctx=st.bytes_ctx)
+                    overflow_pairs=st.overflow_pairs, bytes_ctx=st.bytes_ctx, launches=st.launches)
+
+    def stage_times(self) -> dict:
+        """Per-stage device milliseconds (needs Config(stage_timing=True)); synchronises."""
+        ms = (C.c_float * len(A.STAGES))()
+        A.check(A.lib().apml_ctx_stage_times(self._h, C.cast(ms, C.c_void_p), len(A.STAGES)))
+        return dict(zip(A.STAGES, list(ms)))
 
     def support(self, b: int) -> dict:
         """apml_ctx_support for pair b (synchronises): CSR-ordered i, j, flags, P0, v."""

@@ -58,6 +58,10 @@ struct apml_ctx {
   uint32_t cap = 0;
   int S_rows = 1, S_cols = 1, chunk_rows = 0, chunk_cols = 0;
   bool backward_done = false;
+  bool timing = false;
+  bool bwd_timed = false;
+  cudaEvent_t ev[13] = {};  // 0..8 forward stage boundaries, 9 backward start, 10..12 ends
+  int64_t launches = 0;
   bool smem_sinkhorn = false;
   size_t smem_bytes = 0;
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
@@ -84,7 +88,13 @@ void* ctx_alloc(apml_ctx* c, size_t bytes) {
   return p;
 }
 
+void mark(apml_ctx* c, int k, cudaStream_t s) {
+  if (c->timing) cudaEventRecord(c->ev[k], s);
+}
+
 void ctx_free(apml_ctx* c) {
+  for (auto& e : c->ev)
+    if (e) { cudaEventDestroy(e); e = nullptr; }
   if (!c->base) return;
   if (c->has_alloc) c->alloc.free(c->base, c->bytes, c->stream, c->alloc.user);
   else cudaFreeAsync(c->base, c->stream);
@@ -205,23 +215,30 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt, floa
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   (void)loss;
+  mark(c, 0, s);
   // S0 staging
   k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
   k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
+  mark(c, 1, s);
   // S1 Pass A: rows (own pred, stream gt) and columns (own gt, stream pred)
   k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
       c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
+  mark(c, 2, s);
   k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
       c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
+  mark(c, 3, s);
   // S2 line constants
   k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
       c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
   k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, N, c->lam_c,
       c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+  mark(c, 4, s);
   // S3 Pass B emit
   k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
       c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
       c->aux, c->row_cnt, c->col_cnt);
+  mark(c, 5, s);
+  c->launches += 7;
   CK(cudaGetLastError());
   return APML_OK;
 }
@@ -240,16 +257,20 @@ apml_status launch_sparse(apml_ctx* c, float* loss) {
       c->csr_t, c->csr_jf, c->inv, nullptr);
   k_sort_lines<false><<<dim3((M + 7) / 8, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, M, c->col_ptr,
       c->csc_t, c->csc_i, c->inv, c->csc_perm);
+  mark(c, 6, s);
   // S5 normalisation + symmetrisation
   k_row_norm<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->pred4, c->gt4, N, M, c->cursor, cap,
       c->row_ptr, c->csr_jf, c->rowA, c->rowB, c->d2s, c->cs, c->prow, c->rowidx);
   k_col_norm<<<dim3((M + 255) / 256, B), 256, 0, s>>>(N, M, c->cursor, cap, c->col_ptr, c->csc_i,
       c->csc_perm, c->csr_jf, c->colA, c->colB, c->d2s, c->cs, c->prow, c->pcol, c->P0, c->P0c,
       c->colidx);
+  mark(c, 7, s);
   // S6 + S7 Sinkhorn and loss
   k_sinkhorn<<<B, 1024, c->smem_sinkhorn ? c->smem_bytes : 0, s>>>(N, M, L, c->cfg.eps_stab,
       c->cursor, cap, c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist,
       c->b_hist, c->gscratch, c->smem_sinkhorn ? 1 : 0, loss);
+  mark(c, 8, s);
+  c->launches += 8;
   CK(cudaGetLastError());
   return APML_OK;
 }
@@ -310,6 +331,11 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
     apml_ctx* x = new apml_ctx();
     x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = s;
     if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
+    if (c.flags & APML_FLAG_STAGE_TIMING) {
+      x->timing = true;
+      for (auto& e : x->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, "cudaEventCreate"); }
+    }
     const double p = c.p_min;
     x->lam_r = (float)lambda_K(M, p);
     x->lam_c = (float)lambda_K(N, p);
@@ -358,20 +384,30 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
     CK(cudaStreamWaitEvent(s, ev, 0));
     CK(cudaEventDestroy(ev));
   }
+  mark(x, 9, s);
+  x->bwd_timed = x->timing;
   if (full) {
     k_sinkhorn_bwd<<<B, 1024, x->smem_sinkhorn ? x->smem_bytes : 0, s>>>(N, M, L, x->cfg.eps_stab,
         x->cursor, cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c,
         x->cs, x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch,
         x->smem_sinkhorn ? 1 : 0);
+    mark(x, 10, s);
     k_pbar_rowsoft<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, x->cursor, cap, x->row_ptr,
         x->csr_jf, x->cs, x->prow, x->a_hist, x->b_hist, x->Rbar, x->Qbar, grad_loss, x->rowB,
         x->pbar, x->rowback);
     k_colsoft<<<dim3((M + 255) / 256, B), 256, 0, s>>>(N, M, x->cursor, cap, x->col_ptr,
         x->csc_perm, x->csr_jf, x->cs, x->pcol, x->pbar, x->colB, x->colback);
+    mark(x, 11, s);
+    x->launches += 3;
+  } else {
+    mark(x, 10, s);
+    mark(x, 11, s);
   }
   k_grad<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, full, x->cfg.eps_dist, x->cursor, cap,
       x->pred4, x->gt4, x->row_ptr, x->csr_jf, x->cs, x->P0, x->prow, x->pcol, x->pbar, x->a_hist,
       x->b_hist, grad_loss, x->rowback, x->colback, x->rowidx, x->colidx, grad_pred);
+  mark(x, 12, s);
+  x->launches += 1;
   CK(cudaGetLastError());
   x->backward_done = true;
   return APML_OK;
@@ -397,6 +433,7 @@ apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats*
   st.clamp_count = (int64_t)clamp;
   st.capacity = x->cap;
   st.bytes_ctx = (int64_t)x->bytes;
+  st.launches = x->launches;
   if (out) *out = st;
   return APML_OK;
 }
@@ -457,6 +494,18 @@ apml_status apml_ctx_lines(const apml_ctx* x, int64_t b, int32_t dir, float* om,
     if (oa) oa[k] = idx[k].x;
     if (ob) ob[k] = idx[k].y;
   }
+  return APML_OK;
+}
+
+apml_status apml_ctx_stage_times(const apml_ctx* x, float* ms, int32_t n) {
+  if (!x) return fail(APML_ERR_STATE, "NULL context");
+  if (!x->timing) return fail(APML_ERR_STATE, "context was created without APML_FLAG_STAGE_TIMING");
+  if (!ms || n < APML_NUM_STAGES) return fail(APML_ERR_INVALID_ARG, "ms must hold APML_NUM_STAGES floats");
+  for (int k = 0; k < APML_NUM_STAGES; ++k) ms[k] = 0.f;
+  CK(cudaEventSynchronize(x->ev[x->bwd_timed ? 12 : 8]));
+  for (int k = 0; k < 8; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k], x->ev[k + 1]));
+  if (x->bwd_timed)
+    for (int k = 8; k < 11; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k + 1], x->ev[k + 2]));
   return APML_OK;
 }
 
