@@ -1,5 +1,6 @@
 // apml_capi.cu -- host side of libapml.so: validation, context / workspace, launch sequence.
 // Declarations and the contract of every entry point: include/apml.h.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -10,6 +11,7 @@
 #include "common.cuh"
 #include "k_backward.cuh"
 #include "k_dist.cuh"
+#include "k_sinkhorn.cuh"
 #include "k_sparse.cuh"
 
 using namespace apml;
@@ -62,7 +64,7 @@ struct apml_ctx {
   bool bwd_timed = false;
   cudaEvent_t ev[13] = {};  // 0..8 forward stage boundaries, 9 backward start, 10..12 ends
   int64_t launches = 0;
-  bool smem_sinkhorn = false;
+  bool idx16 = false;
   size_t smem_bytes = 0;
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // sub-buffers
@@ -134,6 +136,16 @@ int num_sms() {
   return sms;
 }
 
+int max_smem_optin() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 232448;
+  }
+  return v;
+}
+
 // Column-range split of a sweep so that the grid covers the SMs several times over.
 void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk) {
   const int64_t blocks = own_np / kOwnTile * B;
@@ -177,7 +189,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
   size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
   size_t o_Rbar = k.take<float>(B * N * (L > 0 ? L : 1)), o_Qbar = k.take<float>(B * M * (L > 0 ? L : 1));
-  size_t o_gs = k.take<float>(B * (N + M));
+  size_t o_gs = k.take<float>(B * 2 * (N + M));
   size_t o_rowback = k.take<LineBack>(B * N), o_colback = k.take<LineBack>(B * M);
   c->bytes = k.off;
   c->base = (char*)ctx_alloc(c, c->bytes);
@@ -202,11 +214,19 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->Rbar = (float*)(p + o_Rbar); c->Qbar = (float*)(p + o_Qbar); c->gscratch = (float*)(p + o_gs);
   c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
   CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
-  c->smem_bytes = (size_t)(N + M) * sizeof(float);
-  c->smem_sinkhorn = c->smem_bytes <= 200 * 1024;
-  if (c->smem_sinkhorn && c->smem_bytes > 48 * 1024) {
-    CK(cudaFuncSetAttribute(k_sinkhorn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
-    CK(cudaFuncSetAttribute(k_sinkhorn_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+  // Sinkhorn shared-memory plan: size for a typical support (4 entries per point, capped by
+  // the capacity); pairs with a larger support fall back to the global-memory loop.
+  c->idx16 = N <= 65536 && M <= 65536;
+  const int64_t est = std::min<int64_t>((int64_t)cap, 4 * (N + M));
+  size_t want = sk_smem_bytes(N, M, est, c->idx16 ? 2 : 4, 2);
+  const size_t mx = (size_t)max_smem_optin() - 1024;
+  c->smem_bytes = want < mx ? want : mx;
+  if (c->idx16) {
+    CK(cudaFuncSetAttribute(k_sinkhorn<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+    CK(cudaFuncSetAttribute(k_sinkhorn_bwd<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+  } else {
+    CK(cudaFuncSetAttribute(k_sinkhorn<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+    CK(cudaFuncSetAttribute(k_sinkhorn_bwd<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
   }
   return APML_OK;
 }
@@ -266,9 +286,14 @@ apml_status launch_sparse(apml_ctx* c, float* loss) {
       c->colidx);
   mark(c, 7, s);
   // S6 + S7 Sinkhorn and loss
-  k_sinkhorn<<<B, 1024, c->smem_sinkhorn ? c->smem_bytes : 0, s>>>(N, M, L, c->cfg.eps_stab,
-      c->cursor, cap, c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist,
-      c->b_hist, c->gscratch, c->smem_sinkhorn ? 1 : 0, loss);
+  if (c->idx16)
+    k_sinkhorn<uint16_t><<<B, kSkThreads, c->smem_bytes, s>>>(N, M, L, c->cfg.eps_stab, c->cursor, cap,
+        c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist, c->b_hist,
+        c->gscratch, c->smem_bytes, loss);
+  else
+    k_sinkhorn<uint32_t><<<B, kSkThreads, c->smem_bytes, s>>>(N, M, L, c->cfg.eps_stab, c->cursor, cap,
+        c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist, c->b_hist,
+        c->gscratch, c->smem_bytes, loss);
   mark(c, 8, s);
   c->launches += 8;
   CK(cudaGetLastError());
@@ -387,10 +412,14 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
   mark(x, 9, s);
   x->bwd_timed = x->timing;
   if (full) {
-    k_sinkhorn_bwd<<<B, 1024, x->smem_sinkhorn ? x->smem_bytes : 0, s>>>(N, M, L, x->cfg.eps_stab,
-        x->cursor, cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c,
-        x->cs, x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch,
-        x->smem_sinkhorn ? 1 : 0);
+    if (x->idx16)
+      k_sinkhorn_bwd<uint16_t><<<B, kSkThreads, x->smem_bytes, s>>>(N, M, L, x->cfg.eps_stab, x->cursor,
+          cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c, x->cs,
+          x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch, x->smem_bytes);
+    else
+      k_sinkhorn_bwd<uint32_t><<<B, kSkThreads, x->smem_bytes, s>>>(N, M, L, x->cfg.eps_stab, x->cursor,
+          cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c, x->cs,
+          x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch, x->smem_bytes);
     mark(x, 10, s);
     k_pbar_rowsoft<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, x->cursor, cap, x->row_ptr,
         x->csr_jf, x->cs, x->prow, x->a_hist, x->b_hist, x->Rbar, x->Qbar, grad_loss, x->rowB,

@@ -3,7 +3,7 @@
 // Discrete choices of the forward (support, argmin, second argmin) are frozen; the gap
 // clamp zeroes the gradient through g.  With grad_loss gl = dL/dloss_b:
 //
-//   k_sinkhorn_bwd (full mode, CTA per pair) -- reverse of the scaling-vector Sinkhorn:
+//   k_sinkhorn_bwd (full mode, CTA per pair, k_sinkhorn.cuh) -- reverse of the scaling-vector Sinkhorn:
 //     abar = gl sum_j P0 b^L c,  bbar = gl sum_i a^L P0 c,  then for l = L..1
 //       row step  a^l = a^{l-1} / (a^{l-1} R^l + eps):
 //         Rbar^l = -abar (a^l)^2,  abar <- abar eps (a^l / a^{l-1})^2,  bbar += P0^T Rbar^l
@@ -24,73 +24,6 @@
 #include "common.cuh"
 
 namespace apml {
-
-__global__ void __launch_bounds__(1024)
-k_sinkhorn_bwd(int N, int M, int L, float eps, const unsigned* __restrict__ cursor, uint32_t cap,
-               const unsigned* __restrict__ row_ptr, const uint32_t* __restrict__ csr_jf,
-               const unsigned* __restrict__ col_ptr, const uint32_t* __restrict__ csc_i,
-               const uint32_t* __restrict__ csc_perm, const float* __restrict__ P0,
-               const float* __restrict__ P0c, const float* __restrict__ cs,
-               const float* __restrict__ a_hist, const float* __restrict__ b_hist,
-               const float* __restrict__ grad_loss, float* __restrict__ Rbar,
-               float* __restrict__ Qbar, float* __restrict__ gscratch, int use_smem) {
-  extern __shared__ float shm[];
-  const int b = blockIdx.x;
-  if (pair_overflow(cursor, b, cap)) return;
-  const size_t pb = (size_t)b * cap;
-  const float gl = grad_loss[b];
-  float* ab = use_smem ? shm : gscratch + (size_t)b * (N + M);
-  float* bb = ab + N;
-  const float* ah = a_hist + (size_t)b * N * (L + 1);
-  const float* bh = b_hist + (size_t)b * M * (L + 1);
-  float* rb = Rbar + (size_t)b * N * L;
-  float* qb = Qbar + (size_t)b * M * L;
-  const unsigned* rp = row_ptr + (size_t)b * (N + 1);
-  const unsigned* cp = col_ptr + (size_t)b * (M + 1);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double t = 0.0;
-    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
-      t += (double)P0[pb + p] * (double)bh[(size_t)(csr_jf[pb + p] & kIdxMask) * (L + 1) + L] * (double)cs[pb + p];
-    ab[i] = (float)((double)gl * t);
-  }
-  for (int j = threadIdx.x; j < M; j += blockDim.x) {
-    double t = 0.0;
-    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q)
-      t += (double)ah[(size_t)csc_i[pb + q] * (L + 1) + L] * (double)P0c[pb + q] * (double)cs[pb + csc_perm[pb + q]];
-    bb[j] = (float)((double)gl * t);
-  }
-  __syncthreads();
-  for (int l = L; l >= 1; --l) {
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      const float al = ah[(size_t)i * (L + 1) + l], alm = ah[(size_t)i * (L + 1) + l - 1];
-      const float r = al / alm;
-      rb[(size_t)i * L + (l - 1)] = -ab[i] * al * al;
-      ab[i] = ab[i] * eps * r * r;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
-      double t = 0.0;
-      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q)
-        t += (double)rb[(size_t)csc_i[pb + q] * L + (l - 1)] * (double)P0c[pb + q];
-      bb[j] = (float)((double)bb[j] + t);
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
-      const float bl = bh[(size_t)j * (L + 1) + l], blm = bh[(size_t)j * (L + 1) + l - 1];
-      const float r = bl / blm;
-      qb[(size_t)j * L + (l - 1)] = -bb[j] * bl * bl;
-      bb[j] = bb[j] * eps * r * r;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      double t = 0.0;
-      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
-        t += (double)qb[(size_t)(csr_jf[pb + p] & kIdxMask) * L + (l - 1)] * (double)P0[pb + p];
-      ab[i] = (float)((double)ab[i] + t);
-    }
-    __syncthreads();
-  }
-}
 
 // Thread per row: P0bar per entry, then the row-softmax reverse -> LineBack.
 __global__ void k_pbar_rowsoft(int N, int M, int L, const unsigned* __restrict__ cursor,

@@ -136,19 +136,35 @@ __global__ void k_line_info(const float2* __restrict__ part, int S, int B, int o
   Bo[(size_t)b * n + k] = o;
 }
 
-// Append one entry to the pair's segment.  Counts keep running past the capacity so the
-// host can size a retry; overflowed pairs are skipped downstream.
-__device__ __forceinline__ void emit_entry(int b, uint32_t i, uint32_t j, uint32_t flags,
-                                           uint32_t cap, uint2* __restrict__ ebuf,
-                                           unsigned* __restrict__ cursor,
+// Emission staging: each warp compacts its hits into a shared-memory buffer (ballot +
+// popc, no atomics) and flushes it to the pair's segment with ONE returning global atomic
+// per flush; the per-line counts are non-returning reductions (RED).  Counts keep running
+// past the capacity so the host can size a retry; overflowed pairs are skipped downstream.
+constexpr int kWarpBuf = 512;                  // staged entries per warp
+constexpr int kFlushAt = kWarpBuf - 32 * 4;    // worst case of one (row, 4 columns) step
+
+__device__ __forceinline__ void warp_flush(int b, uint2* wbuf, int n, uint32_t cap,
+                                           uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
                                            unsigned* __restrict__ aux_cnt,
                                            unsigned* __restrict__ row_cnt, int N,
                                            unsigned* __restrict__ col_cnt, int M) {
-  const unsigned pos = atomicAdd(cursor + b, 1u);
-  if (pos < cap) ebuf[(size_t)b * cap + pos] = make_uint2(i, j | flags);
-  atomicAdd(row_cnt + (size_t)b * (N + 1) + i, 1u);
-  atomicAdd(col_cnt + (size_t)b * (M + 1) + j, 1u);
-  if (!flags) atomicAdd(aux_cnt + b, 1u);
+  const int lane = threadIdx.x & 31;
+  unsigned base = 0;
+  if (lane == 0) base = atomicAdd(cursor + b, (unsigned)n);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  unsigned aux = 0;
+  for (int k = lane; k < n; k += 32) {
+    const uint2 e = wbuf[k];
+    const unsigned pos = base + k;
+    if (pos < cap) ebuf[(size_t)b * cap + pos] = e;
+    const uint32_t j = e.y & kIdxMask;
+    atomicAdd(row_cnt + (size_t)b * (N + 1) + e.x, 1u);
+    atomicAdd(col_cnt + (size_t)b * (M + 1) + j, 1u);
+    aux += (e.y & (kFlagRow | kFlagCol)) ? 0u : 1u;
+  }
+  aux = __reduce_add_sync(0xffffffffu, aux);
+  if (lane == 0 && aux) atomicAdd(aux_cnt + b, aux);
+  __syncwarp();
 }
 
 // S3 (Pass B).  Rows own pred points; gt streamed with its column radii in shared memory.
@@ -163,7 +179,11 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
   const float* own = pred_soa + (size_t)b * 3 * np;
   const float* str = gt_soa + (size_t)b * 3 * mp;
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ], sR[kTQ], sE[kTQ];
+  __shared__ uint2 wbuf_all[kSweepThreads / 32][kWarpBuf];
+  uint2* wbuf = wbuf_all[w];
+  int wcnt = 0;  // warp-uniform staged count
 
   f2_t nx[R], ny[R], nz[R];
   float rR2[R], rE2[R];
@@ -179,6 +199,7 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
       rR2[r] = -1.f; rE2[r] = -1.f;
     }
   }
+  const unsigned lt_mask = (1u << lane) - 1u;
   const int j0 = split * chunk, j1 = min(mp, j0 + chunk);
   for (int jt = j0; jt < j1; jt += kTQ) {
     __syncthreads();
@@ -210,22 +231,31 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
         f2_unpack(d23, d[2], d[3]);
         const bool hit = (d[0] <= fmaxf(rE2[r], ce.x)) | (d[1] <= fmaxf(rE2[r], ce.y)) |
                          (d[2] <= fmaxf(rE2[r], ce.z)) | (d[3] <= fmaxf(rE2[r], ce.w));
-        if (hit) {  // rare: ~5 kept entries per line out of K
+        if (__any_sync(0xffffffffu, hit)) {  // warp-uniform; ~5 kept entries per line of K
           const uint32_t i = base + r * kSweepThreads;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int t = 4 * q + c;
             const uint32_t j = jt + t;
-            const float e = fmaxf(rE2[r], sE[t]);
-            if (d[c] <= e && i < (uint32_t)N && j < (uint32_t)M) {
+            const bool h = d[c] <= fmaxf(rE2[r], sE[t]) && i < (uint32_t)N && j < (uint32_t)M;
+            const unsigned bal = __ballot_sync(0xffffffffu, h);
+            if (h) {
               const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= sR[t] ? kFlagCol : 0u);
-              emit_entry(b, i, j, fl, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+              wbuf[wcnt + __popc(bal & lt_mask)] = make_uint2(i, j | fl);
             }
+            wcnt += __popc(bal);
+          }
+          if (wcnt > kFlushAt) {
+            __syncwarp();
+            warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+            wcnt = 0;
           }
         }
       }
     }
   }
+  __syncwarp();
+  if (wcnt) warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
 }
 
 }  // namespace apml

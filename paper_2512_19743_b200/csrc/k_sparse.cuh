@@ -13,12 +13,7 @@
 //                 argmin / second argmin = first entries whose d2 equals m2 / s2 (R12).
 //   k_col_norm    the same over CSC -> P_col; P0 = (P_row + P_col)/2, a missing direction
 //                 counting as 0 (reading R8); P0 stored in CSR and CSC order.
-//   k_sinkhorn    L_iter x {column scaling Eq. (3), row scaling Eq. (4)} in the
-//                 exactly equivalent scaling-vector form P = diag(a) P0 diag(b):
-//                   b_j <- b_j / (b_j Q_j + eps),  Q_j = sum_i a_i P0_ij   (Eq. (3))
-//                   a_i <- a_i / (a_i R_i + eps),  R_i = sum_j P0_ij b_j   (Eq. (4))
-//                 as deterministic segmented sums (no float atomics), then the loss
-//                   loss_b = sum_t a_i P0_t b_j c_t.
+//   (Sinkhorn + loss: k_sinkhorn.cuh)
 //
 // Per-pair arrays are [B][cap] (cap = emit capacity per pair); positions inside a pair are
 // 32-bit.  A pair whose emission overflowed its capacity is skipped (loss = NaN).
@@ -213,76 +208,6 @@ __global__ void k_col_norm(int N, int M, const unsigned* __restrict__ cursor, ui
     P0c[pb + q] = p0;
   }
   colidx[(size_t)b * M + j] = make_int2(ia, ib);
-}
-
-// Sinkhorn + loss, one CTA per pair.  a / b (current scaling vectors) live in dynamic shared
-// memory when they fit, else in global scratch.  History a^l (l = 0..L) is kept for the
-// backward in [B][N][L+1] / [B][M][L+1].
-__global__ void __launch_bounds__(1024)
-k_sinkhorn(int N, int M, int L, float eps, const unsigned* __restrict__ cursor, uint32_t cap,
-           const unsigned* __restrict__ row_ptr, const uint32_t* __restrict__ csr_jf,
-           const unsigned* __restrict__ col_ptr, const uint32_t* __restrict__ csc_i,
-           const float* __restrict__ P0, const float* __restrict__ P0c,
-           const float* __restrict__ cs, float* __restrict__ a_hist, float* __restrict__ b_hist,
-           float* __restrict__ gscratch, int use_smem, float* __restrict__ loss) {
-  extern __shared__ float shm[];
-  const int b = blockIdx.x;
-  const size_t pb = (size_t)b * cap;
-  __shared__ double red[32];
-  if (pair_overflow(cursor, b, cap)) {
-    if (threadIdx.x == 0) loss[b] = __int_as_float(0x7fc00000);
-    return;
-  }
-  float* a = use_smem ? shm : gscratch + (size_t)b * (N + M);
-  float* bv = a + N;
-  float* ah = a_hist + (size_t)b * N * (L + 1);
-  float* bh = b_hist + (size_t)b * M * (L + 1);
-  const unsigned* rp = row_ptr + (size_t)b * (N + 1);
-  const unsigned* cp = col_ptr + (size_t)b * (M + 1);
-  for (int i = threadIdx.x; i < N; i += blockDim.x) { a[i] = 1.f; ah[(size_t)i * (L + 1)] = 1.f; }
-  for (int j = threadIdx.x; j < M; j += blockDim.x) { bv[j] = 1.f; bh[(size_t)j * (L + 1)] = 1.f; }
-  __syncthreads();
-  for (int l = 1; l <= L; ++l) {
-    // column scaling, Eq. (3): colsum_j = b_j * Q_j
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
-      float Q = 0.f;
-      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) Q = __fmaf_rn(a[csc_i[pb + q]], P0c[pb + q], Q);
-      const float bj = bv[j];
-      const float nb = __fdiv_rn(bj, __fmaf_rn(bj, Q, eps));
-      bv[j] = nb;
-      bh[(size_t)j * (L + 1) + l] = nb;
-    }
-    __syncthreads();
-    // row scaling, Eq. (4): rowsum_i = a_i * R_i
-    for (int i = threadIdx.x; i < N; i += blockDim.x) {
-      float Rs = 0.f;
-      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
-        Rs = __fmaf_rn(P0[pb + p], bv[csr_jf[pb + p] & kIdxMask], Rs);
-      const float ai = a[i];
-      const float na = __fdiv_rn(ai, __fmaf_rn(ai, Rs, eps));
-      a[i] = na;
-      ah[(size_t)i * (L + 1) + l] = na;
-    }
-    __syncthreads();
-  }
-  // loss_b = sum_i a_i sum_j P0_ij b_j c_ij
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    float t = 0.f;
-    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
-      t = __fmaf_rn(__fmul_rn(P0[pb + p], bv[csr_jf[pb + p] & kIdxMask]), cs[pb + p], t);
-    acc += (double)a[i] * (double)t;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (threadIdx.x == 0) loss[b] = (float)v;
-  }
 }
 
 }  // namespace apml
