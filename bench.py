@@ -234,13 +234,9 @@ def main():
     dist_stages = ("passA_rows", "passA_cols", "emit")
     nnz = st0["nnz_total"]
     L = cfg.l_iter
-    sparse_bytes = {  # algorithmic bytes per launch (SURVEY 8(d) per-entry figures x nnz)
-        "sinkhorn": nnz * (16 * L + 12),
-        "bwd_sinkhorn": nnz * (16 * L + 24),
-        "bwd_softmax": nnz * 44,
-        "bwd_grad": nnz * 12,
-        "norm": nnz * 48,
-        "csr": nnz * 20,
+    sparse_bytes = {  # algorithmic bytes per launch (SURVEY 8(d) per-entry totals x nnz)
+        "sparse_fwd": nnz * (8 + 20 + 48 + 16 * L + 12),   # CSR/CSC + normalise + Sinkhorn + loss
+        "sparse_bwd": nnz * (16 * L + 12 + 44 + 12),        # reverse Sinkhorn + P0bar + softmax rev + Eq. 5
     }
     dom = max(med, key=med.get)
     traffic = None

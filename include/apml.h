@@ -87,13 +87,9 @@ enum {
     APML_STAGE_PASSA_COLS = 2,  /* S1: column min / second min sweep (k_line_top2, B N M pairs) */
     APML_STAGE_LINE_INFO = 3,   /* S2: line constants */
     APML_STAGE_EMIT = 4,        /* S3: emit sweep (k_emit, B N M pairs) */
-    APML_STAGE_CSR = 5,         /* S4: scan, scatter, sort -> CSR / CSC */
-    APML_STAGE_NORM = 6,        /* S5: directional normalisation + symmetrisation */
-    APML_STAGE_SINKHORN = 7,    /* S6 + S7: Sinkhorn and loss */
-    APML_STAGE_BWD_SINKHORN = 8,/* S8: Sinkhorn reverse (full mode) */
-    APML_STAGE_BWD_SOFTMAX = 9, /* S8: P0bar + row / column softmax reverse (full mode) */
-    APML_STAGE_BWD_GRAD = 10,   /* S8: cbar + Eq. (5) scatter */
-    APML_NUM_STAGES = 11
+    APML_STAGE_SPARSE_FWD = 5,  /* S4-S7: CSR/CSC, normalisation, Sinkhorn, loss (k_sparse_fwd) */
+    APML_STAGE_SPARSE_BWD = 6,  /* S8: reverse pass (k_sparse_bwd) */
+    APML_NUM_STAGES = 7
 };
 
 typedef struct {

@@ -17,8 +17,7 @@ STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NONFINITE", 4: "CAPAC
                 6: "OOM", 7: "STATE"}
 APML_GRAD_FULL, APML_GRAD_PLAN_DETACHED = 0, 1
 APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE, APML_FLAG_STAGE_TIMING = 1, 2, 4
-STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "csr", "norm", "sinkhorn",
-          "bwd_sinkhorn", "bwd_softmax", "bwd_grad")
+STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "sparse_fwd", "sparse_bwd")
 
 # exported symbols declared in include/apml.h (checked by tests/test_abi.py)
 EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_backward",

@@ -1,5 +1,10 @@
 // apml_capi.cu -- host side of libapml.so: validation, context / workspace, launch sequence.
 // Declarations and the contract of every entry point: include/apml.h.
+//
+// Launch sequence of one forward (Algorithm 1), all on the caller's stream:
+//   k_stage x2 (S0) -> k_line_top2 rows, columns (S1) -> k_line_info x2 (S2) -> k_emit (S3)
+//   -> k_sparse_fwd (S4-S7, one thread-block cluster per pair)
+// and of one backward: k_sparse_bwd (S8, one cluster per pair).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -9,10 +14,8 @@
 
 #include "../../include/apml.h"
 #include "common.cuh"
-#include "k_backward.cuh"
 #include "k_dist.cuh"
-#include "k_sinkhorn.cuh"
-#include "k_sparse.cuh"
+#include "k_mega.cuh"
 
 using namespace apml;
 
@@ -62,10 +65,13 @@ struct apml_ctx {
   bool backward_done = false;
   bool timing = false;
   bool bwd_timed = false;
-  cudaEvent_t ev[13] = {};  // 0..8 forward stage boundaries, 9 backward start, 10..12 ends
+  cudaEvent_t ev[9] = {};  // 0..6 forward stage boundaries, 7 backward start, 8 backward end
   int64_t launches = 0;
-  bool idx16 = false;
-  size_t smem_bytes = 0;
+  // sparse-stage launch plan
+  int cl = 1;             // CTAs per pair (thread-block cluster)
+  bool idx16 = false;     // 16-bit indices in shared memory
+  int rep_smem = 0;       // scaling-vector replicas in shared memory
+  size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // sub-buffers
   float *predS, *gtS; float4 *pred4, *gt4;
@@ -77,21 +83,21 @@ struct apml_ctx {
   uint32_t *csr_t, *csc_t, *inv, *csr_jf, *csc_i, *csc_perm;
   float *d2s, *cs, *prow, *pcol, *P0, *P0c, *pbar;
   int2 *rowidx, *colidx;
-  float *a_hist, *b_hist, *Rbar, *Qbar, *gscratch;
+  float *a_hist, *b_hist, *gvec;
   LineBack *rowback, *colback;
 };
 
 namespace {
+
+void mark(apml_ctx* c, int k, cudaStream_t s) {
+  if (c->timing) cudaEventRecord(c->ev[k], s);
+}
 
 void* ctx_alloc(apml_ctx* c, size_t bytes) {
   if (c->has_alloc) return c->alloc.alloc(bytes, c->stream, c->alloc.user);
   void* p = nullptr;
   if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) return nullptr;
   return p;
-}
-
-void mark(apml_ctx* c, int k, cudaStream_t s) {
-  if (c->timing) cudaEventRecord(c->ev[k], s);
 }
 
 void ctx_free(apml_ctx* c) {
@@ -126,23 +132,19 @@ apml_status validate(const float* pred, const float* gt, int64_t B, int64_t N, i
 // Lambda_K = -log((1 - p) / ((K - 1) p)) (numerator of Eq. (1)), fp64.
 double lambda_K(int64_t K, double p) { return K > 1 ? -std::log((1.0 - p) / ((double)(K - 1) * p)) : 0.0; }
 
-int num_sms() {
-  static int sms = -1;
-  if (sms < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
-  }
-  return sms;
+int dev_attr(cudaDeviceAttr a, int fallback) {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  return cudaDeviceGetAttribute(&v, a, dev) == cudaSuccess ? v : fallback;
 }
-
+int num_sms() {
+  static int v = -1;
+  if (v < 0) v = dev_attr(cudaDevAttrMultiProcessorCount, 148);
+  return v;
+}
 int max_smem_optin() {
   static int v = -1;
-  if (v < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) v = 232448;
-  }
+  if (v < 0) v = dev_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448);
   return v;
 }
 
@@ -154,9 +156,42 @@ void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk) {
   const int64_t tiles = str_np / kTQ;
   if (s > tiles) s = tiles;
   if (s < 1) s = 1;
-  const int64_t ch = round_up((tiles + s - 1) / s, 1) * kTQ;
+  const int64_t ch = ((tiles + s - 1) / s) * kTQ;
   *chunk = (int)ch;
   *S = (int)((str_np + ch - 1) / ch);
+}
+
+// Shared-memory bytes of one CTA's CSR or CSC slice (k_mega.cuh stage_slice), host mirror.
+size_t slice_bytes_h(int64_t nl, int64_t cnt, size_t idx, bool acc) {
+  auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
+  return a16(4 * (size_t)(nl + 1)) + a16(idx * (size_t)cnt) + a16(4 * (size_t)cnt) + (acc ? a16(4 * (size_t)cnt) : 0);
+}
+
+// Sparse-stage plan: cluster size, replica placement, dynamic shared memory.
+void plan_sparse(apml_ctx* c) {
+  const int64_t B = c->B, N = c->N, M = c->M;
+  c->idx16 = N <= 65536 && M <= 65536;
+  const size_t idx = c->idx16 ? 2 : 4;
+  const size_t mx = (size_t)max_smem_optin() - 2048;  // static shared memory headroom
+  // typical union support ~5 entries per point of the larger cloud
+  const int64_t est = std::min<int64_t>((int64_t)c->cap, 5 * std::max(N, M) + 64);
+  const int64_t nmin = std::min(N, M);
+  int cl0 = 1;
+  while (cl0 * 2 <= 8 && (int64_t)cl0 * 2 * B <= num_sms() && cl0 * 2 <= nmin) cl0 *= 2;
+  auto need = [&](int cl, bool rep) {
+    const int64_t nr = (N + cl - 1) / cl, nc = (M + cl - 1) / cl, e = (est + cl - 1) / cl;
+    size_t r = rep ? 4 * (size_t)(N + M) + 32 : 0;
+    return r + 4 * (size_t)(nr + nc) + 32 + slice_bytes_h(nr, e, idx, true) + slice_bytes_h(nc, e, idx, false);
+  };
+  c->cl = cl0;
+  c->rep_smem = 0;
+  bool done = false;
+  for (int cl = cl0; cl <= 8 && !done && cl <= nmin; cl *= 2)
+    if (need(cl, true) <= mx) { c->cl = cl; c->rep_smem = 1; done = true; }
+  if (!done)
+    for (int cl = cl0; cl <= 8 && !done && cl <= nmin; cl *= 2)
+      if (need(cl, false) <= mx) { c->cl = cl; done = true; }
+  c->smem_bytes = std::min(mx, need(c->cl, c->rep_smem != 0));
 }
 
 apml_status build_ctx(apml_ctx* c, uint32_t cap) {
@@ -166,6 +201,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->Mp = round_up(M, kOwnTile);
   plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows);
   plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols);
+  plan_sparse(c);
   Carve k;
   const int64_t E = B * (int64_t)cap;
   size_t o_predS = k.take<float>(B * 3 * c->Np), o_gtS = k.take<float>(B * 3 * c->Mp);
@@ -174,7 +210,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_part_c = k.take<float2>((int64_t)c->S_cols * B * c->Mp);
   size_t o_rowA = k.take<LineA>(B * N), o_colA = k.take<LineA>(B * M);
   size_t o_rowB = k.take<LineB>(B * N), o_colB = k.take<LineB>(B * M);
-  // counters first in one contiguous zeroed block
+  // counters in one contiguous zeroed block
   size_t z0 = k.off;
   size_t o_clamp = k.take<unsigned long long>(1);
   size_t o_cursor = k.take<unsigned>(B), o_aux = k.take<unsigned>(B);
@@ -188,8 +224,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
   size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
   size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
-  size_t o_Rbar = k.take<float>(B * N * (L > 0 ? L : 1)), o_Qbar = k.take<float>(B * M * (L > 0 ? L : 1));
-  size_t o_gs = k.take<float>(B * 2 * (N + M));
+  size_t o_gv = k.take<float>(B * 2 * (N + M));
   size_t o_rowback = k.take<LineBack>(B * N), o_colback = k.take<LineBack>(B * M);
   c->bytes = k.off;
   c->base = (char*)ctx_alloc(c, c->bytes);
@@ -210,31 +245,51 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
   c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
   c->rowidx = (int2*)(p + o_rowidx); c->colidx = (int2*)(p + o_colidx);
-  c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh);
-  c->Rbar = (float*)(p + o_Rbar); c->Qbar = (float*)(p + o_Qbar); c->gscratch = (float*)(p + o_gs);
+  c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh); c->gvec = (float*)(p + o_gv);
   c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
   CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
-  // Sinkhorn shared-memory plan: size for a typical support (4 entries per point, capped by
-  // the capacity); pairs with a larger support fall back to the global-memory loop.
-  c->idx16 = N <= 65536 && M <= 65536;
-  const int64_t est = std::min<int64_t>((int64_t)cap, 4 * (N + M));
-  size_t want = sk_smem_bytes(N, M, est, c->idx16 ? 2 : 4, 2);
-  const size_t mx = (size_t)max_smem_optin() - 1024;
-  c->smem_bytes = want < mx ? want : mx;
-  if (c->idx16) {
-    CK(cudaFuncSetAttribute(k_sinkhorn<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
-    CK(cudaFuncSetAttribute(k_sinkhorn_bwd<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
-  } else {
-    CK(cudaFuncSetAttribute(k_sinkhorn<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
-    CK(cudaFuncSetAttribute(k_sinkhorn_bwd<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
-  }
   return APML_OK;
 }
 
-apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt, float* loss) {
+SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, float* grad_pred) {
+  SparseArgs a;
+  a.N = (int)c->N; a.M = (int)c->M; a.L = c->cfg.l_iter; a.full = c->cfg.grad_mode == APML_GRAD_FULL;
+  a.cap = c->cap; a.eps = c->cfg.eps_stab; a.eps_dist = c->cfg.eps_dist;
+  a.pred4 = c->pred4; a.gt4 = c->gt4; a.rowA = c->rowA; a.rowB = c->rowB; a.colA = c->colA; a.colB = c->colB;
+  a.ebuf = c->ebuf; a.cursor = c->cursor; a.row_cnt = c->row_cnt; a.col_cnt = c->col_cnt;
+  a.row_ptr = c->row_ptr; a.col_ptr = c->col_ptr; a.csr_t = c->csr_t; a.csc_t = c->csc_t; a.inv = c->inv;
+  a.csr_jf = c->csr_jf; a.csc_i = c->csc_i; a.csc_perm = c->csc_perm;
+  a.d2s = c->d2s; a.cs = c->cs; a.prow = c->prow; a.pcol = c->pcol; a.P0 = c->P0; a.P0c = c->P0c; a.pbar = c->pbar;
+  a.rowidx = c->rowidx; a.colidx = c->colidx; a.a_hist = c->a_hist; a.b_hist = c->b_hist; a.gvec = c->gvec;
+  a.rowback = c->rowback; a.colback = c->colback;
+  a.loss = loss; a.grad_loss = grad_loss; a.grad_pred = grad_pred;
+  a.smem_bytes = c->smem_bytes; a.rep_smem = c->rep_smem;
+  return a;
+}
+
+// One cluster of c->cl CTAs per pair.
+template <typename K>
+apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a, cudaStream_t s) {
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(c->B * c->cl), 1, 1);
+  cfg.blockDim = dim3(kMegaThreads, 1, 1);
+  cfg.dynamicSmemBytes = c->smem_bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)c->cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, kernel, a));
+  return APML_OK;
+}
+
+apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
-  (void)loss;
   mark(c, 0, s);
   // S0 staging
   k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
@@ -263,41 +318,13 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt, floa
   return APML_OK;
 }
 
-apml_status launch_sparse(apml_ctx* c, float* loss) {
-  const int B = (int)c->B, N = (int)c->N, M = (int)c->M;
-  const int L = c->cfg.l_iter;
-  cudaStream_t s = c->stream;
-  const uint32_t cap = c->cap;
-  // S4 CSR / CSC
-  k_scan<<<B, 1024, 0, s>>>(c->row_cnt, c->row_ptr, N);
-  k_scan<<<B, 1024, 0, s>>>(c->col_cnt, c->col_ptr, M);
-  k_scatter<<<dim3((cap + 255) / 256, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, N, M, c->row_ptr,
-      c->row_cnt, c->col_ptr, c->col_cnt, c->csr_t, c->csc_t);
-  k_sort_lines<true><<<dim3((N + 7) / 8, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, N, c->row_ptr,
-      c->csr_t, c->csr_jf, c->inv, nullptr);
-  k_sort_lines<false><<<dim3((M + 7) / 8, B), 256, 0, s>>>(c->ebuf, c->cursor, cap, M, c->col_ptr,
-      c->csc_t, c->csc_i, c->inv, c->csc_perm);
-  mark(c, 6, s);
-  // S5 normalisation + symmetrisation
-  k_row_norm<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->pred4, c->gt4, N, M, c->cursor, cap,
-      c->row_ptr, c->csr_jf, c->rowA, c->rowB, c->d2s, c->cs, c->prow, c->rowidx);
-  k_col_norm<<<dim3((M + 255) / 256, B), 256, 0, s>>>(N, M, c->cursor, cap, c->col_ptr, c->csc_i,
-      c->csc_perm, c->csr_jf, c->colA, c->colB, c->d2s, c->cs, c->prow, c->pcol, c->P0, c->P0c,
-      c->colidx);
-  mark(c, 7, s);
-  // S6 + S7 Sinkhorn and loss
-  if (c->idx16)
-    k_sinkhorn<uint16_t><<<B, kSkThreads, c->smem_bytes, s>>>(N, M, L, c->cfg.eps_stab, c->cursor, cap,
-        c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist, c->b_hist,
-        c->gscratch, c->smem_bytes, loss);
-  else
-    k_sinkhorn<uint32_t><<<B, kSkThreads, c->smem_bytes, s>>>(N, M, L, c->cfg.eps_stab, c->cursor, cap,
-        c->row_ptr, c->csr_jf, c->col_ptr, c->csc_i, c->P0, c->P0c, c->cs, c->a_hist, c->b_hist,
-        c->gscratch, c->smem_bytes, loss);
-  mark(c, 8, s);
-  c->launches += 8;
-  CK(cudaGetLastError());
-  return APML_OK;
+apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
+  const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
+  apml_status st = c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream)
+                            : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream);
+  mark(c, 6, c->stream);
+  c->launches += 1;
+  return st;
 }
 
 apml_status check_finite(const float* p, int64_t n, cudaStream_t s) {
@@ -368,7 +395,7 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
     x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
     x->rho_c = N > 1 ? (float)(lt / lambda_K(N, p)) : INFINITY;
     st = build_ctx(x, (uint32_t)cap64);
-    if (st == APML_OK) st = launch_forward(x, pred, gt, loss);
+    if (st == APML_OK) st = launch_forward(x, pred, gt);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
     if (c.flags & APML_FLAG_SYNC_CHECK) {
       std::vector<unsigned> cnt((size_t)B);
@@ -386,7 +413,7 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
         continue;
       }
     }
-    st = launch_sparse(x, loss);
+    st = launch_sparse_fwd(x, loss);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
     if (ctx_out) *ctx_out = x; else apml_ctx_destroy(x);
     return APML_OK;
@@ -399,9 +426,6 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
   if (x->backward_done) return fail(APML_ERR_STATE, "backward already ran on this context");
   if (!grad_loss || !grad_pred) return fail(APML_ERR_INVALID_ARG, "grad_loss / grad_pred must be non-NULL");
   cudaStream_t s = stream ? (cudaStream_t)stream : x->stream;
-  const int B = (int)x->B, N = (int)x->N, M = (int)x->M, L = x->cfg.l_iter;
-  const uint32_t cap = x->cap;
-  const int full = x->cfg.grad_mode == APML_GRAD_FULL;
   if (s != x->stream) {  // order after the forward's stream
     cudaEvent_t ev;
     CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -409,33 +433,13 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
     CK(cudaStreamWaitEvent(s, ev, 0));
     CK(cudaEventDestroy(ev));
   }
-  mark(x, 9, s);
+  mark(x, 7, s);
   x->bwd_timed = x->timing;
-  if (full) {
-    if (x->idx16)
-      k_sinkhorn_bwd<uint16_t><<<B, kSkThreads, x->smem_bytes, s>>>(N, M, L, x->cfg.eps_stab, x->cursor,
-          cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c, x->cs,
-          x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch, x->smem_bytes);
-    else
-      k_sinkhorn_bwd<uint32_t><<<B, kSkThreads, x->smem_bytes, s>>>(N, M, L, x->cfg.eps_stab, x->cursor,
-          cap, x->row_ptr, x->csr_jf, x->col_ptr, x->csc_i, x->csc_perm, x->P0, x->P0c, x->cs,
-          x->a_hist, x->b_hist, grad_loss, x->Rbar, x->Qbar, x->gscratch, x->smem_bytes);
-    mark(x, 10, s);
-    k_pbar_rowsoft<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, x->cursor, cap, x->row_ptr,
-        x->csr_jf, x->cs, x->prow, x->a_hist, x->b_hist, x->Rbar, x->Qbar, grad_loss, x->rowB,
-        x->pbar, x->rowback);
-    k_colsoft<<<dim3((M + 255) / 256, B), 256, 0, s>>>(N, M, x->cursor, cap, x->col_ptr,
-        x->csc_perm, x->csr_jf, x->cs, x->pcol, x->pbar, x->colB, x->colback);
-    mark(x, 11, s);
-    x->launches += 3;
-  } else {
-    mark(x, 10, s);
-    mark(x, 11, s);
-  }
-  k_grad<<<dim3((N + 255) / 256, B), 256, 0, s>>>(N, M, L, full, x->cfg.eps_dist, x->cursor, cap,
-      x->pred4, x->gt4, x->row_ptr, x->csr_jf, x->cs, x->P0, x->prow, x->pcol, x->pbar, x->a_hist,
-      x->b_hist, grad_loss, x->rowback, x->colback, x->rowidx, x->colidx, grad_pred);
-  mark(x, 12, s);
+  const SparseArgs a = sparse_args(x, nullptr, grad_loss, grad_pred);
+  apml_status st = x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s)
+                            : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s);
+  if (st != APML_OK) return st;
+  mark(x, 8, s);
   x->launches += 1;
   CK(cudaGetLastError());
   x->backward_done = true;
@@ -482,15 +486,15 @@ apml_status apml_ctx_support(const apml_ctx* x, int64_t b, int64_t* count, int32
   if (cap_in < (int64_t)cur) return fail(APML_ERR_CAPACITY, "output arrays too small");
   std::vector<unsigned> rp((size_t)N + 1);
   std::vector<uint32_t> jf(cur);
-  std::vector<float> p0(cur), ah((size_t)N * (L + 1)), bh((size_t)M * (L + 1));
+  std::vector<float> p0(cur), aL((size_t)N), bL((size_t)M);
   const size_t pb = (size_t)b * x->cap;
   CK(cudaMemcpyAsync(rp.data(), x->row_ptr + (size_t)b * (N + 1), sizeof(unsigned) * (N + 1), cudaMemcpyDeviceToHost, x->stream));
   if (cur) {
     CK(cudaMemcpyAsync(jf.data(), x->csr_jf + pb, sizeof(uint32_t) * cur, cudaMemcpyDeviceToHost, x->stream));
     CK(cudaMemcpyAsync(p0.data(), x->P0 + pb, sizeof(float) * cur, cudaMemcpyDeviceToHost, x->stream));
   }
-  CK(cudaMemcpyAsync(ah.data(), x->a_hist + (size_t)b * N * (L + 1), sizeof(float) * ah.size(), cudaMemcpyDeviceToHost, x->stream));
-  CK(cudaMemcpyAsync(bh.data(), x->b_hist + (size_t)b * M * (L + 1), sizeof(float) * bh.size(), cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(aL.data(), x->a_hist + ((size_t)b * (L + 1) + L) * N, sizeof(float) * N, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(bL.data(), x->b_hist + ((size_t)b * (L + 1) + L) * M, sizeof(float) * M, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaStreamSynchronize(x->stream));
   for (int64_t i = 0; i < N; ++i)
     for (unsigned p = rp[i]; p < rp[i + 1]; ++p) {
@@ -499,7 +503,7 @@ apml_status apml_ctx_support(const apml_ctx* x, int64_t b, int64_t* count, int32
       if (oj) oj[p] = (int32_t)j;
       if (ofl) ofl[p] = ((jf[p] & kFlagRow) ? 1 : 0) | ((jf[p] & kFlagCol) ? 2 : 0);
       if (op0) op0[p] = p0[p];
-      if (ov) ov[p] = ah[(size_t)i * (L + 1) + L] * p0[p] * bh[(size_t)j * (L + 1) + L];
+      if (ov) ov[p] = aL[i] * p0[p] * bL[j];
     }
   return APML_OK;
 }
@@ -531,10 +535,9 @@ apml_status apml_ctx_stage_times(const apml_ctx* x, float* ms, int32_t n) {
   if (!x->timing) return fail(APML_ERR_STATE, "context was created without APML_FLAG_STAGE_TIMING");
   if (!ms || n < APML_NUM_STAGES) return fail(APML_ERR_INVALID_ARG, "ms must hold APML_NUM_STAGES floats");
   for (int k = 0; k < APML_NUM_STAGES; ++k) ms[k] = 0.f;
-  CK(cudaEventSynchronize(x->ev[x->bwd_timed ? 12 : 8]));
-  for (int k = 0; k < 8; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k], x->ev[k + 1]));
-  if (x->bwd_timed)
-    for (int k = 8; k < 11; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k + 1], x->ev[k + 2]));
+  CK(cudaEventSynchronize(x->ev[x->bwd_timed ? 8 : 6]));
+  for (int k = 0; k < 6; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k], x->ev[k + 1]));
+  if (x->bwd_timed) CK(cudaEventElapsedTime(&ms[APML_STAGE_SPARSE_BWD], x->ev[7], x->ev[8]));
   return APML_OK;
 }
 
@@ -565,7 +568,7 @@ apml_status apml_loss_grad_host(const float* pred_host, const float* gt_host, in
   float* d_gt = (float*)(buf + round_up(bp, 256));
   float* d_loss = (float*)(buf + round_up(bp, 256) + round_up(bg, 256));
   float* d_gl = d_loss + round_up(B, 64);
-  float* d_grad = (float*)((char*)(d_gl + round_up(B, 64)));
+  float* d_grad = d_gl + round_up(B, 64);
   apml_status st = APML_OK;
   apml_ctx* ctx = nullptr;
   std::vector<float> ones((size_t)B, 1.f);

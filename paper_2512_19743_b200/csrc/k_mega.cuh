@@ -1,0 +1,664 @@
+// k_mega.cuh -- the O(nnz) sparse stage of one pair as ONE kernel per direction of the pass,
+// run by a thread-block CLUSTER per pair.
+//
+// Every CTA of the cluster owns a contiguous slice of the pair's rows and of its columns.
+// Phases are separated by cluster barriers (barrier.cluster release/acquire), so the whole
+// sparse forward (or backward) of a batch is a single launch of B x CL CTAs instead of ~10
+// grid-wide launches:
+//
+//   forward  k_sparse_fwd:  scan (cluster-wide, slice totals exchanged through DSMEM) ->
+//            scatter -> rank-sort rows -> rank-sort columns (CSR + CSC) ->
+//            row softmax on the kept support -> column softmax +
+//            symmetrisation P0 = (P_row + P_col)/2 -> Sinkhorn, L_iter x
+//            {Eq. (3), Eq. (4)} -> loss.
+//   backward k_sparse_bwd:  reverse Sinkhorn with P0bar accumulated in shared memory ->
+//            row softmax reverse -> column softmax reverse -> cbar + Eq. (5).
+//
+// Sinkhorn runs in scaling-vector form P = diag(a) P0 diag(b) (see k_sinkhorn.cuh).  Each
+// CTA keeps a full REPLICA of the current scaling vector (a, b forward; Rbar^l, Qbar^l
+// backward) in its shared memory and, after computing its own slice, pushes the new values
+// into every replica of the cluster through distributed shared memory (st.shared::cluster);
+// all gathers of a half-step are then local shared-memory reads.  Its own CSR / CSC slice
+// (16-bit indices when N, M <= 65536) and P0 also sit in shared memory.  When the replicas do
+// not fit (N + M too large) they live in global memory, and a CTA whose own slice does not
+// fit reads it from global memory -- same loop, L2-resident operands.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace apml {
+
+namespace cg = cooperative_groups;
+
+constexpr int kMegaThreads = 512;
+constexpr int kMaxCluster = 16;
+
+struct SparseArgs {
+  int N, M, L, full;
+  uint32_t cap;
+  float eps, eps_dist;
+  const float4* pred4;
+  const float4* gt4;
+  const LineA* rowA;
+  const LineB* rowB;
+  const LineA* colA;
+  const LineB* colB;
+  const uint2* ebuf;
+  const unsigned* cursor;
+  unsigned* row_cnt;  // counts from k_emit; zeroed here and reused as fill cursors
+  unsigned* col_cnt;
+  unsigned* row_ptr;
+  unsigned* col_ptr;
+  uint32_t* csr_t;
+  uint32_t* csc_t;
+  uint32_t* inv;
+  uint32_t* csr_jf;
+  uint32_t* csc_i;
+  uint32_t* csc_perm;
+  float* d2s;
+  float* cs;
+  float* prow;
+  float* pcol;
+  float* P0;
+  float* P0c;
+  float* pbar;
+  int2* rowidx;
+  int2* colidx;
+  float* a_hist;  // [B][L+1][N]
+  float* b_hist;  // [B][L+1][M]
+  float* gvec;    // [B][2 (N + M)] replica scratch when replicas are not in shared memory
+  LineBack* rowback;
+  LineBack* colback;
+  float* loss;
+  const float* grad_loss;
+  float* grad_pred;
+  size_t smem_bytes;
+  int rep_smem;
+};
+
+struct Slice {
+  int lo, hi;
+};
+__device__ __forceinline__ Slice slice_of(int n, int rank, int cl) {
+  return Slice{(int)((long long)n * rank / cl), (int)((long long)n * (rank + 1) / cl)};
+}
+
+// ---------------------------------------------------------------- CSR / CSC construction
+
+// Exclusive scan of cnt[lo, hi) (block-wide) offset by the totals of lower-ranked slices;
+// writes ptr[lo, hi) (+ ptr[n] by the last rank) and zeroes cnt[lo, hi) (fill cursors).
+__device__ void cluster_scan(cg::cluster_group& cl, unsigned* cnt, unsigned* ptr, int n, Slice s,
+                             unsigned* s_tot, unsigned* s_warp) {
+  const int rank = cl.block_rank(), CL = cl.num_blocks();
+  const int len = s.hi - s.lo;
+  const int per = (len + blockDim.x - 1) / blockDim.x;
+  const int beg = s.lo + threadIdx.x * per, end = min(s.hi, beg + per);
+  unsigned sum = 0;
+  for (int k = beg; k < end; ++k) sum += cnt[k];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    unsigned t = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += v;
+    }
+    s_warp[lane] = t;
+  }
+  __syncthreads();
+  const unsigned slice_total = s_warp[(blockDim.x >> 5) - 1];
+  if (threadIdx.x < CL) {
+    unsigned* remote = cl.map_shared_rank(s_tot, (int)threadIdx.x);
+    remote[rank] = slice_total;
+  }
+  cl.sync();
+  unsigned off = 0;
+  for (int r = 0; r < rank; ++r) off += s_tot[r];
+  unsigned run = off + inc - sum + (w ? s_warp[w - 1] : 0u);
+  for (int k = beg; k < end; ++k) {
+    const unsigned v = cnt[k];
+    ptr[k] = run;
+    run += v;
+    cnt[k] = 0u;
+  }
+  if (rank == CL - 1 && threadIdx.x == 0) ptr[n] = off + slice_total;
+  __syncthreads();  // s_tot / s_warp reused by the next scan
+}
+
+// Warp per line rank sort (keys inside a line are distinct).
+template <bool kRows>
+__device__ void sort_lines(const SparseArgs& A, int b, Slice s) {
+  const size_t pb = (size_t)b * A.cap;
+  const int n = kRows ? A.N : A.M;
+  const unsigned* ptr = (kRows ? A.row_ptr : A.col_ptr) + (size_t)b * (n + 1);
+  const uint32_t* seg_t = (kRows ? A.csr_t : A.csc_t) + pb;
+  const uint2* e = A.ebuf + pb;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int line = s.lo + (threadIdx.x >> 5); line < s.hi; line += nw) {
+    const uint32_t beg = ptr[line], end = ptr[line + 1], L = end - beg;
+    auto key_of = [&](uint32_t t) -> uint32_t { return kRows ? (e[t].y & kIdxMask) : e[t].x; };
+    auto place = [&](uint32_t t, uint32_t rank) {
+      const uint32_t pos = beg + rank;
+      if (kRows) {
+        A.csr_jf[pb + pos] = e[t].y;
+        A.inv[pb + t] = pos;
+      } else {
+        A.csc_i[pb + pos] = e[t].x;
+        A.csc_perm[pb + pos] = A.inv[pb + t];
+      }
+    };
+    if (L <= 32) {
+      const uint32_t t = lane < (int)L ? seg_t[beg + lane] : 0u;
+      const uint32_t key = lane < (int)L ? key_of(t) : 0xffffffffu;
+      uint32_t rank = 0;
+      for (uint32_t k = 0; k < L; ++k) rank += (__shfl_sync(0xffffffffu, key, k) < key) ? 1u : 0u;
+      if (lane < (int)L) place(t, rank);
+    } else {
+      for (uint32_t q = beg + lane; q < end; q += 32) {
+        const uint32_t t = seg_t[q];
+        const uint32_t key = key_of(t);
+        uint32_t rank = 0;
+        for (uint32_t f = beg; f < end; ++f) rank += (key_of(seg_t[f]) < key) ? 1u : 0u;
+        place(t, rank);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- normalisation
+
+// Row softmax on the kept support (thread per row): d2, c, P_row, argmin / second argmin.
+__device__ void row_norm(const SparseArgs& A, int b, Slice s) {
+  const int N = A.N, M = A.M;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+    const float4 x = A.pred4[(size_t)b * N + i];
+    const LineA la = A.rowA[(size_t)b * N + i];
+    const LineB lb = A.rowB[(size_t)b * N + i];
+    int ia = -1, ib = -1;
+    float Z = 0.f;
+    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const uint32_t jf = A.csr_jf[pb + p];
+      const uint32_t j = jf & kIdxMask;
+      const float4 y = A.gt4[(size_t)b * M + j];
+      const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+      const float c = __fsqrt_rn(d2);
+      A.d2s[pb + p] = d2;
+      A.cs[pb + p] = c;
+      if (ia < 0 && d2 == la.m2) ia = (int)j;
+      else if (ib < 0 && d2 == la.s2) ib = (int)j;
+      float sv = 0.f;
+      if (jf & kFlagRow) {
+        sv = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (c - lb.m));
+        Z += sv;
+      }
+      A.prow[pb + p] = sv;
+    }
+    const float iz = 1.f / Z;
+    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) A.prow[pb + p] *= iz;
+    A.rowidx[(size_t)b * N + i] = make_int2(ia, ib);
+  }
+}
+
+// Column softmax + symmetrisation (thread per column).
+__device__ void col_norm(const SparseArgs& A, int b, Slice s) {
+  const int M = A.M;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+    const LineA la = A.colA[(size_t)b * M + j];
+    const LineB lb = A.colB[(size_t)b * M + j];
+    int ia = -1, ib = -1;
+    float Z = 0.f;
+    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+      const uint32_t p = A.csc_perm[pb + q];
+      const float d2 = A.d2s[pb + p];
+      const uint32_t i = A.csc_i[pb + q];
+      if (ia < 0 && d2 == la.m2) ia = (int)i;
+      else if (ib < 0 && d2 == la.s2) ib = (int)i;
+      if (A.csr_jf[pb + p] & kFlagCol) Z += (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m));
+    }
+    const float iz = 1.f / Z;
+    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+      const uint32_t p = A.csc_perm[pb + q];
+      float pc = 0.f;
+      if (A.csr_jf[pb + p] & kFlagCol)
+        pc = ((lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m))) * iz;
+      A.pcol[pb + p] = pc;
+      const float p0 = 0.5f * (A.prow[pb + p] + pc);
+      A.P0[pb + p] = p0;
+      A.P0c[pb + q] = p0;
+    }
+    A.colidx[(size_t)b * M + j] = make_int2(ia, ib);
+  }
+}
+
+// ---------------------------------------------------------------- shared-memory views
+
+// One CTA's slice of the CSR (or CSC) structure: entries of local line k are
+// [off[k], off[k+1]) in idx / val (and acc, backward).
+template <typename IdxT>
+struct SliceView {
+  const unsigned* off;
+  const IdxT* idx;
+  const float* val;
+  float* acc;
+  __device__ __forceinline__ uint32_t col(uint32_t p) const { return (uint32_t)idx[p] & kIdxMask; }
+};
+
+__device__ __forceinline__ uint8_t* carve(uint8_t*& sm, size_t bytes) {
+  uint8_t* p = sm;
+  sm += (bytes + 15) & ~size_t(15);
+  return p;
+}
+
+// Stage a line slice [s.lo, s.hi) of a CSR/CSC structure into shared memory (relative offsets).
+template <typename IdxT>
+__device__ SliceView<IdxT> stage_slice(uint8_t*& sm, const unsigned* ptr, Slice s,
+                                       const uint32_t* idx_g, const float* val_g, bool with_acc) {
+  const int nl = s.hi - s.lo;
+  const uint32_t base = ptr[s.lo], cnt = ptr[s.hi] - base;
+  unsigned* off = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)(nl + 1)));
+  IdxT* idx = reinterpret_cast<IdxT*>(carve(sm, sizeof(IdxT) * (size_t)cnt));
+  float* val = reinterpret_cast<float*>(carve(sm, 4 * (size_t)cnt));
+  float* acc = with_acc ? reinterpret_cast<float*>(carve(sm, 4 * (size_t)cnt)) : nullptr;
+  for (int k = threadIdx.x; k <= nl; k += blockDim.x) off[k] = ptr[s.lo + k] - base;
+  for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+    idx[k] = (IdxT)(idx_g[base + k] & kIdxMask);
+    val[k] = val_g[base + k];
+  }
+  return SliceView<IdxT>{off, idx, val, acc};
+}
+
+__device__ __forceinline__ size_t slice_bytes(int nl, uint32_t cnt, size_t idx_bytes, bool acc) {
+  return ((4 * (size_t)(nl + 1) + 15) & ~size_t(15)) + ((idx_bytes * cnt + 15) & ~size_t(15)) +
+         ((4 * (size_t)cnt + 15) & ~size_t(15)) + (acc ? ((4 * (size_t)cnt + 15) & ~size_t(15)) : 0);
+}
+
+// Push v into element k of the replica `rep` in every CTA of the cluster (or once, when the
+// replica lives in global memory).
+__device__ __forceinline__ void push_rep(cg::cluster_group& cl, float* rep, int k, float v, bool smem) {
+  if (!smem) { rep[k] = v; return; }
+  const int CL = cl.num_blocks();
+  for (int r = 0; r < CL; ++r) cl.map_shared_rank(rep, r)[k] = v;
+}
+
+// ---------------------------------------------------------------- forward Sinkhorn + loss
+
+template <typename IdxT>
+__device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
+                             const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* a, float* bv,
+                             bool rep_smem) {
+  const int N = A.N, M = A.M, L = A.L;
+  float* ah = A.a_hist + (size_t)b * (L + 1) * N;
+  float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+  for (int l = 1; l <= L; ++l) {
+    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {  // Eq. (3): colsum = b_j Q_j
+      const int k = j - sc.lo;
+      float Q = 0.f;
+      for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) Q = __fmaf_rn(a[C.col(q)], C.val[q], Q);
+      const float bj = bv[j];
+      const float nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
+      bh[(size_t)l * M + j] = nb;
+      push_rep(cl, bv, j, nb, rep_smem);
+    }
+    cl.sync();
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {  // Eq. (4): rowsum = a_i R_i
+      const int k = i - sr.lo;
+      float Rs = 0.f;
+      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) Rs = __fmaf_rn(R.val[p], bv[R.col(p)], Rs);
+      const float ai = a[i];
+      const float na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+      ah[(size_t)l * N + i] = na;
+      push_rep(cl, a, i, na, rep_smem);
+    }
+    cl.sync();
+  }
+}
+
+// ---------------------------------------------------------------- the forward kernel
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs A) {
+  extern __shared__ __align__(16) uint8_t shm[];
+  __shared__ unsigned s_tot_r[kMaxCluster], s_tot_c[kMaxCluster];  // one per scan (no reuse race)
+  __shared__ unsigned s_warp[32];
+  __shared__ double s_part[kMaxCluster];
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = cl.num_blocks(), rank = cl.block_rank();
+  const int b = blockIdx.x / CL;
+  const int N = A.N, M = A.M, L = A.L;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned total = A.cursor[b];
+  if (total > A.cap) {  // overflowed pair: uniform across the cluster, no barrier follows
+    if (rank == 0 && threadIdx.x == 0) A.loss[b] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const Slice sr = slice_of(N, rank, CL), sc = slice_of(M, rank, CL);
+  unsigned* rc = A.row_cnt + (size_t)b * (N + 1);
+  unsigned* cc = A.col_cnt + (size_t)b * (M + 1);
+  unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  // S4: counts -> offsets ("exclusive prefix sum"), then bucket the entries
+  cluster_scan(cl, rc, rp, N, sr, s_tot_r, s_warp);
+  cluster_scan(cl, cc, cp, M, sc, s_tot_c, s_warp);
+  cl.sync();
+  for (uint32_t t = rank * blockDim.x + threadIdx.x; t < total; t += CL * blockDim.x) {
+    const uint2 e = A.ebuf[pb + t];
+    const uint32_t i = e.x, j = e.y & kIdxMask;
+    A.csr_t[pb + rp[i] + atomicAdd(rc + i, 1u)] = t;
+    A.csc_t[pb + cp[j] + atomicAdd(cc + j, 1u)] = t;
+  }
+  cl.sync();
+  sort_lines<true>(A, b, sr);
+  cl.sync();
+  sort_lines<false>(A, b, sc);
+  // S5: directional softmax on the kept supports, symmetrisation
+  row_norm(A, b, sr);
+  cl.sync();
+  col_norm(A, b, sc);
+  cl.sync();
+  // S6: Sinkhorn.  Replicas of a and b (full length) + own CSR / CSC slices in shared memory.
+  uint8_t* sm = shm;
+  float *a, *bv;
+  if (A.rep_smem) {
+    a = reinterpret_cast<float*>(carve(sm, 4 * (size_t)N));
+    bv = reinterpret_cast<float*>(carve(sm, 4 * (size_t)M));
+    for (int k = threadIdx.x; k < N; k += blockDim.x) a[k] = 1.f;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) bv[k] = 1.f;
+  } else {
+    a = A.gvec + (size_t)b * 2 * (N + M);
+    bv = a + N;
+    for (int k = sr.lo + threadIdx.x; k < sr.hi; k += blockDim.x) a[k] = 1.f;
+    for (int k = sc.lo + threadIdx.x; k < sc.hi; k += blockDim.x) bv[k] = 1.f;
+  }
+  float* ah = A.a_hist + (size_t)b * (L + 1) * N;
+  float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+  for (int k = sr.lo + threadIdx.x; k < sr.hi; k += blockDim.x) ah[k] = 1.f;
+  for (int k = sc.lo + threadIdx.x; k < sc.hi; k += blockDim.x) bh[k] = 1.f;
+  const size_t used = (size_t)(sm - shm);
+  const bool fit = used + slice_bytes(sr.hi - sr.lo, rp[sr.hi] - rp[sr.lo], sizeof(IdxT), false) +
+                       slice_bytes(sc.hi - sc.lo, cp[sc.hi] - cp[sc.lo], sizeof(IdxT), false) <= A.smem_bytes;
+  if (fit) {
+    const SliceView<IdxT> R = stage_slice<IdxT>(sm, rp, sr, A.csr_jf + pb, A.P0 + pb, false);
+    const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
+    cl.sync();
+    sinkhorn_fwd<IdxT>(cl, A, b, sr, sc, R, C, a, bv, A.rep_smem);
+  } else {
+    const SliceView<uint32_t> R{rp + sr.lo, A.csr_jf + pb, A.P0 + pb, nullptr};
+    const SliceView<uint32_t> C{cp + sc.lo, A.csc_i + pb, A.P0c + pb, nullptr};
+    cl.sync();
+    sinkhorn_fwd<uint32_t>(cl, A, b, sr, sc, R, C, a, bv, A.rep_smem);
+  }
+  // S7: loss_b = sum_i a_i sum_j P0_ij b_j c_ij over own rows, then cluster reduction in rank order
+  double acc = 0.0;
+  for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+    float t = 0.f;
+    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
+      t = __fmaf_rn(__fmul_rn(A.P0[pb + p], bv[A.csr_jf[pb + p] & kIdxMask]), A.cs[pb + p], t);
+    acc += (double)a[i] * (double)t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  __shared__ double s_red[32];
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+    cl.map_shared_rank(s_part, 0)[rank] = t;
+  }
+  cl.sync();
+  if (rank == 0 && threadIdx.x == 0) {
+    double t = 0.0;
+    for (int r = 0; r < CL; ++r) t += s_part[r];
+    A.loss[b] = (float)t;
+  }
+}
+
+// ---------------------------------------------------------------- backward
+
+template <typename IdxT>
+__device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
+                             const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* ab, float* bb,
+                             float* rcur, float* qcur, bool rep_smem) {
+  const int N = A.N, M = A.M, L = A.L;
+  const float* ah = A.a_hist + (size_t)b * (L + 1) * N;
+  const float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+  for (int l = L; l >= 1; --l) {
+    // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
+    // P0bar_ij += Rbar^l_i b^l_j
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+      const int k = i - sr.lo;
+      const float al = ah[(size_t)l * N + i], alm = ah[(size_t)(l - 1) * N + i];
+      const float r = al / alm;
+      const float Rb = -ab[k] * al * al;
+      ab[k] = ab[k] * A.eps * r * r;
+      push_rep(cl, rcur, i, Rb, rep_smem);
+      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += Rb * bh[(size_t)l * M + R.col(p)];
+    }
+    cl.sync();
+    // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
+    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
+      const int k = j - sc.lo;
+      double t = 0.0;
+      for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) t += (double)rcur[C.col(q)] * (double)C.val[q];
+      const float bsum = (float)((double)bb[k] + t);
+      const float bl = bh[(size_t)l * M + j], blm = bh[(size_t)(l - 1) * M + j];
+      const float r = bl / blm;
+      bb[k] = bsum * A.eps * r * r;
+      push_rep(cl, qcur, j, -bsum * bl * bl, rep_smem);
+    }
+    cl.sync();
+    // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+      const int k = i - sr.lo;
+      const float alm = ah[(size_t)(l - 1) * N + i];
+      double t = 0.0;
+      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) {
+        const float qv = qcur[R.col(p)];
+        t += (double)qv * (double)R.val[p];
+        R.acc[p] += qv * alm;
+      }
+      ab[k] = (float)((double)ab[k] + t);
+    }
+    // no barrier needed: the next row step touches only this thread's rows and rcur, which
+    // no CTA reads until after the next cl.sync()
+  }
+  cl.sync();
+}
+
+// Row softmax reverse (thread per row) -> LineBack; P0bar read from the CSR-order array.
+__device__ void row_soft_rev(const SparseArgs& A, int b, Slice s) {
+  const int N = A.N;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+    const LineB lb = A.rowB[(size_t)b * N + i];
+    LineBack out = {0.f, 0.f, 0.f, 0.f};
+    if (!(lb.flags & kLineK1)) {
+      double S = 0.0;
+      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
+        if (A.csr_jf[pb + p] & kFlagRow) S += (double)A.prow[pb + p] * 0.5 * (double)A.pbar[pb + p];
+      double szb = 0.0, Tbar = 0.0;
+      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
+        if (!(A.csr_jf[pb + p] & kFlagRow)) continue;
+        const double zb = (double)A.prow[pb + p] * (0.5 * (double)A.pbar[pb + p] - S);
+        szb += zb;
+        Tbar -= zb * ((double)A.cs[pb + p] - (double)lb.m);
+      }
+      const double mbar = (double)lb.T * szb;
+      const double gbar = (lb.flags & kLineClamped) ? 0.0 : -Tbar * (double)lb.T / (double)lb.g;
+      out = {(float)S, (float)(mbar - gbar), (float)gbar, lb.T};
+    }
+    A.rowback[(size_t)b * N + i] = out;
+  }
+}
+
+__device__ void col_soft_rev(const SparseArgs& A, int b, Slice s) {
+  const int M = A.M;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+    const LineB lb = A.colB[(size_t)b * M + j];
+    LineBack out = {0.f, 0.f, 0.f, 0.f};
+    if (!(lb.flags & kLineK1)) {
+      double S = 0.0;
+      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+        const uint32_t p = A.csc_perm[pb + q];
+        if (A.csr_jf[pb + p] & kFlagCol) S += (double)A.pcol[pb + p] * 0.5 * (double)A.pbar[pb + p];
+      }
+      double szb = 0.0, Tbar = 0.0;
+      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+        const uint32_t p = A.csc_perm[pb + q];
+        if (!(A.csr_jf[pb + p] & kFlagCol)) continue;
+        const double zb = (double)A.pcol[pb + p] * (0.5 * (double)A.pbar[pb + p] - S);
+        szb += zb;
+        Tbar -= zb * ((double)A.cs[pb + p] - (double)lb.m);
+      }
+      const double mbar = (double)lb.T * szb;
+      const double gbar = (lb.flags & kLineClamped) ? 0.0 : -Tbar * (double)lb.T / (double)lb.g;
+      out = {(float)S, (float)(mbar - gbar), (float)gbar, lb.T};
+    }
+    A.colback[(size_t)b * M + j] = out;
+  }
+}
+
+// cbar per entry and the Eq. (5) scatter into grad_pred (thread per row, overwrites).
+__device__ void grad_rows(const SparseArgs& A, int b, Slice s) {
+  const int N = A.N, M = A.M, L = A.L;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  const float gl = A.grad_loss[b];
+  const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
+  const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
+  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+    const float4 x = A.pred4[(size_t)b * N + i];
+    LineBack rbk = {0.f, 0.f, 0.f, 0.f};
+    int2 ri = make_int2(-1, -1);
+    if (A.full) { rbk = A.rowback[(size_t)b * N + i]; ri = A.rowidx[(size_t)b * N + i]; }
+    const double ai = (double)aL[i];
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const uint32_t jf = A.csr_jf[pb + p];
+      const uint32_t j = jf & kIdxMask;
+      const double c = (double)A.cs[pb + p];
+      double cbar = (double)gl * ai * (double)A.P0[pb + p] * (double)bL[j];  // d loss / d c = v
+      if (A.full) {
+        const double hp = 0.5 * (double)A.pbar[pb + p];
+        if (jf & kFlagRow) cbar -= (double)rbk.T * (double)A.prow[pb + p] * (hp - (double)rbk.S);
+        if ((int)j == ri.x) cbar += rbk.ca;
+        if ((int)j == ri.y) cbar += rbk.cb;
+        const int2 ci = A.colidx[(size_t)b * M + j];
+        const bool cf = (jf & kFlagCol) != 0;
+        if (cf || ci.x == i || ci.y == i) {
+          const LineBack cbk = A.colback[(size_t)b * M + j];
+          if (cf) cbar -= (double)cbk.T * (double)A.pcol[pb + p] * (hp - (double)cbk.S);
+          if (ci.x == i) cbar += cbk.ca;
+          if (ci.y == i) cbar += cbk.cb;
+        }
+      }
+      const float4 y = A.gt4[(size_t)b * M + j];
+      const double w = cbar / (c + (double)A.eps_dist);  // Eq. (5)
+      gx += w * ((double)x.x - (double)y.x);
+      gy += w * ((double)x.y - (double)y.y);
+      gz += w * ((double)x.z - (double)y.z);
+    }
+    float* g = A.grad_pred + ((size_t)b * N + i) * 3;
+    g[0] = (float)gx; g[1] = (float)gy; g[2] = (float)gz;
+  }
+}
+
+template <typename IdxT>
+__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs A) {
+  extern __shared__ __align__(16) uint8_t shm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = cl.num_blocks(), rank = cl.block_rank();
+  const int b = blockIdx.x / CL;
+  const int N = A.N, M = A.M, L = A.L;
+  const size_t pb = (size_t)b * A.cap;
+  const Slice sr = slice_of(N, rank, CL), sc = slice_of(M, rank, CL);
+  if (A.cursor[b] > A.cap) {
+    const float nan = __int_as_float(0x7fc00000);
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+      float* g = A.grad_pred + ((size_t)b * N + i) * 3;
+      g[0] = nan; g[1] = nan; g[2] = nan;
+    }
+    return;
+  }
+  if (A.full) {
+    const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+    const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+    const float gl = A.grad_loss[b];
+    const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
+    const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
+    uint8_t* sm = shm;
+    float *rcur, *qcur;
+    if (A.rep_smem) {
+      rcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)N));
+      qcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)M));
+    } else {
+      rcur = A.gvec + (size_t)b * 2 * (N + M);
+      qcur = rcur + N;
+    }
+    float* ab = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sr.hi - sr.lo)));
+    float* bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
+    // abar = gl sum_j P0 b^L c, bbar = gl sum_i a^L P0 c   (loss = sum a P0 b c)
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+      double t = 0.0;
+      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
+        t += (double)A.P0[pb + p] * (double)bL[A.csr_jf[pb + p] & kIdxMask] * (double)A.cs[pb + p];
+      ab[i - sr.lo] = (float)((double)gl * t);
+    }
+    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
+      double t = 0.0;
+      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q)
+        t += (double)aL[A.csc_i[pb + q]] * (double)A.P0c[pb + q] * (double)A.cs[pb + A.csc_perm[pb + q]];
+      bb[j - sc.lo] = (float)((double)gl * t);
+    }
+    const size_t used = (size_t)(sm - shm);
+    const bool fit = used + slice_bytes(sr.hi - sr.lo, rp[sr.hi] - rp[sr.lo], sizeof(IdxT), true) +
+                         slice_bytes(sc.hi - sc.lo, cp[sc.hi] - cp[sc.lo], sizeof(IdxT), false) <= A.smem_bytes;
+    // P0bar accumulator starts at the direct term gl a^L_i b^L_j c_ij
+    if (fit) {
+      const SliceView<IdxT> R = stage_slice<IdxT>(sm, rp, sr, A.csr_jf + pb, A.P0 + pb, true);
+      const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
+      __syncthreads();  // offsets staged by other threads
+      for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+        const int k = i - sr.lo;
+        for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p)
+          R.acc[p] = gl * aL[i] * bL[R.col(p)] * A.cs[pb + rp[sr.lo] + p];
+      }
+      cl.sync();
+      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem);
+      const uint32_t base = rp[sr.lo], cnt = rp[sr.hi] - base;
+      for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) A.pbar[pb + base + k] = R.acc[k];
+    } else {
+      const SliceView<uint32_t> R{rp + sr.lo, A.csr_jf + pb, A.P0 + pb, A.pbar + pb};
+      const SliceView<uint32_t> C{cp + sc.lo, A.csc_i + pb, A.P0c + pb, nullptr};
+      for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x)
+        for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
+          A.pbar[pb + p] = gl * aL[i] * bL[A.csr_jf[pb + p] & kIdxMask] * A.cs[pb + p];
+      cl.sync();
+      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem);
+    }
+    __syncthreads();
+    row_soft_rev(A, b, sr);
+    cl.sync();
+    col_soft_rev(A, b, sc);
+    cl.sync();
+  }
+  grad_rows(A, b, sr);
+}
+
+}  // namespace apml
