@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -180,7 +181,7 @@ void plan_sparse(apml_ctx* c) {
   while (cl0 * 2 <= 8 && (int64_t)cl0 * 2 * B <= num_sms() && cl0 * 2 <= nmin) cl0 *= 2;
   auto need = [&](int cl, bool rep) {
     const int64_t nr = (N + cl - 1) / cl, nc = (M + cl - 1) / cl, e = (est + cl - 1) / cl;
-    size_t r = rep ? 4 * (size_t)(N + M) + 32 : 0;
+    size_t r = rep ? 4 * (size_t)(N + M) + 8 * (size_t)M + 48 : 0;  // replicas + staged b^l (x2)
     return r + 4 * (size_t)(nr + nc) + 32 + slice_bytes_h(nr, e, idx, true) + slice_bytes_h(nc, e, idx, false);
   };
   c->cl = cl0;
@@ -264,12 +265,41 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.rowback = c->rowback; a.colback = c->colback;
   a.loss = loss; a.grad_loss = grad_loss; a.grad_pred = grad_pred;
   a.smem_bytes = c->smem_bytes; a.rep_smem = c->rep_smem;
+  a.dbg = nullptr;
   return a;
+}
+
+// APML_PHASES=1: per-phase globaltimer stamps of the sparse megakernels, averaged over CTAs
+// and printed to stderr (diagnostics only; synchronises).
+bool phases_on() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("APML_PHASES"); v = (e && e[0] == '1') ? 1 : 0; }
+  return v == 1;
+}
+void print_phases(const char* name, const unsigned long long* d, int grid, int n) {
+  std::vector<unsigned long long> h((size_t)grid * 16);
+  cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
+  std::string out = std::string("[apml phases] ") + name + " us:";
+  for (int k = 1; k < n; ++k) {
+    double s = 0;
+    for (int g = 0; g < grid; ++g) s += (double)(h[g * 16 + k] - h[g * 16 + k - 1]);
+    out += " " + std::to_string(s / grid / 1e3);
+  }
+  fprintf(stderr, "%s\n", out.c_str());
 }
 
 // One cluster of c->cl CTAs per pair.
 template <typename K>
-apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a, cudaStream_t s) {
+apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a0, cudaStream_t s,
+                           const char* name = "", int nphase = 0) {
+  SparseArgs a = a0;
+  unsigned long long* dbg = nullptr;
+  const int grid = (int)(c->B * c->cl);
+  if (phases_on() && nphase) {
+    CK(cudaMalloc(&dbg, (size_t)grid * 16 * 8));
+    CK(cudaMemset(dbg, 0, (size_t)grid * 16 * 8));
+    a.dbg = dbg;
+  }
   CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_bytes));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(c->B * c->cl), 1, 1);
@@ -284,6 +314,11 @@ apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a, cud
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CK(cudaLaunchKernelEx(&cfg, kernel, a));
+  if (dbg) {
+    CK(cudaStreamSynchronize(s));
+    print_phases(name, dbg, grid, nphase);
+    cudaFree(dbg);
+  }
   return APML_OK;
 }
 
@@ -320,8 +355,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
 
 apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
   const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
-  apml_status st = c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream)
-                            : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream);
+  apml_status st = c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream, "fwd", 9)
+                            : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream, "fwd", 9);
   mark(c, 6, c->stream);
   c->launches += 1;
   return st;
@@ -436,8 +471,8 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
   mark(x, 7, s);
   x->bwd_timed = x->timing;
   const SparseArgs a = sparse_args(x, nullptr, grad_loss, grad_pred);
-  apml_status st = x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s)
-                            : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s);
+  apml_status st = x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s, "bwd", 6)
+                            : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s, "bwd", 6);
   if (st != APML_OK) return st;
   mark(x, 8, s);
   x->launches += 1;

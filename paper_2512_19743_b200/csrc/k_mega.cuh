@@ -75,7 +75,16 @@ struct SparseArgs {
   float* grad_pred;
   size_t smem_bytes;
   int rep_smem;
+  unsigned long long* dbg;  // optional phase timestamps [grid][16] (APML_PHASES=1), else NULL
 };
+
+__device__ __forceinline__ void phase(const SparseArgs& A, int k) {
+  if (A.dbg && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.dbg[blockIdx.x * 16 + k] = t;
+  }
+}
 
 struct Slice {
   int lo, hi;
@@ -134,7 +143,9 @@ __device__ void cluster_scan(cg::cluster_group& cl, unsigned* cnt, unsigned* ptr
   __syncthreads();  // s_tot / s_warp reused by the next scan
 }
 
-// Warp per line rank sort (keys inside a line are distinct).
+constexpr uint32_t kRegLine = 16;  // lines up to this length are sorted in registers by one thread
+
+// Warp per line rank sort of the lines longer than kRegLine (keys inside a line are distinct).
 template <bool kRows>
 __device__ void sort_lines(const SparseArgs& A, int b, Slice s) {
   const size_t pb = (size_t)b * A.cap;
@@ -145,6 +156,7 @@ __device__ void sort_lines(const SparseArgs& A, int b, Slice s) {
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int line = s.lo + (threadIdx.x >> 5); line < s.hi; line += nw) {
     const uint32_t beg = ptr[line], end = ptr[line + 1], L = end - beg;
+    if (L <= kRegLine) continue;
     auto key_of = [&](uint32_t t) -> uint32_t { return kRows ? (e[t].y & kIdxMask) : e[t].x; };
     auto place = [&](uint32_t t, uint32_t rank) {
       const uint32_t pos = beg + rank;
@@ -177,11 +189,13 @@ __device__ void sort_lines(const SparseArgs& A, int b, Slice s) {
 // ---------------------------------------------------------------- normalisation
 
 // Row softmax on the kept support (thread per row): d2, c, P_row, argmin / second argmin.
+// Long rows only (the others are done in registers by row_sort_norm_regs).
 __device__ void row_norm(const SparseArgs& A, int b, Slice s) {
   const int N = A.N, M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
   for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+    if (rp[i + 1] - rp[i] <= kRegLine) continue;
     const float4 x = A.pred4[(size_t)b * N + i];
     const LineA la = A.rowA[(size_t)b * N + i];
     const LineB lb = A.rowB[(size_t)b * N + i];
@@ -210,12 +224,13 @@ __device__ void row_norm(const SparseArgs& A, int b, Slice s) {
   }
 }
 
-// Column softmax + symmetrisation (thread per column).
+// Column softmax + symmetrisation (thread per column).  Long columns only.
 __device__ void col_norm(const SparseArgs& A, int b, Slice s) {
   const int M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
   for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+    if (cp[j + 1] - cp[j] <= kRegLine) continue;
     const LineA la = A.colA[(size_t)b * M + j];
     const LineB lb = A.colB[(size_t)b * M + j];
     int ia = -1, ib = -1;
@@ -238,6 +253,148 @@ __device__ void col_norm(const SparseArgs& A, int b, Slice s) {
       const float p0 = 0.5f * (A.prow[pb + p] + pc);
       A.P0[pb + p] = p0;
       A.P0c[pb + q] = p0;
+    }
+    A.colidx[(size_t)b * M + j] = make_int2(ia, ib);
+  }
+}
+
+// Thread per row, row length <= kRegLine: rank-sort the row's entries by j in registers,
+// write the CSR row (+ entry -> CSR position), then the row softmax in sorted order.
+__device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
+  const int N = A.N, M = A.M;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+    const uint32_t beg = rp[i], L = rp[i + 1] - beg;
+    if (L > kRegLine) continue;
+    uint32_t t[kRegLine], jf[kRegLine], rk[kRegLine], sj[kRegLine];
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? A.ebuf[pb + t[k]].y : 0xffffffffu;
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) {
+      uint32_t r = 0;
+#pragma unroll
+      for (uint32_t f = 0; f < kRegLine; ++f) r += ((jf[f] & kIdxMask) < (jf[k] & kIdxMask)) ? 1u : 0u;
+      rk[k] = r;  // padded entries (key = mask) rank L and never precede a real key
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k)
+      if (k < L) { A.csr_jf[pb + beg + rk[k]] = jf[k]; A.inv[pb + t[k]] = beg + rk[k]; }
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      uint32_t v = 0u;
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) v = rk[k] == r ? jf[k] : v;
+      sj[r] = v;
+    }
+    const float4 x = A.pred4[(size_t)b * N + i];
+    const LineA la = A.rowA[(size_t)b * N + i];
+    const LineB lb = A.rowB[(size_t)b * N + i];
+    float d2v[kRegLine], cv[kRegLine];
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      if (r < L) {
+        const float4 y = A.gt4[(size_t)b * M + (sj[r] & kIdxMask)];
+        d2v[r] = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+        cv[r] = __fsqrt_rn(d2v[r]);
+      }
+    }
+    int ia = -1, ib = -1;
+    float Z = 0.f;
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      if (r < L) {
+        const int j = (int)(sj[r] & kIdxMask);
+        if (ia < 0 && d2v[r] == la.m2) ia = j;
+        else if (ib < 0 && d2v[r] == la.s2) ib = j;
+        float sv = 0.f;
+        if (sj[r] & kFlagRow) {
+          sv = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (cv[r] - lb.m));
+          Z += sv;
+        }
+        A.d2s[pb + beg + r] = d2v[r];
+        A.cs[pb + beg + r] = cv[r];
+        cv[r] = sv;  // reuse: unnormalised similarity
+      }
+    }
+    const float iz = 1.f / Z;
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r)
+      if (r < L) A.prow[pb + beg + r] = cv[r] * iz;
+    A.rowidx[(size_t)b * N + i] = make_int2(ia, ib);
+  }
+}
+
+// Thread per column, length <= kRegLine: rank-sort by i in registers, write the CSC column
+// (+ CSR position of each entry), column softmax, P0 = (P_row + P_col)/2 in both orders.
+__device__ void col_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
+  const int M = A.M;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+    const uint32_t beg = cp[j], L = cp[j + 1] - beg;
+    if (L > kRegLine) continue;
+    uint32_t t[kRegLine], key[kRegLine], pp[kRegLine], rk[kRegLine];
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csc_t[pb + beg + k] : 0u;
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) {
+      key[k] = k < L ? A.ebuf[pb + t[k]].x : 0xffffffffu;
+      pp[k] = k < L ? A.inv[pb + t[k]] : 0u;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) {
+      uint32_t r = 0;
+#pragma unroll
+      for (uint32_t f = 0; f < kRegLine; ++f) r += (key[f] < key[k]) ? 1u : 0u;
+      rk[k] = r;
+    }
+    uint32_t si[kRegLine], sp[kRegLine];
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      uint32_t vi = 0u, vp = 0u;
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) {
+        vi = rk[k] == r ? key[k] : vi;
+        vp = rk[k] == r ? pp[k] : vp;
+      }
+      si[r] = vi;
+      sp[r] = vp;
+    }
+    const LineA la = A.colA[(size_t)b * M + j];
+    const LineB lb = A.colB[(size_t)b * M + j];
+    float sv[kRegLine];
+    int ia = -1, ib = -1;
+    float Z = 0.f;
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      if (r < L) {
+        const float d2 = A.d2s[pb + sp[r]];
+        const uint32_t fl = A.csr_jf[pb + sp[r]];
+        A.csc_i[pb + beg + r] = si[r];
+        A.csc_perm[pb + beg + r] = sp[r];
+        if (ia < 0 && d2 == la.m2) ia = (int)si[r];
+        else if (ib < 0 && d2 == la.s2) ib = (int)si[r];
+        float e = 0.f;
+        if (fl & kFlagCol) {
+          e = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + sp[r]] - lb.m));
+          Z += e;
+        }
+        sv[r] = e;
+      }
+    }
+    const float iz = 1.f / Z;
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      if (r < L) {
+        const float pc = sv[r] * iz;
+        A.pcol[pb + sp[r]] = pc;
+        const float p0 = 0.5f * (A.prow[pb + sp[r]] + pc);
+        A.P0[pb + sp[r]] = p0;
+        A.P0c[pb + beg + r] = p0;
+      }
     }
     A.colidx[(size_t)b * M + j] = make_int2(ia, ib);
   }
@@ -349,10 +506,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   unsigned* cc = A.col_cnt + (size_t)b * (M + 1);
   unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
   unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  phase(A, 0);
   // S4: counts -> offsets ("exclusive prefix sum"), then bucket the entries
   cluster_scan(cl, rc, rp, N, sr, s_tot_r, s_warp);
   cluster_scan(cl, cc, cp, M, sc, s_tot_c, s_warp);
   cl.sync();
+  phase(A, 1);
   for (uint32_t t = rank * blockDim.x + threadIdx.x; t < total; t += CL * blockDim.x) {
     const uint2 e = A.ebuf[pb + t];
     const uint32_t i = e.x, j = e.y & kIdxMask;
@@ -360,14 +519,25 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     A.csc_t[pb + cp[j] + atomicAdd(cc + j, 1u)] = t;
   }
   cl.sync();
+  phase(A, 2);
+  // rows: sort by j (registers for short rows, warp rank sort for long ones) and the row
+  // softmax (S5) on the kept support
+  row_sort_norm_regs(A, b, sr);
+  __syncthreads();
   sort_lines<true>(A, b, sr);
-  cl.sync();
-  sort_lines<false>(A, b, sc);
-  // S5: directional softmax on the kept supports, symmetrisation
+  __syncthreads();
   row_norm(A, b, sr);
   cl.sync();
+  phase(A, 3);
+  // columns: sort by i, column softmax, symmetrisation P0 = (P_row + P_col)/2
+  col_sort_norm_regs(A, b, sc);
+  __syncthreads();
+  sort_lines<false>(A, b, sc);
+  __syncthreads();
   col_norm(A, b, sc);
   cl.sync();
+  phase(A, 4);
+  phase(A, 5);
   // S6: Sinkhorn.  Replicas of a and b (full length) + own CSR / CSC slices in shared memory.
   uint8_t* sm = shm;
   float *a, *bv;
@@ -393,13 +563,16 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     const SliceView<IdxT> R = stage_slice<IdxT>(sm, rp, sr, A.csr_jf + pb, A.P0 + pb, false);
     const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
     cl.sync();
+    phase(A, 6);
     sinkhorn_fwd<IdxT>(cl, A, b, sr, sc, R, C, a, bv, A.rep_smem);
   } else {
     const SliceView<uint32_t> R{rp + sr.lo, A.csr_jf + pb, A.P0 + pb, nullptr};
     const SliceView<uint32_t> C{cp + sc.lo, A.csc_i + pb, A.P0c + pb, nullptr};
     cl.sync();
+    phase(A, 6);
     sinkhorn_fwd<uint32_t>(cl, A, b, sr, sc, R, C, a, bv, A.rep_smem);
   }
+  phase(A, 7);
   // S7: loss_b = sum_i a_i sum_j P0_ij b_j c_ij over own rows, then cluster reduction in rank order
   double acc = 0.0;
   for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
@@ -424,18 +597,36 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     for (int r = 0; r < CL; ++r) t += s_part[r];
     A.loss[b] = (float)t;
   }
+  phase(A, 8);
 }
 
 // ---------------------------------------------------------------- backward
 
+constexpr int kPf = 8;  // b^l prefetch registers per thread (bls staging needs M <= kPf * blockDim)
+
 template <typename IdxT>
 __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* ab, float* bb,
-                             float* rcur, float* qcur, bool rep_smem) {
+                             float* rcur, float* qcur, bool rep_smem, float* bls) {
   const int N = A.N, M = A.M, L = A.L;
   const float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   const float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+  // bls (2 x M floats, shared memory, optional): b^l staged for the P0bar gathers, double
+  // buffered -- b^{l-1} is loaded into registers at the top of iteration l and stored after it.
+  if (bls) {
+    for (int k = threadIdx.x; k < M; k += blockDim.x) bls[(L & 1) * M + k] = bh[(size_t)L * M + k];
+    __syncthreads();
+  }
   for (int l = L; l >= 1; --l) {
+    float pf[kPf];
+    if (bls && l > 1) {
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        const int k = threadIdx.x + u * blockDim.x;
+        pf[u] = k < M ? bh[(size_t)(l - 1) * M + k] : 0.f;
+      }
+    }
+    const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;
     // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
     // P0bar_ij += Rbar^l_i b^l_j
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
@@ -445,7 +636,7 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       const float Rb = -ab[k] * al * al;
       ab[k] = ab[k] * A.eps * r * r;
       push_rep(cl, rcur, i, Rb, rep_smem);
-      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += Rb * bh[(size_t)l * M + R.col(p)];
+      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += Rb * bcur[R.col(p)];
     }
     cl.sync();
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
@@ -472,8 +663,16 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       }
       ab[k] = (float)((double)ab[k] + t);
     }
-    // no barrier needed: the next row step touches only this thread's rows and rcur, which
-    // no CTA reads until after the next cl.sync()
+    // the next row step touches only this thread's rows and rcur (read by no CTA before the
+    // next cl.sync); only the staged b^{l-1} needs a CTA barrier
+    if (bls && l > 1) {
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        const int k = threadIdx.x + u * blockDim.x;
+        if (k < M) bls[((l - 1) & 1) * M + k] = pf[u];
+      }
+      __syncthreads();
+    }
   }
   cl.sync();
 }
@@ -596,6 +795,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     }
     return;
   }
+  phase(A, 0);
   if (A.full) {
     const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
     const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
@@ -613,6 +813,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     }
     float* ab = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sr.hi - sr.lo)));
     float* bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
+    float* bls = nullptr;
+    if (A.rep_smem && M <= kPf * (int)blockDim.x) bls = reinterpret_cast<float*>(carve(sm, 8 * (size_t)M));
     // abar = gl sum_j P0 b^L c, bbar = gl sum_i a^L P0 c   (loss = sum a P0 b c)
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       double t = 0.0;
@@ -640,7 +842,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
           R.acc[p] = gl * aL[i] * bL[R.col(p)] * A.cs[pb + rp[sr.lo] + p];
       }
       cl.sync();
-      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem);
+      phase(A, 1);
+      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem, bls);
       const uint32_t base = rp[sr.lo], cnt = rp[sr.hi] - base;
       for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) A.pbar[pb + base + k] = R.acc[k];
     } else {
@@ -650,15 +853,20 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
         for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
           A.pbar[pb + p] = gl * aL[i] * bL[A.csr_jf[pb + p] & kIdxMask] * A.cs[pb + p];
       cl.sync();
-      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem);
+      phase(A, 1);
+      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem, bls);
     }
     __syncthreads();
+    phase(A, 2);
     row_soft_rev(A, b, sr);
     cl.sync();
+    phase(A, 3);
     col_soft_rev(A, b, sc);
     cl.sync();
+    phase(A, 4);
   }
   grad_rows(A, b, sr);
+  phase(A, 5);
 }
 
 }  // namespace apml
