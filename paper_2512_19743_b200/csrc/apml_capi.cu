@@ -173,7 +173,7 @@ void plan_sparse(apml_ctx* c) {
   const int64_t B = c->B, N = c->N, M = c->M;
   c->idx16 = N <= 65536 && M <= 65536;
   const size_t idx = c->idx16 ? 2 : 4;
-  const size_t mx = (size_t)max_smem_optin() - 2048;  // static shared memory headroom
+  const size_t mx = (size_t)max_smem_optin() - 12 * 1024;  // static shared memory (long-line lists)
   // typical union support ~5 entries per point of the larger cloud
   const int64_t est = std::min<int64_t>((int64_t)c->cap, 5 * std::max(N, M) + 64);
   const int64_t nmin = std::min(N, M);
@@ -192,7 +192,10 @@ void plan_sparse(apml_ctx* c) {
   if (!done)
     for (int cl = cl0; cl <= 8 && !done && cl <= nmin; cl *= 2)
       if (need(cl, false) <= mx) { c->cl = cl; done = true; }
-  c->smem_bytes = std::min(mx, need(c->cl, c->rep_smem != 0));
+  // One wave (every CTA resident at once): take the whole shared memory so that no CTA's
+  // slice falls back to global memory.  Otherwise leave ~30% headroom over the estimate.
+  if (B * c->cl <= num_sms()) c->smem_bytes = mx;
+  else c->smem_bytes = std::min(mx, need(c->cl, c->rep_smem != 0) * 13 / 10);
 }
 
 apml_status build_ctx(apml_ctx* c, uint32_t cap) {

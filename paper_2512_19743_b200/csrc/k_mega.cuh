@@ -144,17 +144,50 @@ __device__ void cluster_scan(cg::cluster_group& cl, unsigned* cnt, unsigned* ptr
 }
 
 constexpr uint32_t kRegLine = 16;  // lines up to this length are sorted in registers by one thread
+constexpr int kLongCap = 1024;     // per-CTA list of longer lines (warp per line)
+
+// The lines of a slice longer than kRegLine, collected once so that warp-per-line passes do
+// not walk (and load the offsets of) every line of the slice.
+struct LongList {
+  const uint32_t* idx;
+  int n, lo, hi;
+  bool all;  // list overflowed: walk the whole slice
+  __device__ __forceinline__ int count() const { return all ? hi - lo : n; }
+  __device__ __forceinline__ int line(int k) const { return all ? lo + k : (int)idx[k]; }
+};
+
+__device__ LongList collect_long(const unsigned* ptr, Slice s, uint32_t* list, int* cnt) {
+  if (threadIdx.x == 0) *cnt = 0;
+  __syncthreads();
+  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x)
+    if (ptr[i + 1] - ptr[i] > kRegLine) {
+      const int k = atomicAdd(cnt, 1);
+      if (k < kLongCap) list[k] = (uint32_t)i;
+    }
+  __syncthreads();
+  const int n = *cnt;
+  return LongList{list, n < kLongCap ? n : kLongCap, s.lo, s.hi, n > kLongCap};
+}
+
+// G == 1: thread per line over the whole slice (short lines are its business);
+// G == 32: warp per line over the long-line list.
+#define APML_FOR_LINES(G, s, ll, var)                                                              \
+  for (int _k = (G == 1 ? (int)threadIdx.x : (int)(threadIdx.x >> 5)),                             \
+           _n = (G == 1 ? (s).hi - (s).lo : (ll).count());                                         \
+       _k < _n; _k += (G == 1 ? (int)blockDim.x : (int)(blockDim.x >> 5)))                         \
+    if (const int var = (G == 1 ? (s).lo + _k : (ll).line(_k)); true)
 
 // Warp per line rank sort of the lines longer than kRegLine (keys inside a line are distinct).
 template <bool kRows>
-__device__ void sort_lines(const SparseArgs& A, int b, Slice s) {
+__device__ void sort_lines(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const size_t pb = (size_t)b * A.cap;
   const int n = kRows ? A.N : A.M;
   const unsigned* ptr = (kRows ? A.row_ptr : A.col_ptr) + (size_t)b * (n + 1);
   const uint32_t* seg_t = (kRows ? A.csr_t : A.csc_t) + pb;
   const uint2* e = A.ebuf + pb;
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int line = s.lo + (threadIdx.x >> 5); line < s.hi; line += nw) {
+  (void)nw;
+  APML_FOR_LINES(32, s, ll, line) {
     const uint32_t beg = ptr[line], end = ptr[line + 1], L = end - beg;
     if (L <= kRegLine) continue;
     auto key_of = [&](uint32_t t) -> uint32_t { return kRows ? (e[t].y & kIdxMask) : e[t].x; };
@@ -188,63 +221,98 @@ __device__ void sort_lines(const SparseArgs& A, int b, Slice s) {
 
 // ---------------------------------------------------------------- normalisation
 
-// Row softmax on the kept support (thread per row): d2, c, P_row, argmin / second argmin.
-// Long rows only (the others are done in registers by row_sort_norm_regs).
-__device__ void row_norm(const SparseArgs& A, int b, Slice s) {
+// Deterministic sum over a group of G lanes (butterfly: every lane ends with the same bits).
+template <int G, typename T>
+__device__ __forceinline__ T gsum(T v) {
+  if (G > 1) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  }
+  return v;
+}
+
+// First and second match in sorted line order (argmin = first entry with d2 == m2; second
+// argmin = first other entry with d2 == s2), warp-cooperative over a 32-entry chunk.
+__device__ __forceinline__ void first_two(unsigned bal_m, unsigned bal_s, int& ka, int& kb, int chunk0) {
+  if (ka < 0 && bal_m) {
+    const int f = __ffs(bal_m) - 1;
+    ka = chunk0 + f;
+    bal_s &= ~(1u << f);
+  }
+  if (kb < 0 && bal_s) kb = chunk0 + __ffs(bal_s) - 1;
+}
+
+// Row softmax on the kept support for rows longer than kRegLine: one warp per row, 32
+// entries per step (the short rows are done in registers by row_sort_norm_regs).
+__device__ void row_norm(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const int N = A.N, M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
-  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
-    if (rp[i + 1] - rp[i] <= kRegLine) continue;
+  const int lane = threadIdx.x & 31;
+  APML_FOR_LINES(32, s, ll, i) {
+    const uint32_t beg = rp[i], end = rp[i + 1];
+    if (end - beg <= kRegLine) continue;
     const float4 x = A.pred4[(size_t)b * N + i];
     const LineA la = A.rowA[(size_t)b * N + i];
     const LineB lb = A.rowB[(size_t)b * N + i];
-    int ia = -1, ib = -1;
+    int ka = -1, kb = -1;
     float Z = 0.f;
-    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const uint32_t jf = A.csr_jf[pb + p];
-      const uint32_t j = jf & kIdxMask;
-      const float4 y = A.gt4[(size_t)b * M + j];
-      const float d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
-      const float c = __fsqrt_rn(d2);
-      A.d2s[pb + p] = d2;
-      A.cs[pb + p] = c;
-      if (ia < 0 && d2 == la.m2) ia = (int)j;
-      else if (ib < 0 && d2 == la.s2) ib = (int)j;
-      float sv = 0.f;
-      if (jf & kFlagRow) {
-        sv = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (c - lb.m));
+    for (uint32_t p0 = beg; p0 < end; p0 += 32) {
+      const uint32_t p = p0 + lane;
+      const bool v = p < end;
+      uint32_t jf = 0;
+      float d2 = 0.f, sv = 0.f;
+      if (v) {
+        jf = A.csr_jf[pb + p];
+        const float4 y = A.gt4[(size_t)b * M + (jf & kIdxMask)];
+        d2 = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
+        const float c = __fsqrt_rn(d2);
+        A.d2s[pb + p] = d2;
+        A.cs[pb + p] = c;
+        if (jf & kFlagRow) sv = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (c - lb.m));
+        A.prow[pb + p] = sv;
         Z += sv;
       }
-      A.prow[pb + p] = sv;
+      first_two(__ballot_sync(0xffffffffu, v && d2 == la.m2), __ballot_sync(0xffffffffu, v && d2 == la.s2),
+                ka, kb, (int)(p0 - beg));
     }
-    const float iz = 1.f / Z;
-    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) A.prow[pb + p] *= iz;
-    A.rowidx[(size_t)b * N + i] = make_int2(ia, ib);
+    const float iz = 1.f / gsum<32>(Z);
+    for (uint32_t p = beg + lane; p < end; p += 32) A.prow[pb + p] *= iz;
+    if (lane == 0) {
+      const int ja = ka >= 0 ? (int)(A.csr_jf[pb + beg + ka] & kIdxMask) : -1;
+      const int jb = kb >= 0 ? (int)(A.csr_jf[pb + beg + kb] & kIdxMask) : -1;
+      A.rowidx[(size_t)b * N + i] = make_int2(ja, jb);
+    }
   }
 }
 
-// Column softmax + symmetrisation (thread per column).  Long columns only.
-__device__ void col_norm(const SparseArgs& A, int b, Slice s) {
+// Column softmax + symmetrisation for columns longer than kRegLine (warp per column).
+__device__ void col_norm(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const int M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
-  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
-    if (cp[j + 1] - cp[j] <= kRegLine) continue;
+  const int lane = threadIdx.x & 31;
+  APML_FOR_LINES(32, s, ll, j) {
+    const uint32_t beg = cp[j], end = cp[j + 1];
+    if (end - beg <= kRegLine) continue;
     const LineA la = A.colA[(size_t)b * M + j];
     const LineB lb = A.colB[(size_t)b * M + j];
-    int ia = -1, ib = -1;
+    int ka = -1, kb = -1;
     float Z = 0.f;
-    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
-      const uint32_t p = A.csc_perm[pb + q];
-      const float d2 = A.d2s[pb + p];
-      const uint32_t i = A.csc_i[pb + q];
-      if (ia < 0 && d2 == la.m2) ia = (int)i;
-      else if (ib < 0 && d2 == la.s2) ib = (int)i;
-      if (A.csr_jf[pb + p] & kFlagCol) Z += (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m));
+    for (uint32_t q0 = beg; q0 < end; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const bool v = q < end;
+      float d2 = 0.f;
+      if (v) {
+        const uint32_t p = A.csc_perm[pb + q];
+        d2 = A.d2s[pb + p];
+        if (A.csr_jf[pb + p] & kFlagCol) Z += (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m));
+      }
+      first_two(__ballot_sync(0xffffffffu, v && d2 == la.m2), __ballot_sync(0xffffffffu, v && d2 == la.s2),
+                ka, kb, (int)(q0 - beg));
     }
-    const float iz = 1.f / Z;
-    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+    const float iz = 1.f / gsum<32>(Z);
+    for (uint32_t q = beg + lane; q < end; q += 32) {
       const uint32_t p = A.csc_perm[pb + q];
       float pc = 0.f;
       if (A.csr_jf[pb + p] & kFlagCol)
@@ -254,7 +322,11 @@ __device__ void col_norm(const SparseArgs& A, int b, Slice s) {
       A.P0[pb + p] = p0;
       A.P0c[pb + q] = p0;
     }
-    A.colidx[(size_t)b * M + j] = make_int2(ia, ib);
+    if (lane == 0) {
+      const int ia = ka >= 0 ? (int)A.csc_i[pb + beg + ka] : -1;
+      const int ib = kb >= 0 ? (int)A.csc_i[pb + beg + kb] : -1;
+      A.colidx[(size_t)b * M + j] = make_int2(ia, ib);
+    }
   }
 }
 
@@ -442,44 +514,90 @@ __device__ __forceinline__ size_t slice_bytes(int nl, uint32_t cnt, size_t idx_b
          ((4 * (size_t)cnt + 15) & ~size_t(15)) + (acc ? ((4 * (size_t)cnt + 15) & ~size_t(15)) : 0);
 }
 
-// Push v into element k of the replica `rep` in every CTA of the cluster (or once, when the
-// replica lives in global memory).
-__device__ __forceinline__ void push_rep(cg::cluster_group& cl, float* rep, int k, float v, bool smem) {
-  if (!smem) { rep[k] = v; return; }
-  const int CL = cl.num_blocks();
-  for (int r = 0; r < CL; ++r) cl.map_shared_rank(rep, r)[k] = v;
+// ---------------------------------------------------------------- replica exchange
+//
+// After a CTA computes the new values of its own slice of a scaling vector it writes them
+// into the replica of every CTA of the cluster with st.async (DSMEM), each store signalling
+// the destination's mbarrier (complete_tx); a CTA then waits on its own mbarrier for the
+// whole vector (4 n bytes).  No cluster barrier (and hence no MEMBAR.GPU) per half-step.
+// Reuse safety is causal: a CTA's push of the next vector depends on its reads of the
+// current replica, and nobody can produce vector v+1 before receiving all of vector v.
+// When the replicas live in global memory the exchange degrades to a store + cluster
+// barrier.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+struct Xchg {
+  float* rep;      // replica (shared) or the single global copy
+  uint32_t mbar;   // shared address of this CTA's mbarrier for the vector
+  int n;           // vector length
+  bool smem;
+  uint32_t phase;  // parity of the next completion
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void xchg_begin(const Xchg& x) {
+  if (x.smem && threadIdx.x == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(x.mbar), "r"(4u * (uint32_t)x.n) : "memory");
+}
+__device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) {
+  if (!x.smem) { x.rep[k] = v; return; }
+  const uint32_t a = smem_addr(x.rep + k);
+  for (int r = 0; r < CL; ++r)
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 :: "r"(map_rank(a, r)), "r"(__float_as_uint(v)), "r"(map_rank(x.mbar, r)) : "memory");
+}
+__device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x) {
+  if (!x.smem) { cl.sync(); return; }
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(x.mbar), "r"(x.phase) : "memory");
+  x.phase ^= 1u;
 }
 
 // ---------------------------------------------------------------- forward Sinkhorn + loss
 
 template <typename IdxT>
 __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
-                             const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* a, float* bv,
-                             bool rep_smem) {
-  const int N = A.N, M = A.M, L = A.L;
+                             const SliceView<IdxT>& R, const SliceView<IdxT>& C, Xchg& xa, Xchg& xb) {
+  const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks();
   float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+  const float* a = xa.rep;
+  const float* bv = xb.rep;
   for (int l = 1; l <= L; ++l) {
+    xchg_begin(xb);
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {  // Eq. (3): colsum = b_j Q_j
       const int k = j - sc.lo;
       float Q = 0.f;
       for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) Q = __fmaf_rn(a[C.col(q)], C.val[q], Q);
       const float bj = bv[j];
       const float nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
+      xchg_put(xb, CL, j, nb);
       bh[(size_t)l * M + j] = nb;
-      push_rep(cl, bv, j, nb, rep_smem);
     }
-    cl.sync();
+    xchg_end(cl, xb);
+    xchg_begin(xa);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {  // Eq. (4): rowsum = a_i R_i
       const int k = i - sr.lo;
       float Rs = 0.f;
       for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) Rs = __fmaf_rn(R.val[p], bv[R.col(p)], Rs);
       const float ai = a[i];
       const float na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+      xchg_put(xa, CL, i, na);
       ah[(size_t)l * N + i] = na;
-      push_rep(cl, a, i, na, rep_smem);
     }
-    cl.sync();
+    xchg_end(cl, xa);
   }
 }
 
@@ -491,6 +609,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   __shared__ unsigned s_tot_r[kMaxCluster], s_tot_c[kMaxCluster];  // one per scan (no reuse race)
   __shared__ unsigned s_warp[32];
   __shared__ double s_part[kMaxCluster];
+  __shared__ uint32_t s_long_r[kLongCap], s_long_c[kLongCap];
+  __shared__ int s_nlong[2];
   cg::cluster_group cl = cg::this_cluster();
   const int CL = cl.num_blocks(), rank = cl.block_rank();
   const int b = blockIdx.x / CL;
@@ -522,30 +642,38 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   phase(A, 2);
   // rows: sort by j (registers for short rows, warp rank sort for long ones) and the row
   // softmax (S5) on the kept support
+  const LongList llr = collect_long(rp, sr, s_long_r, &s_nlong[0]);
+  const LongList llc = collect_long(cp, sc, s_long_c, &s_nlong[1]);
   row_sort_norm_regs(A, b, sr);
   __syncthreads();
-  sort_lines<true>(A, b, sr);
+  sort_lines<true>(A, b, sr, llr);
   __syncthreads();
-  row_norm(A, b, sr);
+  row_norm(A, b, sr, llr);
   cl.sync();
   phase(A, 3);
   // columns: sort by i, column softmax, symmetrisation P0 = (P_row + P_col)/2
   col_sort_norm_regs(A, b, sc);
   __syncthreads();
-  sort_lines<false>(A, b, sc);
+  sort_lines<false>(A, b, sc, llc);
   __syncthreads();
-  col_norm(A, b, sc);
+  col_norm(A, b, sc, llc);
   cl.sync();
   phase(A, 4);
   phase(A, 5);
   // S6: Sinkhorn.  Replicas of a and b (full length) + own CSR / CSC slices in shared memory.
   uint8_t* sm = shm;
   float *a, *bv;
+  __shared__ __align__(8) unsigned long long s_mbar[2];
   if (A.rep_smem) {
     a = reinterpret_cast<float*>(carve(sm, 4 * (size_t)N));
     bv = reinterpret_cast<float*>(carve(sm, 4 * (size_t)M));
     for (int k = threadIdx.x; k < N; k += blockDim.x) a[k] = 1.f;
     for (int k = threadIdx.x; k < M; k += blockDim.x) bv[k] = 1.f;
+    if (threadIdx.x == 0) {
+      mbar_init(smem_addr(&s_mbar[0]));
+      mbar_init(smem_addr(&s_mbar[1]));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
   } else {
     a = A.gvec + (size_t)b * 2 * (N + M);
     bv = a + N;
@@ -556,6 +684,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   float* bh = A.b_hist + (size_t)b * (L + 1) * M;
   for (int k = sr.lo + threadIdx.x; k < sr.hi; k += blockDim.x) ah[k] = 1.f;
   for (int k = sc.lo + threadIdx.x; k < sc.hi; k += blockDim.x) bh[k] = 1.f;
+  Xchg xa{a, smem_addr(&s_mbar[0]), N, A.rep_smem != 0, 0u};
+  Xchg xb{bv, smem_addr(&s_mbar[1]), M, A.rep_smem != 0, 0u};
   const size_t used = (size_t)(sm - shm);
   const bool fit = used + slice_bytes(sr.hi - sr.lo, rp[sr.hi] - rp[sr.lo], sizeof(IdxT), false) +
                        slice_bytes(sc.hi - sc.lo, cp[sc.hi] - cp[sc.lo], sizeof(IdxT), false) <= A.smem_bytes;
@@ -564,13 +694,13 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
     cl.sync();
     phase(A, 6);
-    sinkhorn_fwd<IdxT>(cl, A, b, sr, sc, R, C, a, bv, A.rep_smem);
+    sinkhorn_fwd<IdxT>(cl, A, b, sr, sc, R, C, xa, xb);
   } else {
     const SliceView<uint32_t> R{rp + sr.lo, A.csr_jf + pb, A.P0 + pb, nullptr};
     const SliceView<uint32_t> C{cp + sc.lo, A.csc_i + pb, A.P0c + pb, nullptr};
     cl.sync();
     phase(A, 6);
-    sinkhorn_fwd<uint32_t>(cl, A, b, sr, sc, R, C, a, bv, A.rep_smem);
+    sinkhorn_fwd<uint32_t>(cl, A, b, sr, sc, R, C, xa, xb);
   }
   phase(A, 7);
   // S7: loss_b = sum_i a_i sum_j P0_ij b_j c_ij over own rows, then cluster reduction in rank order
@@ -607,10 +737,12 @@ constexpr int kPf = 8;  // b^l prefetch registers per thread (bls staging needs 
 template <typename IdxT>
 __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* ab, float* bb,
-                             float* rcur, float* qcur, bool rep_smem, float* bls) {
-  const int N = A.N, M = A.M, L = A.L;
+                             Xchg& xr, Xchg& xq, float* bls) {
+  const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks();
   const float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   const float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+  const float* rcur = xr.rep;
+  const float* qcur = xq.rep;
   // bls (2 x M floats, shared memory, optional): b^l staged for the P0bar gathers, double
   // buffered -- b^{l-1} is loaded into registers at the top of iteration l and stored after it.
   if (bls) {
@@ -629,42 +761,44 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;
     // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
     // P0bar_ij += Rbar^l_i b^l_j
+    xchg_begin(xr);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
       const float al = ah[(size_t)l * N + i], alm = ah[(size_t)(l - 1) * N + i];
       const float r = al / alm;
       const float Rb = -ab[k] * al * al;
       ab[k] = ab[k] * A.eps * r * r;
-      push_rep(cl, rcur, i, Rb, rep_smem);
+      xchg_put(xr, CL, i, Rb);
       for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += Rb * bcur[R.col(p)];
     }
-    cl.sync();
+    xchg_end(cl, xr);
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
+    xchg_begin(xq);
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
       const int k = j - sc.lo;
-      double t = 0.0;
-      for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) t += (double)rcur[C.col(q)] * (double)C.val[q];
-      const float bsum = (float)((double)bb[k] + t);
+      float t = 0.f;
+      for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) t = __fmaf_rn(rcur[C.col(q)], C.val[q], t);
+      const float bsum = bb[k] + t;
       const float bl = bh[(size_t)l * M + j], blm = bh[(size_t)(l - 1) * M + j];
       const float r = bl / blm;
       bb[k] = bsum * A.eps * r * r;
-      push_rep(cl, qcur, j, -bsum * bl * bl, rep_smem);
+      xchg_put(xq, CL, j, -bsum * bl * bl);
     }
-    cl.sync();
+    xchg_end(cl, xq);
     // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
       const float alm = ah[(size_t)(l - 1) * N + i];
-      double t = 0.0;
+      float t = 0.f;
       for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) {
         const float qv = qcur[R.col(p)];
-        t += (double)qv * (double)R.val[p];
+        t = __fmaf_rn(qv, R.val[p], t);
         R.acc[p] += qv * alm;
       }
-      ab[k] = (float)((double)ab[k] + t);
+      ab[k] += t;
     }
-    // the next row step touches only this thread's rows and rcur (read by no CTA before the
-    // next cl.sync); only the staged b^{l-1} needs a CTA barrier
+    // the next row step touches only this thread's rows; only the staged b^{l-1} needs a
+    // CTA barrier
     if (bls && l > 1) {
 #pragma unroll
       for (int u = 0; u < kPf; ++u) {
@@ -677,104 +811,284 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
   cl.sync();
 }
 
-// Row softmax reverse (thread per row) -> LineBack; P0bar read from the CSR-order array.
-__device__ void row_soft_rev(const SparseArgs& A, int b, Slice s) {
+// ---- per-line loops of the backward, run by groups of G lanes: G = 1 (thread per line,
+// lines of length <= kRegLine, U entries loaded per step) and G = 32 (warp per longer line).
+// Loads of a step are issued together so a line costs ~2 round trips per G*U entries.
+
+template <int G>
+__device__ __forceinline__ bool line_mine(uint32_t L) { return G == 1 ? L <= kRegLine : L > kRegLine; }
+
+// Row softmax reverse -> LineBack (two passes: S = sum P Pbar/2, then zbar = P (Pbar/2 - S)).
+template <int G, int U>
+__device__ void row_soft_rev(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const int N = A.N;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
-  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+  const int mem = G == 1 ? 0 : (threadIdx.x & 31);
+  APML_FOR_LINES(G, s, ll, i) {
+    const uint32_t beg = rp[i], end = rp[i + 1];
+    if (!line_mine<G>(end - beg)) continue;
     const LineB lb = A.rowB[(size_t)b * N + i];
     LineBack out = {0.f, 0.f, 0.f, 0.f};
     if (!(lb.flags & kLineK1)) {
       double S = 0.0;
-      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
-        if (A.csr_jf[pb + p] & kFlagRow) S += (double)A.prow[pb + p] * 0.5 * (double)A.pbar[pb + p];
-      double szb = 0.0, Tbar = 0.0;
-      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
-        if (!(A.csr_jf[pb + p] & kFlagRow)) continue;
-        const double zb = (double)A.prow[pb + p] * (0.5 * (double)A.pbar[pb + p] - S);
-        szb += zb;
-        Tbar -= zb * ((double)A.cs[pb + p] - (double)lb.m);
+      for (uint32_t p0 = beg; p0 < end; p0 += G * U) {
+        uint32_t jf[U];
+        float pr[U], pbv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t p = p0 + u * G + mem;
+          jf[u] = p < end ? A.csr_jf[pb + p] : 0u;
+          pr[u] = p < end ? A.prow[pb + p] : 0.f;
+          pbv[u] = p < end ? A.pbar[pb + p] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (jf[u] & kFlagRow) S += (double)pr[u] * 0.5 * (double)pbv[u];
       }
+      S = gsum<G>(S);
+      double szb = 0.0, Tbar = 0.0;
+      for (uint32_t p0 = beg; p0 < end; p0 += G * U) {
+        uint32_t jf[U];
+        float pr[U], pbv[U], cv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t p = p0 + u * G + mem;
+          jf[u] = p < end ? A.csr_jf[pb + p] : 0u;
+          pr[u] = p < end ? A.prow[pb + p] : 0.f;
+          pbv[u] = p < end ? A.pbar[pb + p] : 0.f;
+          cv[u] = p < end ? A.cs[pb + p] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!(jf[u] & kFlagRow)) continue;
+          const double zb = (double)pr[u] * (0.5 * (double)pbv[u] - S);
+          szb += zb;
+          Tbar -= zb * ((double)cv[u] - (double)lb.m);
+        }
+      }
+      szb = gsum<G>(szb);
+      Tbar = gsum<G>(Tbar);
       const double mbar = (double)lb.T * szb;
       const double gbar = (lb.flags & kLineClamped) ? 0.0 : -Tbar * (double)lb.T / (double)lb.g;
       out = {(float)S, (float)(mbar - gbar), (float)gbar, lb.T};
     }
-    A.rowback[(size_t)b * N + i] = out;
+    if (mem == 0) A.rowback[(size_t)b * N + i] = out;
   }
 }
 
-__device__ void col_soft_rev(const SparseArgs& A, int b, Slice s) {
+template <int G, int U>
+__device__ void col_soft_rev(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const int M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
-  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+  const int mem = G == 1 ? 0 : (threadIdx.x & 31);
+  APML_FOR_LINES(G, s, ll, j) {
+    const uint32_t beg = cp[j], end = cp[j + 1];
+    if (!line_mine<G>(end - beg)) continue;
     const LineB lb = A.colB[(size_t)b * M + j];
     LineBack out = {0.f, 0.f, 0.f, 0.f};
     if (!(lb.flags & kLineK1)) {
       double S = 0.0;
-      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
-        const uint32_t p = A.csc_perm[pb + q];
-        if (A.csr_jf[pb + p] & kFlagCol) S += (double)A.pcol[pb + p] * 0.5 * (double)A.pbar[pb + p];
+      for (uint32_t q0 = beg; q0 < end; q0 += G * U) {
+        uint32_t pp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = q0 + u * G + mem;
+          pp[u] = q < end ? A.csc_perm[pb + q] : 0xffffffffu;
+        }
+        uint32_t jf[U];
+        float pc[U], pbv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool v = pp[u] != 0xffffffffu;
+          jf[u] = v ? A.csr_jf[pb + pp[u]] : 0u;
+          pc[u] = v ? A.pcol[pb + pp[u]] : 0.f;
+          pbv[u] = v ? A.pbar[pb + pp[u]] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (jf[u] & kFlagCol) S += (double)pc[u] * 0.5 * (double)pbv[u];
       }
+      S = gsum<G>(S);
       double szb = 0.0, Tbar = 0.0;
-      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
-        const uint32_t p = A.csc_perm[pb + q];
-        if (!(A.csr_jf[pb + p] & kFlagCol)) continue;
-        const double zb = (double)A.pcol[pb + p] * (0.5 * (double)A.pbar[pb + p] - S);
-        szb += zb;
-        Tbar -= zb * ((double)A.cs[pb + p] - (double)lb.m);
+      for (uint32_t q0 = beg; q0 < end; q0 += G * U) {
+        uint32_t pp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t q = q0 + u * G + mem;
+          pp[u] = q < end ? A.csc_perm[pb + q] : 0xffffffffu;
+        }
+        uint32_t jf[U];
+        float pc[U], pbv[U], cv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool v = pp[u] != 0xffffffffu;
+          jf[u] = v ? A.csr_jf[pb + pp[u]] : 0u;
+          pc[u] = v ? A.pcol[pb + pp[u]] : 0.f;
+          pbv[u] = v ? A.pbar[pb + pp[u]] : 0.f;
+          cv[u] = v ? A.cs[pb + pp[u]] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!(jf[u] & kFlagCol)) continue;
+          const double zb = (double)pc[u] * (0.5 * (double)pbv[u] - S);
+          szb += zb;
+          Tbar -= zb * ((double)cv[u] - (double)lb.m);
+        }
       }
+      szb = gsum<G>(szb);
+      Tbar = gsum<G>(Tbar);
       const double mbar = (double)lb.T * szb;
       const double gbar = (lb.flags & kLineClamped) ? 0.0 : -Tbar * (double)lb.T / (double)lb.g;
       out = {(float)S, (float)(mbar - gbar), (float)gbar, lb.T};
     }
-    A.colback[(size_t)b * M + j] = out;
+    if (mem == 0) A.colback[(size_t)b * M + j] = out;
   }
 }
 
-// cbar per entry and the Eq. (5) scatter into grad_pred (thread per row, overwrites).
-__device__ void grad_rows(const SparseArgs& A, int b, Slice s) {
+// cbar per entry and the Eq. (5) scatter into grad_pred (overwrites).
+template <int G, int U>
+__device__ void grad_rows(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const int N = A.N, M = A.M, L = A.L;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
   const float gl = A.grad_loss[b];
   const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
   const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
-  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+  const int mem = G == 1 ? 0 : (threadIdx.x & 31);
+  APML_FOR_LINES(G, s, ll, i) {
+    const uint32_t beg = rp[i], end = rp[i + 1];
+    if (!line_mine<G>(end - beg)) continue;
     const float4 x = A.pred4[(size_t)b * N + i];
     LineBack rbk = {0.f, 0.f, 0.f, 0.f};
     int2 ri = make_int2(-1, -1);
     if (A.full) { rbk = A.rowback[(size_t)b * N + i]; ri = A.rowidx[(size_t)b * N + i]; }
     const double ai = (double)aL[i];
     double gx = 0.0, gy = 0.0, gz = 0.0;
-    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
-      const uint32_t jf = A.csr_jf[pb + p];
-      const uint32_t j = jf & kIdxMask;
-      const double c = (double)A.cs[pb + p];
-      double cbar = (double)gl * ai * (double)A.P0[pb + p] * (double)bL[j];  // d loss / d c = v
-      if (A.full) {
-        const double hp = 0.5 * (double)A.pbar[pb + p];
-        if (jf & kFlagRow) cbar -= (double)rbk.T * (double)A.prow[pb + p] * (hp - (double)rbk.S);
-        if ((int)j == ri.x) cbar += rbk.ca;
-        if ((int)j == ri.y) cbar += rbk.cb;
-        const int2 ci = A.colidx[(size_t)b * M + j];
-        const bool cf = (jf & kFlagCol) != 0;
-        if (cf || ci.x == i || ci.y == i) {
-          const LineBack cbk = A.colback[(size_t)b * M + j];
-          if (cf) cbar -= (double)cbk.T * (double)A.pcol[pb + p] * (hp - (double)cbk.S);
-          if (ci.x == i) cbar += cbk.ca;
-          if (ci.y == i) cbar += cbk.cb;
+    for (uint32_t p0 = beg; p0 < end; p0 += G * U) {
+      uint32_t jf[U];
+      float cv[U], p0v[U], pbv[U], prv[U], pcv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t p = p0 + u * G + mem;
+        const bool v = p < end;
+        jf[u] = v ? A.csr_jf[pb + p] : 0u;
+        cv[u] = v ? A.cs[pb + p] : 1.f;
+        p0v[u] = v ? A.P0[pb + p] : 0.f;
+        if (A.full) {
+          pbv[u] = v ? A.pbar[pb + p] : 0.f;
+          prv[u] = v ? A.prow[pb + p] : 0.f;
+          pcv[u] = v ? A.pcol[pb + p] : 0.f;
         }
       }
-      const float4 y = A.gt4[(size_t)b * M + j];
-      const double w = cbar / (c + (double)A.eps_dist);  // Eq. (5)
-      gx += w * ((double)x.x - (double)y.x);
-      gy += w * ((double)x.y - (double)y.y);
-      gz += w * ((double)x.z - (double)y.z);
+      float4 y[U];
+      float bLv[U];
+      int2 ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool v = p0 + u * G + mem < end;
+        const uint32_t j = jf[u] & kIdxMask;
+        y[u] = v ? A.gt4[(size_t)b * M + j] : x;
+        bLv[u] = v ? bL[j] : 0.f;
+        ci[u] = (v && A.full) ? A.colidx[(size_t)b * M + j] : make_int2(-1, -1);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (p0 + u * G + mem >= end) continue;
+        const uint32_t j = jf[u] & kIdxMask;
+        double cbar = (double)gl * ai * (double)p0v[u] * (double)bLv[u];  // d loss / d c = v
+        if (A.full) {
+          const double hp = 0.5 * (double)pbv[u];
+          if (jf[u] & kFlagRow) cbar -= (double)rbk.T * (double)prv[u] * (hp - (double)rbk.S);
+          if ((int)j == ri.x) cbar += rbk.ca;
+          if ((int)j == ri.y) cbar += rbk.cb;
+          const bool cf = (jf[u] & kFlagCol) != 0;
+          if (cf || ci[u].x == i || ci[u].y == i) {
+            const LineBack cbk = A.colback[(size_t)b * M + j];
+            if (cf) cbar -= (double)cbk.T * (double)pcv[u] * (hp - (double)cbk.S);
+            if (ci[u].x == i) cbar += cbk.ca;
+            if (ci[u].y == i) cbar += cbk.cb;
+          }
+        }
+        const double w = cbar / ((double)cv[u] + (double)A.eps_dist);  // Eq. (5)
+        gx += w * ((double)x.x - (double)y[u].x);
+        gy += w * ((double)x.y - (double)y[u].y);
+        gz += w * ((double)x.z - (double)y[u].z);
+      }
     }
-    float* g = A.grad_pred + ((size_t)b * N + i) * 3;
-    g[0] = (float)gx; g[1] = (float)gy; g[2] = (float)gz;
+    gx = gsum<G>(gx);
+    gy = gsum<G>(gy);
+    gz = gsum<G>(gz);
+    if (mem == 0) {
+      float* g = A.grad_pred + ((size_t)b * N + i) * 3;
+      g[0] = (float)gx; g[1] = (float)gy; g[2] = (float)gz;
+    }
+  }
+}
+
+// abar_i = gl sum_j P0 b^L c (rows) and bbar_j = gl sum_i a^L P0 c (columns), own slices.
+template <int G, int U>
+__device__ void bwd_init_rows(const SparseArgs& A, int b, Slice s, const LongList& ll, float* ab) {
+  const int N = A.N, M = A.M, L = A.L;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
+  const double gl = (double)A.grad_loss[b];
+  const int mem = G == 1 ? 0 : (threadIdx.x & 31);
+  APML_FOR_LINES(G, s, ll, i) {
+    const uint32_t beg = rp[i], end = rp[i + 1];
+    if (!line_mine<G>(end - beg)) continue;
+    double t = 0.0;
+    for (uint32_t p0 = beg; p0 < end; p0 += G * U) {
+      uint32_t jf[U];
+      float pv[U], cv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t p = p0 + u * G + mem;
+        const bool v = p < end;
+        jf[u] = v ? A.csr_jf[pb + p] : 0u;
+        pv[u] = v ? A.P0[pb + p] : 0.f;
+        cv[u] = v ? A.cs[pb + p] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (p0 + u * G + mem < end) t += (double)pv[u] * (double)bL[jf[u] & kIdxMask] * (double)cv[u];
+    }
+    t = gsum<G>(t);
+    if (mem == 0) ab[i - s.lo] = (float)(gl * t);
+  }
+}
+
+template <int G, int U>
+__device__ void bwd_init_cols(const SparseArgs& A, int b, Slice s, const LongList& ll, float* bb) {
+  const int N = A.N, M = A.M, L = A.L;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
+  const double gl = (double)A.grad_loss[b];
+  const int mem = G == 1 ? 0 : (threadIdx.x & 31);
+  APML_FOR_LINES(G, s, ll, j) {
+    const uint32_t beg = cp[j], end = cp[j + 1];
+    if (!line_mine<G>(end - beg)) continue;
+    double t = 0.0;
+    for (uint32_t q0 = beg; q0 < end; q0 += G * U) {
+      uint32_t ii[U], pp[U];
+      float pv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t q = q0 + u * G + mem;
+        const bool v = q < end;
+        ii[u] = v ? A.csc_i[pb + q] : 0u;
+        pp[u] = v ? A.csc_perm[pb + q] : 0u;
+        pv[u] = v ? A.P0c[pb + q] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q0 + u * G + mem < end) t += (double)aL[ii[u]] * (double)pv[u] * (double)A.cs[pb + pp[u]];
+    }
+    t = gsum<G>(t);
+    if (mem == 0) bb[j - s.lo] = (float)(gl * t);
   }
 }
 
@@ -795,6 +1109,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     }
     return;
   }
+  __shared__ uint32_t s_long_r[kLongCap], s_long_c[kLongCap];
+  __shared__ int s_nlong[2];
+  const LongList llr = collect_long(A.row_ptr + (size_t)b * (N + 1), sr, s_long_r, &s_nlong[0]);
+  const LongList llc = collect_long(A.col_ptr + (size_t)b * (M + 1), sc, s_long_c, &s_nlong[1]);
   phase(A, 0);
   if (A.full) {
     const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
@@ -804,30 +1122,30 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
     uint8_t* sm = shm;
     float *rcur, *qcur;
+    __shared__ __align__(8) unsigned long long s_mbar[2];
     if (A.rep_smem) {
       rcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)N));
       qcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)M));
+      if (threadIdx.x == 0) {
+        mbar_init(smem_addr(&s_mbar[0]));
+        mbar_init(smem_addr(&s_mbar[1]));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
     } else {
       rcur = A.gvec + (size_t)b * 2 * (N + M);
       qcur = rcur + N;
     }
     float* ab = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sr.hi - sr.lo)));
     float* bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
+    Xchg xr{rcur, smem_addr(&s_mbar[0]), N, A.rep_smem != 0, 0u};
+    Xchg xq{qcur, smem_addr(&s_mbar[1]), M, A.rep_smem != 0, 0u};
     float* bls = nullptr;
     if (A.rep_smem && M <= kPf * (int)blockDim.x) bls = reinterpret_cast<float*>(carve(sm, 8 * (size_t)M));
     // abar = gl sum_j P0 b^L c, bbar = gl sum_i a^L P0 c   (loss = sum a P0 b c)
-    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
-      double t = 0.0;
-      for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
-        t += (double)A.P0[pb + p] * (double)bL[A.csr_jf[pb + p] & kIdxMask] * (double)A.cs[pb + p];
-      ab[i - sr.lo] = (float)((double)gl * t);
-    }
-    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
-      double t = 0.0;
-      for (uint32_t q = cp[j]; q < cp[j + 1]; ++q)
-        t += (double)aL[A.csc_i[pb + q]] * (double)A.P0c[pb + q] * (double)A.cs[pb + A.csc_perm[pb + q]];
-      bb[j - sc.lo] = (float)((double)gl * t);
-    }
+    bwd_init_rows<1, 8>(A, b, sr, llr, ab);
+    bwd_init_rows<32, 1>(A, b, sr, llr, ab);
+    bwd_init_cols<1, 8>(A, b, sc, llc, bb);
+    bwd_init_cols<32, 1>(A, b, sc, llc, bb);
     const size_t used = (size_t)(sm - shm);
     const bool fit = used + slice_bytes(sr.hi - sr.lo, rp[sr.hi] - rp[sr.lo], sizeof(IdxT), true) +
                          slice_bytes(sc.hi - sc.lo, cp[sc.hi] - cp[sc.lo], sizeof(IdxT), false) <= A.smem_bytes;
@@ -843,7 +1161,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
       }
       cl.sync();
       phase(A, 1);
-      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem, bls);
+      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls);
       const uint32_t base = rp[sr.lo], cnt = rp[sr.hi] - base;
       for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) A.pbar[pb + base + k] = R.acc[k];
     } else {
@@ -854,18 +1172,21 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
           A.pbar[pb + p] = gl * aL[i] * bL[A.csr_jf[pb + p] & kIdxMask] * A.cs[pb + p];
       cl.sync();
       phase(A, 1);
-      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, rcur, qcur, A.rep_smem, bls);
+      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls);
     }
     __syncthreads();
     phase(A, 2);
-    row_soft_rev(A, b, sr);
+    row_soft_rev<1, 8>(A, b, sr, llr);
+    row_soft_rev<32, 1>(A, b, sr, llr);
     cl.sync();
     phase(A, 3);
-    col_soft_rev(A, b, sc);
+    col_soft_rev<1, 8>(A, b, sc, llc);
+    col_soft_rev<32, 1>(A, b, sc, llc);
     cl.sync();
     phase(A, 4);
   }
-  grad_rows(A, b, sr);
+  grad_rows<1, 4>(A, b, sr, llr);
+  grad_rows<32, 1>(A, b, sr, llr);
   phase(A, 5);
 }
 
