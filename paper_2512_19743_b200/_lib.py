@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libapml.so")
+LIB_PATH = os.environ.get("APML_LIB") or os.path.join(HERE, "libapml.so")
 
 APML_OK, APML_ERR_INVALID_ARG, APML_ERR_SHAPE, APML_ERR_NONFINITE, APML_ERR_CAPACITY, \
     APML_ERR_CUDA, APML_ERR_OOM, APML_ERR_STATE = range(8)

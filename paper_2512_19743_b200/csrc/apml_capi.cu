@@ -35,7 +35,10 @@ apml_status fail(apml_status s, const std::string& msg) {
     if (e_ != cudaSuccess) return fail(APML_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-constexpr int kR = 4;                        // owned points per thread in the sweeps
+#ifndef APML_SWEEP_R
+#define APML_SWEEP_R 4
+#endif
+constexpr int kR = APML_SWEEP_R;             // owned points per thread in the sweeps
 constexpr int kOwnTile = kSweepThreads * kR; // owned points per CTA (512)
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
@@ -181,7 +184,7 @@ void plan_sparse(apml_ctx* c) {
   while (cl0 * 2 <= 8 && (int64_t)cl0 * 2 * B <= num_sms() && cl0 * 2 <= nmin) cl0 *= 2;
   auto need = [&](int cl, bool rep) {
     const int64_t nr = (N + cl - 1) / cl, nc = (M + cl - 1) / cl, e = (est + cl - 1) / cl;
-    size_t r = rep ? 4 * (size_t)(N + M) + 8 * (size_t)M + 48 : 0;  // replicas + staged b^l (x2)
+    size_t r = rep ? 4 * (size_t)(N + M) + 8 * (size_t)M + 96 : 0;  // replicas + staged b^l (x2)
     return r + 4 * (size_t)(nr + nc) + 32 + slice_bytes_h(nr, e, idx, true) + slice_bytes_h(nc, e, idx, false);
   };
   c->cl = cl0;

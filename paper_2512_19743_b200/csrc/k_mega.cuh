@@ -89,8 +89,13 @@ __device__ __forceinline__ void phase(const SparseArgs& A, int k) {
 struct Slice {
   int lo, hi;
 };
+// Slice boundaries are multiples of 4 lines so that every slice of a replica is 16-byte
+// aligned for the bulk DSMEM exchange.
+__device__ __forceinline__ int slice_lo(int n, int rank, int cl) {
+  return rank >= cl ? n : (int)(((long long)n * rank / cl) & ~3LL);
+}
 __device__ __forceinline__ Slice slice_of(int n, int rank, int cl) {
-  return Slice{(int)((long long)n * rank / cl), (int)((long long)n * (rank + 1) / cl)};
+  return Slice{slice_lo(n, rank, cl), rank + 1 >= cl ? n : slice_lo(n, rank + 1, cl)};
 }
 
 // ---------------------------------------------------------------- CSR / CSC construction
@@ -535,7 +540,8 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t addr, int rank) {
 }
 
 struct Xchg {
-  float* rep;      // replica (shared) or the single global copy
+  float* rep;      // replica (shared; 16-byte aligned, length padded to a multiple of 4 + 4)
+                   // or the single global copy
   uint32_t mbar;   // shared address of this CTA's mbarrier for the vector
   int n;           // vector length
   bool smem;
@@ -545,10 +551,13 @@ struct Xchg {
 __device__ __forceinline__ void mbar_init(uint32_t mbar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar) : "memory");
 }
-__device__ __forceinline__ void xchg_begin(const Xchg& x) {
+__device__ __forceinline__ void xchg_begin(const Xchg& x, int CL, int me) {
+  (void)CL; (void)me;
   if (x.smem && threadIdx.x == 0)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(x.mbar), "r"(4u * (uint32_t)x.n) : "memory");
 }
+// Write element k of the vector into the replica of every CTA of the cluster (st.async, DSMEM),
+// each store signalling the destination's mbarrier.
 __device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) {
   if (!x.smem) { x.rep[k] = v; return; }
   const uint32_t a = smem_addr(x.rep + k);
@@ -556,7 +565,9 @@ __device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) 
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
                  :: "r"(map_rank(a, r)), "r"(__float_as_uint(v)), "r"(map_rank(x.mbar, r)) : "memory");
 }
-__device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x) {
+// Wait until the whole vector (4 n bytes from all CTAs, own slice included) has arrived.
+__device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x, int CL, int me) {
+  (void)CL; (void)me;
   if (!x.smem) { cl.sync(); return; }
   uint32_t done = 0;
   while (!done)
@@ -570,13 +581,13 @@ __device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x) {
 template <typename IdxT>
 __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, Xchg& xa, Xchg& xb) {
-  const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks();
+  const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks(), me = cl.block_rank();
   float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   float* bh = A.b_hist + (size_t)b * (L + 1) * M;
   const float* a = xa.rep;
   const float* bv = xb.rep;
   for (int l = 1; l <= L; ++l) {
-    xchg_begin(xb);
+    xchg_begin(xb, CL, me);
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {  // Eq. (3): colsum = b_j Q_j
       const int k = j - sc.lo;
       float Q = 0.f;
@@ -586,8 +597,8 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       xchg_put(xb, CL, j, nb);
       bh[(size_t)l * M + j] = nb;
     }
-    xchg_end(cl, xb);
-    xchg_begin(xa);
+    xchg_end(cl, xb, CL, me);
+    xchg_begin(xa, CL, me);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {  // Eq. (4): rowsum = a_i R_i
       const int k = i - sr.lo;
       float Rs = 0.f;
@@ -597,7 +608,7 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       xchg_put(xa, CL, i, na);
       ah[(size_t)l * N + i] = na;
     }
-    xchg_end(cl, xa);
+    xchg_end(cl, xa, CL, me);
   }
 }
 
@@ -665,8 +676,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   float *a, *bv;
   __shared__ __align__(8) unsigned long long s_mbar[2];
   if (A.rep_smem) {
-    a = reinterpret_cast<float*>(carve(sm, 4 * (size_t)N));
-    bv = reinterpret_cast<float*>(carve(sm, 4 * (size_t)M));
+    a = reinterpret_cast<float*>(carve(sm, 4 * (size_t)((N + 3) / 4 * 4 + 4)));
+    bv = reinterpret_cast<float*>(carve(sm, 4 * (size_t)((M + 3) / 4 * 4 + 4)));
     for (int k = threadIdx.x; k < N; k += blockDim.x) a[k] = 1.f;
     for (int k = threadIdx.x; k < M; k += blockDim.x) bv[k] = 1.f;
     if (threadIdx.x == 0) {
@@ -737,10 +748,15 @@ constexpr int kPf = 8;  // b^l prefetch registers per thread (bls staging needs 
 template <typename IdxT>
 __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* ab, float* bb,
-                             Xchg& xr, Xchg& xq, float* bls) {
-  const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks();
-  const float* ah = A.a_hist + (size_t)b * (L + 1) * N;
-  const float* bh = A.b_hist + (size_t)b * (L + 1) * M;
+                             Xchg& xr, Xchg& xq, float* bls, const float* ahs, const float* bhs) {
+  const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks(), me = cl.block_rank();
+  // ahs: own rows' a history [L+1][nr] and bhs: full b history [L+1][M], staged in shared
+  // memory when they fit (else read from global memory, b^l optionally staged via bls).
+  const int nr = sr.hi - sr.lo;
+  const float* ah = ahs ? ahs - sr.lo : A.a_hist + (size_t)b * (L + 1) * N;
+  const size_t ald = ahs ? (size_t)nr : (size_t)N;
+  const float* bh = bhs ? bhs : A.b_hist + (size_t)b * (L + 1) * M;
+  if (bhs) bls = nullptr;
   const float* rcur = xr.rep;
   const float* qcur = xq.rep;
   // bls (2 x M floats, shared memory, optional): b^l staged for the P0bar gathers, double
@@ -758,22 +774,22 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
         pf[u] = k < M ? bh[(size_t)(l - 1) * M + k] : 0.f;
       }
     }
-    const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;
+    const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;  // b^l
     // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
     // P0bar_ij += Rbar^l_i b^l_j
-    xchg_begin(xr);
+    xchg_begin(xr, CL, me);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
-      const float al = ah[(size_t)l * N + i], alm = ah[(size_t)(l - 1) * N + i];
+      const float al = ah[(size_t)l * ald + i], alm = ah[(size_t)(l - 1) * ald + i];
       const float r = al / alm;
       const float Rb = -ab[k] * al * al;
       ab[k] = ab[k] * A.eps * r * r;
       xchg_put(xr, CL, i, Rb);
       for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += Rb * bcur[R.col(p)];
     }
-    xchg_end(cl, xr);
+    xchg_end(cl, xr, CL, me);
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
-    xchg_begin(xq);
+    xchg_begin(xq, CL, me);
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
       const int k = j - sc.lo;
       float t = 0.f;
@@ -784,11 +800,11 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       bb[k] = bsum * A.eps * r * r;
       xchg_put(xq, CL, j, -bsum * bl * bl);
     }
-    xchg_end(cl, xq);
+    xchg_end(cl, xq, CL, me);
     // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
-      const float alm = ah[(size_t)(l - 1) * N + i];
+      const float alm = ah[(size_t)(l - 1) * ald + i];
       float t = 0.f;
       for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) {
         const float qv = qcur[R.col(p)];
@@ -1124,8 +1140,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     float *rcur, *qcur;
     __shared__ __align__(8) unsigned long long s_mbar[2];
     if (A.rep_smem) {
-      rcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)N));
-      qcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)M));
+      rcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)((N + 3) / 4 * 4 + 4)));
+      qcur = reinterpret_cast<float*>(carve(sm, 4 * (size_t)((M + 3) / 4 * 4 + 4)));
       if (threadIdx.x == 0) {
         mbar_init(smem_addr(&s_mbar[0]));
         mbar_init(smem_addr(&s_mbar[1]));
@@ -1159,9 +1175,21 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
         for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p)
           R.acc[p] = gl * aL[i] * bL[R.col(p)] * A.cs[pb + rp[sr.lo] + p];
       }
+      // stage the Sinkhorn history (own rows of a, all of b) when it fits
+      float *ahs = nullptr, *bhs = nullptr;
+      const int nr = sr.hi - sr.lo;
+      if ((size_t)(sm - shm) + 4 * (size_t)(L + 1) * (nr + M) + 64 <= A.smem_bytes) {
+        ahs = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(L + 1) * nr));
+        bhs = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(L + 1) * M));
+        const float* ahg = A.a_hist + (size_t)b * (L + 1) * N;
+        const float* bhg = A.b_hist + (size_t)b * (L + 1) * M;
+        for (int k = threadIdx.x; k < (L + 1) * nr; k += blockDim.x)
+          ahs[k] = ahg[(size_t)(k / nr) * N + sr.lo + k % nr];
+        for (int k = threadIdx.x; k < (L + 1) * M; k += blockDim.x) bhs[k] = bhg[k];
+      }
       cl.sync();
       phase(A, 1);
-      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls);
+      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, ahs, bhs);
       const uint32_t base = rp[sr.lo], cnt = rp[sr.hi] - base;
       for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) A.pbar[pb + base + k] = R.acc[k];
     } else {
@@ -1172,7 +1200,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
           A.pbar[pb + p] = gl * aL[i] * bL[A.csr_jf[pb + p] & kIdxMask] * A.cs[pb + p];
       cl.sync();
       phase(A, 1);
-      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls);
+      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, nullptr, nullptr);
     }
     __syncthreads();
     phase(A, 2);
