@@ -160,6 +160,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2512_19743_b200 import Config, forward, loss_grad_host
+    from paper_2512_19743_b200.parallel import sharded_reduce
     from synth import clouds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -184,8 +185,7 @@ def main():
         loss, ctx = forward(pred, gt, cfg, loss_out=loss_buf)
         ctx.backward(ones, out=grad_buf)
         if world > 1:
-            tot = loss.sum()
-            dist.all_reduce(tot)  # X1: NCCL loss all-reduce (batch sharding)
+            sharded_reduce(loss)  # X1: NCCL all-reduce of the loss (batch sharding)
         return ctx
 
     for _ in range(args.warmup):

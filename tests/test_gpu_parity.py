@@ -237,3 +237,19 @@ def test_full_size_C3_mmfi_sampled():
 def test_full_size_C4_pcn_sampled():
     """configs[3] per-GPU shard at 1 GPU: B = 64, N = M = 16384; sampled pairs (loss + nnz)."""
     _full_size("shapenet", 64, 16384, 16384, [0, 63], seed=300, grad=False)
+
+
+def test_sharded_loss_single_rank_equals_plain_sum():
+    """parallel.apml_loss_sharded without a process group reduces to the plain batch sum."""
+    from paper_2512_19743_b200 import apml_loss
+    from paper_2512_19743_b200.parallel import apml_loss_sharded
+    _gpu()
+    x, y = clouds.batch("shapenet", 3, 300, 280, 16)
+    p1 = torch.tensor(x, device="cuda", requires_grad=True)
+    p2 = torch.tensor(x, device="cuda", requires_grad=True)
+    gt = torch.tensor(y, device="cuda")
+    a = apml_loss(p1, gt)
+    b = apml_loss_sharded(p2, gt)
+    a.backward(); b.backward()
+    assert a.item() == b.item()
+    assert torch.equal(p1.grad, p2.grad)
