@@ -551,8 +551,13 @@ struct Xchg {
 __device__ __forceinline__ void mbar_init(uint32_t mbar) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mbar) : "memory");
 }
-__device__ __forceinline__ void xchg_begin(const Xchg& x, int CL, int me) {
-  (void)CL; (void)me;
+// Arm this CTA's mbarrier for the next use of the vector (4 n bytes: every element of the
+// vector, own slice included, arrives through st.async).  Arming must precede any peer's
+// pushes for that use: xchg_arm runs at set-up (before a cluster barrier) and at the end of
+// every xchg_end (followed by a CTA barrier), so a peer -- which can only push the next
+// round after receiving this CTA's pushes of the other vector, issued after that barrier --
+// never sends bytes before the arm.
+__device__ __forceinline__ void xchg_arm(const Xchg& x) {
   if (x.smem && threadIdx.x == 0)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(x.mbar), "r"(4u * (uint32_t)x.n) : "memory");
 }
@@ -565,15 +570,35 @@ __device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) 
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
                  :: "r"(map_rank(a, r)), "r"(__float_as_uint(v)), "r"(map_rank(x.mbar, r)) : "memory");
 }
-// Wait until the whole vector (4 n bytes from all CTAs, own slice included) has arrived.
+// Wait until the whole vector has arrived, then re-arm for its next use.
 __device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x, int CL, int me) {
   (void)CL; (void)me;
   if (!x.smem) { cl.sync(); return; }
   uint32_t done = 0;
   while (!done)
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(done) : "r"(x.mbar), "r"(x.phase) : "memory");
   x.phase ^= 1u;
+  xchg_arm(x);
+  __syncthreads();
+}
+
+// Segment dot product sum_{p in [p0, p1)} vec[col(p)] * val[p] with four independent
+// accumulators (4x shorter dependent chain on long lines; fixed order -> deterministic).
+template <typename IdxT>
+__device__ __forceinline__ float seg_dot(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* vec) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  uint32_t p = p0;
+  for (; p + 4 <= p1; p += 4) {
+    s0 = __fmaf_rn(vec[V.col(p)], V.val[p], s0);
+    s1 = __fmaf_rn(vec[V.col(p + 1)], V.val[p + 1], s1);
+    s2 = __fmaf_rn(vec[V.col(p + 2)], V.val[p + 2], s2);
+    s3 = __fmaf_rn(vec[V.col(p + 3)], V.val[p + 3], s3);
+  }
+  if (p < p1) s0 = __fmaf_rn(vec[V.col(p)], V.val[p], s0);
+  if (p + 1 < p1) s1 = __fmaf_rn(vec[V.col(p + 1)], V.val[p + 1], s1);
+  if (p + 2 < p1) s2 = __fmaf_rn(vec[V.col(p + 2)], V.val[p + 2], s2);
+  return (s0 + s1) + (s2 + s3);
 }
 
 // ---------------------------------------------------------------- forward Sinkhorn + loss
@@ -587,22 +612,18 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
   const float* a = xa.rep;
   const float* bv = xb.rep;
   for (int l = 1; l <= L; ++l) {
-    xchg_begin(xb, CL, me);
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {  // Eq. (3): colsum = b_j Q_j
       const int k = j - sc.lo;
-      float Q = 0.f;
-      for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) Q = __fmaf_rn(a[C.col(q)], C.val[q], Q);
+      const float Q = seg_dot(C, C.off[k], C.off[k + 1], a);
       const float bj = bv[j];
       const float nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
       xchg_put(xb, CL, j, nb);
       bh[(size_t)l * M + j] = nb;
     }
     xchg_end(cl, xb, CL, me);
-    xchg_begin(xa, CL, me);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {  // Eq. (4): rowsum = a_i R_i
       const int k = i - sr.lo;
-      float Rs = 0.f;
-      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) Rs = __fmaf_rn(R.val[p], bv[R.col(p)], Rs);
+      const float Rs = seg_dot(R, R.off[k], R.off[k + 1], bv);
       const float ai = a[i];
       const float na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
       xchg_put(xa, CL, i, na);
@@ -697,6 +718,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   for (int k = sc.lo + threadIdx.x; k < sc.hi; k += blockDim.x) bh[k] = 1.f;
   Xchg xa{a, smem_addr(&s_mbar[0]), N, A.rep_smem != 0, 0u};
   Xchg xb{bv, smem_addr(&s_mbar[1]), M, A.rep_smem != 0, 0u};
+  xchg_arm(xa);  // first use of each mbarrier; peers start pushing after the next cl.sync
+  xchg_arm(xb);
   const size_t used = (size_t)(sm - shm);
   const bool fit = used + slice_bytes(sr.hi - sr.lo, rp[sr.hi] - rp[sr.lo], sizeof(IdxT), false) +
                        slice_bytes(sc.hi - sc.lo, cp[sc.hi] - cp[sc.lo], sizeof(IdxT), false) <= A.smem_bytes;
@@ -777,7 +800,6 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;  // b^l
     // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
     // P0bar_ij += Rbar^l_i b^l_j
-    xchg_begin(xr, CL, me);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
       const float al = ah[(size_t)l * ald + i], alm = ah[(size_t)(l - 1) * ald + i];
@@ -789,11 +811,9 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     }
     xchg_end(cl, xr, CL, me);
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
-    xchg_begin(xq, CL, me);
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
       const int k = j - sc.lo;
-      float t = 0.f;
-      for (uint32_t q = C.off[k]; q < C.off[k + 1]; ++q) t = __fmaf_rn(rcur[C.col(q)], C.val[q], t);
+      const float t = seg_dot(C, C.off[k], C.off[k + 1], rcur);
       const float bsum = bb[k] + t;
       const float bl = bh[(size_t)l * M + j], blm = bh[(size_t)(l - 1) * M + j];
       const float r = bl / blm;
@@ -805,12 +825,8 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
       const float alm = ah[(size_t)(l - 1) * ald + i];
-      float t = 0.f;
-      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) {
-        const float qv = qcur[R.col(p)];
-        t = __fmaf_rn(qv, R.val[p], t);
-        R.acc[p] += qv * alm;
-      }
+      const float t = seg_dot(R, R.off[k], R.off[k + 1], qcur);
+      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += qcur[R.col(p)] * alm;
       ab[k] += t;
     }
     // the next row step touches only this thread's rows; only the staged b^{l-1} needs a
@@ -1155,6 +1171,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     float* bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
     Xchg xr{rcur, smem_addr(&s_mbar[0]), N, A.rep_smem != 0, 0u};
     Xchg xq{qcur, smem_addr(&s_mbar[1]), M, A.rep_smem != 0, 0u};
+    xchg_arm(xr);
+    xchg_arm(xq);
     float* bls = nullptr;
     if (A.rep_smem && M <= kPf * (int)blockDim.x) bls = reinterpret_cast<float*>(carve(sm, 8 * (size_t)M));
     // abar = gl sum_j P0 b^L c, bbar = gl sum_i a^L P0 c   (loss = sum a P0 b c)
