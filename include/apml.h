@@ -126,6 +126,19 @@ typedef struct {
     int64_t launches;       /* kernels launched so far by this context (forward + backward) */
 } apml_stats;
 
+/* Caller-supplied, stream-ordered collectives for the row-sharded mode (torch.distributed /
+ * NCCL over NVLink in practice).  Both must be called by every rank in the same order with
+ * the same n; they return 0 on success.
+ *   allreduce_sum_f32: buf[0..n) <- sum over ranks of buf[0..n), in place, device memory.
+ *   allgather_f32:     recv[r*n .. (r+1)*n) <- rank r's send[0..n), device memory (the
+ *                      library also moves int32 bit patterns through it; no arithmetic). */
+typedef struct {
+    int32_t rank, world;
+    int (*allreduce_sum_f32)(float* buf, int64_t n, void* stream, void* user);
+    int (*allgather_f32)(const float* send, float* recv, int64_t n, void* stream, void* user);
+    void* user;
+} apml_comm;
+
 typedef struct apml_ctx apml_ctx; /* opaque: state saved by forward for backward */
 
 APML_API int apml_abi_version(void);
@@ -145,6 +158,22 @@ APML_API void apml_config_default(apml_config* cfg);
 APML_API apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
                          const apml_config* cfg, const apml_allocator* alloc, void* stream,
                          float* loss, apml_ctx** ctx_out);
+
+/* Forward with one cloud's pred rows SHARDED over the ranks of `comm` (north_star: "pred
+ * rows shard and per-iteration column sums are all-reduced").  This rank holds pred rows
+ * [row_offset, row_offset + N_local) of every pair (pred_local device [B][N_local][3]) and
+ * the whole gt (device [B][M][3]); N_global = sum of N_local over ranks (the column line
+ * length K of Eq. (1)).  Row statistics, the row softmax and the row scaling are local;
+ * column statistics are merged with one all-gather (X2), and the column softmax sum, the
+ * column argmin, every Sinkhorn column sum (Eq. (3), X3) and the loss are all-reduced.
+ * loss (device [B]) receives the GLOBAL per-pair loss on every rank.  The returned context
+ * drives the matching sharded backward through apml_backward (grad_pred = this rank's rows).
+ * Collective and synchronising like apml_forward; all ranks must pass the same B, M, cfg. */
+APML_API apml_status apml_forward_rowsharded(const float* pred_local, const float* gt, int64_t B,
+                                             int64_t N_local, int64_t row_offset, int64_t N_global,
+                                             int64_t M, const apml_config* cfg,
+                                             const apml_allocator* alloc, const apml_comm* comm,
+                                             void* stream, float* loss, apml_ctx** ctx_out);
 
 /* Backward: grad_pred [B][N][3] (device, overwritten) = sum_b grad_loss[b] *
  * d loss_b / d pred_b.  grad_loss device [B].  One backward per context (ERR_STATE after). */

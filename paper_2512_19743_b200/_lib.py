@@ -20,7 +20,8 @@ APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE, APML_FLAG_STAGE_TIMING = 1, 2, 4
 STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "sparse_fwd", "sparse_bwd")
 
 # exported symbols declared in include/apml.h (checked by tests/test_abi.py)
-EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_backward",
+EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forward_rowsharded",
+           "apml_backward",
            "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
            "apml_ctx_destroy",
            "apml_loss_grad_host", "apml_last_error")
@@ -39,6 +40,15 @@ FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
 class ApmlAllocator(C.Structure):
     _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", C.c_void_p)]
+
+
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class ApmlComm(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce_sum_f32", ALLREDUCE_FN),
+                ("allgather_f32", ALLGATHER_FN), ("user", C.c_void_p)]
 
 
 class ApmlStats(C.Structure):
@@ -72,6 +82,10 @@ def lib() -> C.CDLL:
         L.apml_forward.restype = C.c_int
         L.apml_forward.argtypes = [vp, vp, i64, i64, i64, C.POINTER(ApmlConfig),
                                    C.POINTER(ApmlAllocator), vp, vp, C.POINTER(vp)]
+        L.apml_forward_rowsharded.restype = C.c_int
+        L.apml_forward_rowsharded.argtypes = [vp, vp, i64, i64, i64, i64, i64, C.POINTER(ApmlConfig),
+                                              C.POINTER(ApmlAllocator), C.POINTER(ApmlComm), vp, vp,
+                                              C.POINTER(vp)]
         L.apml_backward.restype = C.c_int
         L.apml_backward.argtypes = [vp, vp, vp, vp]
         L.apml_ctx_stats.restype = C.c_int

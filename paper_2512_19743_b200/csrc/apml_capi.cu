@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "k_dist.cuh"
 #include "k_mega.cuh"
+#include "k_rowshard.cuh"
 
 using namespace apml;
 
@@ -77,6 +78,13 @@ struct apml_ctx {
   int rep_smem = 0;       // scaling-vector replicas in shared memory
   size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
+  // row-sharded mode
+  bool rs = false;
+  apml_comm comm{};
+  int64_t row_offset = 0, N_global = 0;
+  float2 *colpart = nullptr, *gath = nullptr;
+  float *colred = nullptr, *qbuf = nullptr, *flag = nullptr;
+  int *cand = nullptr, *gcand = nullptr;
   // sub-buffers
   float *predS, *gtS; float4 *pred4, *gt4;
   float2 *part_r, *part_c;
@@ -233,6 +241,11 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
   size_t o_gv = k.take<float>(B * 2 * (N + M));
   size_t o_rowback = k.take<LineBack>(B * N), o_colback = k.take<LineBack>(B * M);
+  const int64_t W = c->rs ? c->comm.world : 0;
+  size_t o_colpart = k.take<float2>(c->rs ? B * M : 0), o_gath = k.take<float2>(W * B * M);
+  size_t o_colred = k.take<float>(c->rs ? 3 * B * M : 0), o_qbuf = k.take<float>(c->rs ? B * M : 0);
+  size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(3 * W * B * M);
+  size_t o_flag = k.take<float>(16);
   c->bytes = k.off;
   c->base = (char*)ctx_alloc(c, c->bytes);
   if (!c->base) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->bytes) + " bytes failed");
@@ -254,6 +267,9 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->rowidx = (int2*)(p + o_rowidx); c->colidx = (int2*)(p + o_colidx);
   c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh); c->gvec = (float*)(p + o_gv);
   c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
+  c->colpart = (float2*)(p + o_colpart); c->gath = (float2*)(p + o_gath);
+  c->colred = (float*)(p + o_colred); c->qbuf = (float*)(p + o_qbuf);
+  c->cand = (int*)(p + o_cand); c->gcand = (int*)(p + o_gcand); c->flag = (float*)(p + o_flag);
   CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
   return APML_OK;
 }
@@ -272,6 +288,7 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.loss = loss; a.grad_loss = grad_loss; a.grad_pred = grad_pred;
   a.smem_bytes = c->smem_bytes; a.rep_smem = c->rep_smem;
   a.dbg = nullptr;
+  a.row_offset = (int)c->row_offset; a.colred = c->colred; a.cand = c->cand;
   return a;
 }
 
@@ -368,6 +385,123 @@ apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
   return st;
 }
 
+// ---------------------------------------------------------------- row-sharded mode
+
+apml_status coll_sum(apml_ctx* c, float* buf, int64_t n) {
+  if (c->comm.allreduce_sum_f32(buf, n, c->stream, c->comm.user) != 0)
+    return fail(APML_ERR_CUDA, "allreduce_sum_f32 collective failed");
+  return APML_OK;
+}
+apml_status coll_gather(apml_ctx* c, const float* send, float* recv, int64_t n) {
+  if (c->comm.allgather_f32(send, recv, n, c->stream, c->comm.user) != 0)
+    return fail(APML_ERR_CUDA, "allgather_f32 collective failed");
+  return APML_OK;
+}
+
+// S0-S3 with rows local and the column statistics merged over ranks (X2).
+apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
+  cudaStream_t s = c->stream;
+  mark(c, 0, s);
+  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
+  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
+  mark(c, 1, s);
+  k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
+      c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
+  mark(c, 2, s);
+  k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
+      c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
+  k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, c->colpart);
+  CK(cudaGetLastError());
+  apml_status st = coll_gather(c, (const float*)c->colpart, (float*)c->gath, 2LL * B * M);
+  if (st != APML_OK) return st;
+  mark(c, 3, s);
+  k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
+      c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+  k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->gath, c->comm.world, B, M, M, (int)c->N_global,
+      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+  mark(c, 4, s);
+  k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
+      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
+      c->aux, c->row_cnt, c->col_cnt);
+  mark(c, 5, s);
+  c->launches += 9;
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
+// S4-S7 over this rank's entries; column sums all-reduced.
+apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M, L = c->cfg.l_iter;
+  cudaStream_t s = c->stream;
+  const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
+  const dim3 gr((N + kRsThreads - 1) / kRsThreads, B), gc((M + kRsThreads - 1) / kRsThreads, B);
+  const dim3 gr256((N + 255) / 256, B), gc256((M + 255) / 256, B);
+  apml_status st;
+  k_rs_scan<<<B, 1024, 0, s>>>(a);
+  k_rs_scatter<<<dim3((c->cap + 255) / 256, B), 256, 0, s>>>(a);
+  k_rs_rows<<<gr, kRsThreads, 0, s>>>(a);
+  k_rs_cols_a<<<gc, kRsThreads, 0, s>>>(a);
+  CK(cudaGetLastError());
+  if ((st = coll_sum(c, c->colred, 3LL * B * M)) != APML_OK) return st;
+  if ((st = coll_gather(c, (const float*)c->cand, (float*)c->gcand, 3LL * B * M)) != APML_OK) return st;
+  k_rs_cols_b<<<gc, kRsThreads, 0, s>>>(a, c->gcand, c->comm.world);
+  k_rs_bstep<<<gc256, 256, 0, s>>>(a, 0, nullptr);
+  k_rs_astep<<<gr256, 256, 0, s>>>(a, 0);
+  c->launches += 7;
+  for (int l = 1; l <= L; ++l) {  // Eq. (3) column sums all-reduced (X3), Eq. (4) local
+    k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
+    CK(cudaGetLastError());
+    if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
+    k_rs_bstep<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
+    k_rs_astep<<<gr256, 256, 0, s>>>(a, l);
+    c->launches += 3;
+  }
+  k_rs_loss<<<B, 1024, 0, s>>>(a);
+  CK(cudaGetLastError());
+  if ((st = coll_sum(c, loss, B)) != APML_OK) return st;
+  mark(c, 6, s);
+  c->launches += 1;
+  return APML_OK;
+}
+
+apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_pred, cudaStream_t s) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M, L = c->cfg.l_iter;
+  const SparseArgs a = sparse_args(c, nullptr, grad_loss, grad_pred);
+  const dim3 gr((N + kRsThreads - 1) / kRsThreads, B), gc256((M + 255) / 256, B), gr256((N + 255) / 256, B);
+  apml_status st;
+  if (c->cfg.grad_mode == APML_GRAD_FULL) {
+    k_rs_bwd_init_rows<<<gr256, 256, 0, s>>>(a);
+    k_rs_bwd_init_cols<<<gc256, 256, 0, s>>>(a, c->qbuf);
+    CK(cudaGetLastError());
+    if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
+    k_rs_bwd_set_bbar<<<gc256, 256, 0, s>>>(a, c->qbuf);
+    c->launches += 3;
+    for (int l = L; l >= 1; --l) {
+      k_rs_bwd_rowrev<<<gr256, 256, 0, s>>>(a, l);
+      k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec + N + M, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
+      CK(cudaGetLastError());
+      if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
+      k_rs_bwd_colrev<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
+      k_rs_bwd_rowrev2<<<gr256, 256, 0, s>>>(a, l);
+      c->launches += 4;
+    }
+    k_rs_row_soft<<<gr, kRsThreads, 0, s>>>(a);
+    k_rs_col_soft_part<<<gc256, 256, 0, s>>>(a, 0, c->comm.rank);
+    CK(cudaGetLastError());
+    if ((st = coll_sum(c, c->colred, 3LL * B * M)) != APML_OK) return st;
+    k_rs_col_soft_part<<<gc256, 256, 0, s>>>(a, 1, c->comm.rank);
+    CK(cudaGetLastError());
+    if ((st = coll_sum(c, c->colred, 3LL * B * M)) != APML_OK) return st;
+    k_rs_col_soft_fin<<<gc256, 256, 0, s>>>(a);
+    c->launches += 4;
+  }
+  k_rs_grad<<<gr, kRsThreads, 0, s>>>(a);
+  c->launches += 1;
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
 apml_status check_finite(const float* p, int64_t n, cudaStream_t s) {
   std::vector<float> h((size_t)n);
   CK(cudaMemcpyAsync(h.data(), p, sizeof(float) * (size_t)n, cudaMemcpyDeviceToHost, s));
@@ -462,6 +596,77 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
   return fail(APML_ERR_CAPACITY, "unreachable");
 }
 
+apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t B, int64_t N,
+                                    int64_t row_offset, int64_t N_global, int64_t M,
+                                    const apml_config* cfg, const apml_allocator* alloc,
+                                    const apml_comm* comm, void* stream, float* loss,
+                                    apml_ctx** ctx_out) {
+  if (ctx_out) *ctx_out = nullptr;
+  apml_config c;
+  if (cfg) c = *cfg; else apml_config_default(&c);
+  if (!comm || !comm->allreduce_sum_f32 || !comm->allgather_f32 || comm->world < 1 ||
+      comm->rank < 0 || comm->rank >= comm->world)
+    return fail(APML_ERR_INVALID_ARG, "comm needs rank < world and both collectives");
+  if (row_offset < 0 || N_global < N + row_offset || N_global >= (1 << 30))
+    return fail(APML_ERR_SHAPE, "row_offset / N_global inconsistent with N_local");
+  apml_status st = validate(pred, gt, B, N_global, M, c);
+  if (st != APML_OK) return st;
+  if (N < 1) return fail(APML_ERR_SHAPE, "N_local must be >= 1");
+  if (!loss) return fail(APML_ERR_INVALID_ARG, "loss must be a non-NULL device pointer");
+  if (alloc && (!alloc->alloc || !alloc->free)) return fail(APML_ERR_INVALID_ARG, "allocator needs alloc and free");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t per = c.capacity > 0 ? c.capacity : 6;
+  int64_t cap64 = std::min<int64_t>(per * (N + M), N * M);
+  if (cap64 < 1) cap64 = 1;
+  if (cap64 >= ((int64_t)1 << 32)) return fail(APML_ERR_SHAPE, "emit capacity exceeds 32-bit positions");
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    apml_ctx* x = new apml_ctx();
+    x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = s;
+    x->rs = true; x->comm = *comm; x->row_offset = row_offset; x->N_global = N_global;
+    if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
+    if (c.flags & APML_FLAG_STAGE_TIMING) {
+      x->timing = true;
+      for (auto& e : x->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, "cudaEventCreate"); }
+    }
+    const double p = c.p_min;
+    x->lam_r = (float)lambda_K(M, p);
+    x->lam_c = (float)lambda_K(N_global, p);
+    const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;
+    x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
+    x->rho_c = N_global > 1 ? (float)(lt / lambda_K(N_global, p)) : INFINITY;
+    st = build_ctx(x, (uint32_t)cap64);
+    if (st == APML_OK) st = launch_forward_rs(x, pred, gt);
+    if (st != APML_OK) { apml_ctx_destroy(x); return st; }
+    if (c.flags & APML_FLAG_SYNC_CHECK) {  // collective: every rank retries together
+      std::vector<unsigned> cnt((size_t)B);
+      cudaError_t e = cudaMemcpyAsync(cnt.data(), x->cursor, sizeof(unsigned) * (size_t)B, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, cudaGetErrorString(e)); }
+      unsigned mx = 0;
+      for (unsigned v : cnt) mx = v > mx ? v : mx;
+      float over = mx > x->cap ? 1.f : 0.f;
+      e = cudaMemcpyAsync(x->flag, &over, sizeof(float), cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, cudaGetErrorString(e)); }
+      if ((st = coll_sum(x, x->flag, 1)) != APML_OK) { apml_ctx_destroy(x); return st; }
+      e = cudaMemcpyAsync(&over, x->flag, sizeof(float), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, cudaGetErrorString(e)); }
+      if (over > 0.f) {
+        apml_ctx_destroy(x);
+        if (attempt == 1) return fail(APML_ERR_CAPACITY, "support exceeded capacity after retry");
+        cap64 = std::min<int64_t>(std::max<int64_t>(cap64, round_up((int64_t)mx + (int64_t)mx / 16 + 16, 64)), N * M);
+        continue;
+      }
+    }
+    st = launch_sparse_fwd_rs(x, loss);
+    if (st != APML_OK) { apml_ctx_destroy(x); return st; }
+    if (ctx_out) *ctx_out = x; else apml_ctx_destroy(x);
+    return APML_OK;
+  }
+  return fail(APML_ERR_CAPACITY, "unreachable");
+}
+
 apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred, void* stream) {
   if (!x) return fail(APML_ERR_STATE, "NULL context");
   if (x->backward_done) return fail(APML_ERR_STATE, "backward already ran on this context");
@@ -476,6 +681,13 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
   }
   mark(x, 7, s);
   x->bwd_timed = x->timing;
+  if (x->rs) {
+    apml_status st = launch_backward_rs(x, grad_loss, grad_pred, s);
+    if (st != APML_OK) return st;
+    mark(x, 8, s);
+    x->backward_done = true;
+    return APML_OK;
+  }
   const SparseArgs a = sparse_args(x, nullptr, grad_loss, grad_pred);
   apml_status st = x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s, "bwd", 6)
                             : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s, "bwd", 6);

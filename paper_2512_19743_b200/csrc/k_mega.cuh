@@ -76,6 +76,11 @@ struct SparseArgs {
   size_t smem_bytes;
   int rep_smem;
   unsigned long long* dbg;  // optional phase timestamps [grid][16] (APML_PHASES=1), else NULL
+  // row-sharded mode (k_rowshard.cuh): global index of local row 0, column partial sums /
+  // argmin candidates exchanged through the caller's collectives
+  int row_offset;
+  float* colred;  // [B][M][3]
+  int* cand;      // [B][M][3]
 };
 
 __device__ __forceinline__ void phase(const SparseArgs& A, int k) {
@@ -1036,11 +1041,12 @@ __device__ void grad_rows(const SparseArgs& A, int b, Slice s, const LongList& l
           if ((int)j == ri.x) cbar += rbk.ca;
           if ((int)j == ri.y) cbar += rbk.cb;
           const bool cf = (jf[u] & kFlagCol) != 0;
-          if (cf || ci[u].x == i || ci[u].y == i) {
+          const int gi = i + A.row_offset;  // colidx holds global row indices
+          if (cf || ci[u].x == gi || ci[u].y == gi) {
             const LineBack cbk = A.colback[(size_t)b * M + j];
             if (cf) cbar -= (double)cbk.T * (double)pcv[u] * (hp - (double)cbk.S);
-            if (ci[u].x == i) cbar += cbk.ca;
-            if (ci[u].y == i) cbar += cbk.cb;
+            if (ci[u].x == gi) cbar += cbk.ca;
+            if (ci[u].y == gi) cbar += cbk.cb;
           }
         }
         const double w = cbar / ((double)cv[u] + (double)A.eps_dist);  // Eq. (5)

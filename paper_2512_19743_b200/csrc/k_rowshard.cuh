@@ -1,0 +1,462 @@
+// k_rowshard.cuh -- the sparse stage when one cloud's pred rows are sharded over GPUs
+// (north_star "pred rows shard and per-iteration column sums are
+// all-reduced").  Rank r owns pred rows [row_offset, row_offset + N) of every pair and all M
+// gt points.  Row quantities are local; every column quantity is a sum over the column's
+// entries, which are spread over the ranks, so each one is formed as a local partial and
+// all-reduced by the caller's collective (apml_comm, NCCL over NVLink in practice) between
+// the kernels below.  Per forward: column (min, second) all-gather (X2), column softmax sum,
+// column argmin candidates, L_iter column sums Q_j (X3), the loss.  Per backward: bbar init,
+// L_iter column sums P0^T Rbar^l, column softmax reverse sums.  Every kernel is grid-wide
+// (no cluster), reusing the per-line device functions of k_mega.cuh.
+#pragma once
+#include "k_mega.cuh"
+
+namespace apml {
+
+constexpr int kRsThreads = 512;
+
+// ---------------------------------------------------------------- column statistics (X2)
+
+// Collapse the S column-split partials of Pass A into one (min, second) per column.
+__global__ void k_top2_collapse(const float2* __restrict__ part, int S, int B, int Mp, int M,
+                                float2* __restrict__ out) {
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  float m = __int_as_float(0x7f800000), s = m;
+  for (int k = 0; k < S; ++k) {
+    const float2 p = part[((size_t)k * B + b) * Mp + j];
+    top2_merge(m, s, p.x, p.y);
+  }
+  out[(size_t)b * M + j] = make_float2(m, s);
+}
+
+// ---------------------------------------------------------------- CSR / CSC (local entries)
+
+// Single-CTA exclusive scan of cnt[0..n] -> ptr (zeroes cnt for the scatter cursors).
+__device__ void block_scan(unsigned* cnt, unsigned* ptr, int n, unsigned* s_warp) {
+  const int len = n + 1;
+  const int per = (len + blockDim.x - 1) / blockDim.x;
+  const int beg = threadIdx.x * per, end = min(len, beg + per);
+  unsigned sum = 0;
+  for (int k = beg; k < end; ++k) sum += cnt[k];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    unsigned t = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += v;
+    }
+    s_warp[lane] = t;
+  }
+  __syncthreads();
+  unsigned run = inc - sum + (w ? s_warp[w - 1] : 0u);
+  for (int k = beg; k < end; ++k) {
+    const unsigned v = cnt[k];
+    ptr[k] = run;
+    run += v;
+    cnt[k] = 0u;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(1024) k_rs_scan(const SparseArgs A) {
+  __shared__ unsigned s_warp[32];
+  const int b = blockIdx.x;
+  if (A.cursor[b] > A.cap) return;
+  block_scan(A.row_cnt + (size_t)b * (A.N + 1), A.row_ptr + (size_t)b * (A.N + 1), A.N, s_warp);
+  block_scan(A.col_cnt + (size_t)b * (A.M + 1), A.col_ptr + (size_t)b * (A.M + 1), A.M, s_warp);
+}
+
+__global__ void k_rs_scatter(const SparseArgs A) {
+  const int b = blockIdx.y;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned total = A.cursor[b];
+  if (total > A.cap || t >= total) return;
+  const size_t pb = (size_t)b * A.cap;
+  const uint2 e = A.ebuf[pb + t];
+  const uint32_t i = e.x, j = e.y & kIdxMask;
+  const size_t rb = (size_t)b * (A.N + 1), cb = (size_t)b * (A.M + 1);
+  A.csr_t[pb + A.row_ptr[rb + i] + atomicAdd(A.row_cnt + rb + i, 1u)] = t;
+  A.csc_t[pb + A.col_ptr[cb + j] + atomicAdd(A.col_cnt + cb + j, 1u)] = t;
+}
+
+__device__ __forceinline__ Slice block_slice(int n) {
+  return Slice{min(n, (int)(blockIdx.x * blockDim.x)), min(n, (int)((blockIdx.x + 1) * blockDim.x))};
+}
+
+// Rows: sort by j + row softmax (everything row-local).
+__global__ void __launch_bounds__(kRsThreads) k_rs_rows(const SparseArgs A) {
+  __shared__ uint32_t s_long[kLongCap];
+  __shared__ int s_n;
+  const int b = blockIdx.y;
+  if (A.cursor[b] > A.cap) return;
+  const Slice s = block_slice(A.N);
+  const LongList ll = collect_long(A.row_ptr + (size_t)b * (A.N + 1), s, s_long, &s_n);
+  row_sort_norm_regs(A, b, s);
+  __syncthreads();
+  sort_lines<true>(A, b, s, ll);
+  __syncthreads();
+  row_norm(A, b, s, ll);
+}
+
+// Columns, pass 1: sort by i; partial column-softmax sum over this rank's entries and this
+// rank's argmin / second-argmin candidates (global row indices, or -1):
+//   cand = {first entry with d2 == m2, second entry with d2 == m2, first entry with d2 == s2}.
+__global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
+  __shared__ uint32_t s_long[kLongCap];
+  __shared__ int s_n;
+  const int b = blockIdx.y, M = A.M;
+  if (A.cursor[b] > A.cap) return;
+  const Slice s = block_slice(M);
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const LongList ll = collect_long(cp, s, s_long, &s_n);
+  // short columns sorted in registers by col_sort_norm_regs would also normalise; here the
+  // warp rank sort handles every column (long lists only cover long ones), so sort all:
+  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+    const uint32_t beg = cp[j], end = cp[j + 1];
+    if (end - beg > kRegLine) continue;
+    // insertion sort by i of the (t) ids, in place in csc_t (short column, thread-private)
+    const size_t pb = (size_t)b * A.cap;
+    for (uint32_t q = beg + 1; q < end; ++q) {
+      const uint32_t t = A.csc_t[pb + q];
+      const uint32_t key = A.ebuf[pb + t].x;
+      uint32_t r = q;
+      while (r > beg && A.ebuf[pb + A.csc_t[pb + r - 1]].x > key) {
+        A.csc_t[pb + r] = A.csc_t[pb + r - 1];
+        --r;
+      }
+      A.csc_t[pb + r] = t;
+    }
+    for (uint32_t q = beg; q < end; ++q) {
+      const uint32_t t = A.csc_t[pb + q];
+      A.csc_i[pb + q] = A.ebuf[pb + t].x;
+      A.csc_perm[pb + q] = A.inv[pb + t];
+    }
+  }
+  __syncthreads();
+  sort_lines<false>(A, b, s, ll);
+  __syncthreads();
+  const size_t pb = (size_t)b * A.cap;
+  for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
+    const LineA la = A.colA[(size_t)b * M + j];
+    const LineB lb = A.colB[(size_t)b * M + j];
+    int x1 = -1, x2 = -1, y1 = -1;
+    float Z = 0.f;
+    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+      const uint32_t p = A.csc_perm[pb + q];
+      const float d2 = A.d2s[pb + p];
+      const int gi = A.row_offset + (int)A.csc_i[pb + q];
+      if (d2 == la.m2) { if (x1 < 0) x1 = gi; else if (x2 < 0) x2 = gi; }
+      if (d2 == la.s2 && y1 < 0) y1 = gi;
+      if (A.csr_jf[pb + p] & kFlagCol) Z += (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m));
+    }
+    float* red = A.colred + ((size_t)b * M + j) * 3;
+    red[0] = Z; red[1] = 0.f; red[2] = 0.f;
+    int* c = A.cand + ((size_t)b * M + j) * 3;
+    c[0] = x1; c[1] = x2; c[2] = y1;
+  }
+}
+
+// Columns, pass 2 (after the all-reduce of Z and the all-gather of the candidates):
+// P_col, P0 in CSR and CSC order, and the global argmin / second argmin of the column.
+__global__ void __launch_bounds__(kRsThreads) k_rs_cols_b(const SparseArgs A, const int* __restrict__ gcand,
+                                                          int world) {
+  const int b = blockIdx.y, M = A.M, B = gridDim.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (A.cursor[b] > A.cap || j >= M) return;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const LineA la = A.colA[(size_t)b * M + j];
+  const LineB lb = A.colB[(size_t)b * M + j];
+  // merge candidates over ranks: argmin = lowest index with d2 == m2; second = second-lowest
+  // such index when s2 == m2, else the lowest index with d2 == s2
+  int a1 = -1, a2 = -1, y = -1;
+  auto ins = [&](int v) {
+    if (v < 0) return;
+    if (a1 < 0 || v < a1) { a2 = a1; a1 = v; }
+    else if (a2 < 0 || v < a2) a2 = v;
+  };
+  for (int r = 0; r < world; ++r) {
+    const int* c = gcand + (((size_t)r * B + b) * M + j) * 3;
+    ins(c[0]);
+    ins(c[1]);
+    if (c[2] >= 0 && (y < 0 || c[2] < y)) y = c[2];
+  }
+  const int second = (la.s2 == la.m2) ? a2 : y;
+  A.colidx[(size_t)b * M + j] = make_int2(a1, second);
+  const float iz = 1.f / A.colred[((size_t)b * M + j) * 3];
+  for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+    const uint32_t p = A.csc_perm[pb + q];
+    float pc = 0.f;
+    if (A.csr_jf[pb + p] & kFlagCol) pc = ((lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m))) * iz;
+    A.pcol[pb + p] = pc;
+    const float p0 = 0.5f * (A.prow[pb + p] + pc);
+    A.P0[pb + p] = p0;
+    A.P0c[pb + q] = p0;
+  }
+}
+
+// ---------------------------------------------------------------- Sinkhorn (X3)
+
+// out[b][j] = sum over this rank's entries of column j of w[i] * P0_ij  (w: N-vector).
+__global__ void k_rs_colsum(const SparseArgs A, const float* __restrict__ w, size_t w_stride,
+                            float* __restrict__ out, size_t out_stride) {
+  const int b = blockIdx.y, M = A.M;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (A.cursor[b] > A.cap || j >= M) return;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const float* wb = w + (size_t)b * w_stride;
+  float t = 0.f;
+  for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) t = __fmaf_rn(wb[A.csc_i[pb + q]], A.P0c[pb + q], t);
+  out[(size_t)b * out_stride + j] = t;
+}
+
+// Column step of Eq. (3) on the all-reduced Q: b_j <- b_j / (b_j Q_j + eps) (every rank).
+__global__ void k_rs_bstep(const SparseArgs A, int l, const float* __restrict__ Q) {
+  const int b = blockIdx.y, M = A.M;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  float* bv = A.gvec + (size_t)b * 2 * (A.N + M) + A.N;
+  float nb = 1.f;
+  if (l > 0) {
+    const float bj = bv[j];
+    nb = __fdividef(bj, __fmaf_rn(bj, Q[(size_t)b * M + j], A.eps));
+  }
+  bv[j] = nb;
+  A.b_hist[((size_t)b * (A.L + 1) + l) * M + j] = nb;
+}
+
+// Row step of Eq. (4) (local rows): a_i <- a_i / (a_i R_i + eps), R_i = sum_j P0_ij b_j.
+__global__ void k_rs_astep(const SparseArgs A, int l) {
+  const int b = blockIdx.y, N = A.N;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N || A.cursor[b] > A.cap) return;
+  const size_t pb = (size_t)b * A.cap;
+  float* a = A.gvec + (size_t)b * 2 * (N + A.M);
+  const float* bv = a + N;
+  float na = 1.f;
+  if (l > 0) {
+    const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+    float Rs = 0.f;
+    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) Rs = __fmaf_rn(A.P0[pb + p], bv[A.csr_jf[pb + p] & kIdxMask], Rs);
+    const float ai = a[i];
+    na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+  }
+  a[i] = na;
+  A.a_hist[((size_t)b * (A.L + 1) + l) * N + i] = na;
+}
+
+// This rank's part of loss_b = sum_i a_i sum_j P0_ij b_j c_ij (deterministic block sum).
+__global__ void __launch_bounds__(1024) k_rs_loss(const SparseArgs A) {
+  __shared__ double red[32];
+  const int b = blockIdx.x, N = A.N;
+  if (A.cursor[b] > A.cap) {
+    if (threadIdx.x == 0) A.loss[b] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  const float* a = A.gvec + (size_t)b * 2 * (N + A.M);
+  const float* bv = a + N;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    float t = 0.f;
+    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
+      t = __fmaf_rn(__fmul_rn(A.P0[pb + p], bv[A.csr_jf[pb + p] & kIdxMask]), A.cs[pb + p], t);
+    acc += (double)a[i] * (double)t;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    A.loss[b] = (float)t;
+  }
+}
+
+// ---------------------------------------------------------------- backward
+
+// abar_i = gl sum_j P0 b^L c (local rows); P0bar_ij = gl a^L_i b^L_j c_ij (direct term).
+__global__ void k_rs_bwd_init_rows(const SparseArgs A) {
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N || A.cursor[b] > A.cap) return;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
+  const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
+  const float gl = A.grad_loss[b];
+  double t = 0.0;
+  for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
+    const uint32_t j = A.csr_jf[pb + p] & kIdxMask;
+    t += (double)A.P0[pb + p] * (double)bL[j] * (double)A.cs[pb + p];
+    A.pbar[pb + p] = gl * aL[i] * bL[j] * A.cs[pb + p];
+  }
+  A.gvec[(size_t)b * 2 * (N + M) + i] = (float)((double)gl * t);  // abar
+}
+
+// Partial bbar_j = sum over local entries of a^L_i P0_ij c_ij (times gl after the reduce).
+__global__ void k_rs_bwd_init_cols(const SparseArgs A, float* __restrict__ out) {
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M || A.cursor[b] > A.cap) return;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
+  float t = 0.f;
+  for (uint32_t q = cp[j]; q < cp[j + 1]; ++q)
+    t = __fmaf_rn(aL[A.csc_i[pb + q]] * A.P0c[pb + q], A.cs[pb + A.csc_perm[pb + q]], t);
+  out[(size_t)b * M + j] = t;
+}
+
+__global__ void k_rs_bwd_set_bbar(const SparseArgs A, const float* __restrict__ red) {
+  const int b = blockIdx.y, N = A.N, M = A.M;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  A.gvec[(size_t)b * 2 * (N + M) + N + j] = A.grad_loss[b] * red[(size_t)b * M + j];
+}
+
+// Row step reverse at iteration l (local rows): Rbar, abar, P0bar += Rbar^l_i b^l_j.
+__global__ void k_rs_bwd_rowrev(const SparseArgs A, int l) {
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N || A.cursor[b] > A.cap) return;
+  const size_t pb = (size_t)b * A.cap;
+  float* ab = A.gvec + (size_t)b * 2 * (N + M);
+  float* rcur = ab + N + M;
+  const float al = A.a_hist[((size_t)b * (L + 1) + l) * N + i];
+  const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
+  const float r = al / alm;
+  const float Rb = -ab[i] * al * al;
+  ab[i] = ab[i] * A.eps * r * r;
+  rcur[i] = Rb;
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  const float* bl = A.b_hist + ((size_t)b * (L + 1) + l) * M;
+  for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) A.pbar[pb + p] += Rb * bl[A.csr_jf[pb + p] & kIdxMask];
+}
+
+// Column step reverse (every rank, all columns) on the all-reduced t = P0^T Rbar^l.
+__global__ void k_rs_bwd_colrev(const SparseArgs A, int l, const float* __restrict__ t) {
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  float* bb = A.gvec + (size_t)b * 2 * (N + M) + N;
+  float* qcur = bb + M + N;
+  const float bsum = bb[j] + t[(size_t)b * M + j];
+  const float bl = A.b_hist[((size_t)b * (L + 1) + l) * M + j];
+  const float blm = A.b_hist[((size_t)b * (L + 1) + l - 1) * M + j];
+  const float r = bl / blm;
+  bb[j] = bsum * A.eps * r * r;
+  qcur[j] = -bsum * bl * bl;
+}
+
+// abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (local rows).
+__global__ void k_rs_bwd_rowrev2(const SparseArgs A, int l) {
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N || A.cursor[b] > A.cap) return;
+  const size_t pb = (size_t)b * A.cap;
+  float* ab = A.gvec + (size_t)b * 2 * (N + M);
+  const float* qcur = ab + N + M + N;
+  const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
+  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  float t = 0.f;
+  for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
+    const float qv = qcur[A.csr_jf[pb + p] & kIdxMask];
+    t = __fmaf_rn(qv, A.P0[pb + p], t);
+    A.pbar[pb + p] += qv * alm;
+  }
+  ab[i] += t;
+}
+
+// Row softmax reverse (local rows).
+__global__ void __launch_bounds__(kRsThreads) k_rs_row_soft(const SparseArgs A) {
+  __shared__ uint32_t s_long[kLongCap];
+  __shared__ int s_n;
+  const int b = blockIdx.y;
+  if (A.cursor[b] > A.cap) return;
+  const Slice s = block_slice(A.N);
+  const LongList ll = collect_long(A.row_ptr + (size_t)b * (A.N + 1), s, s_long, &s_n);
+  row_soft_rev<1, 8>(A, b, s, ll);
+  row_soft_rev<32, 1>(A, b, s, ll);
+}
+
+// Column softmax reverse, partial sums over local entries (two passes, each all-reduced):
+// pass 0: S_j = sum P_col Pbar/2;  pass 1: (sum zbar, -sum zbar (c - m)) with zbar = P (Pbar/2 - S).
+__global__ void k_rs_col_soft_part(const SparseArgs A, int pass, int rank) {
+  const int b = blockIdx.y, M = A.M;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M || A.cursor[b] > A.cap) return;
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const LineB lb = A.colB[(size_t)b * M + j];
+  float* red = A.colred + ((size_t)b * M + j) * 3;
+  if (pass == 0) {
+    float S = 0.f;
+    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+      const uint32_t p = A.csc_perm[pb + q];
+      if (A.csr_jf[pb + p] & kFlagCol) S = __fmaf_rn(A.pcol[pb + p], 0.5f * A.pbar[pb + p], S);
+    }
+    red[0] = S; red[1] = 0.f; red[2] = 0.f;
+  } else {
+    const float S = red[0];
+    float szb = 0.f, Tb = 0.f;
+    for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
+      const uint32_t p = A.csc_perm[pb + q];
+      if (!(A.csr_jf[pb + p] & kFlagCol)) continue;
+      const float zb = A.pcol[pb + p] * (0.5f * A.pbar[pb + p] - S);
+      szb += zb;
+      Tb -= zb * (A.cs[pb + p] - lb.m);
+    }
+    red[0] = rank == 0 ? S : 0.f;  // S is already global: keep it through the next all-reduce
+    red[1] = szb;
+    red[2] = Tb;
+  }
+}
+
+__global__ void k_rs_col_soft_fin(const SparseArgs A) {
+  const int b = blockIdx.y, M = A.M;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  const LineB lb = A.colB[(size_t)b * M + j];
+  const float* red = A.colred + ((size_t)b * M + j) * 3;
+  LineBack out = {0.f, 0.f, 0.f, 0.f};
+  if (!(lb.flags & kLineK1)) {
+    const double mbar = (double)lb.T * (double)red[1];
+    const double gbar = (lb.flags & kLineClamped) ? 0.0 : -(double)red[2] * (double)lb.T / (double)lb.g;
+    out = {red[0], (float)(mbar - gbar), (float)gbar, lb.T};
+  }
+  A.colback[(size_t)b * M + j] = out;
+}
+
+__global__ void __launch_bounds__(kRsThreads) k_rs_grad(const SparseArgs A) {
+  __shared__ uint32_t s_long[kLongCap];
+  __shared__ int s_n;
+  const int b = blockIdx.y;
+  const Slice s = block_slice(A.N);
+  if (A.cursor[b] > A.cap) {
+    const float nan = __int_as_float(0x7fc00000);
+    for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+      float* g = A.grad_pred + ((size_t)b * A.N + i) * 3;
+      g[0] = nan; g[1] = nan; g[2] = nan;
+    }
+    return;
+  }
+  const LongList ll = collect_long(A.row_ptr + (size_t)b * (A.N + 1), s, s_long, &s_n);
+  grad_rows<1, 4>(A, b, s, ll);
+  grad_rows<32, 1>(A, b, s, ll);
+}
+
+}  // namespace apml
