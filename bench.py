@@ -87,6 +87,18 @@ class ClockSampler:
                 "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2] not in ("", "[N/A]"))}
 
 
+# Largest pair the oracle is timed on directly; bigger pairs (C5) are timed at this size and
+# scaled by the O(N M) cost of its line passes (stated in the JSON "sample").
+ORACLE_MAX_NM = 16384 * 16384
+
+
+def _oracle_sample(c):
+    N, M = c["N"], c["M"]
+    if N * M <= ORACLE_MAX_NM:
+        return N, M, 1.0
+    return 16384, 16384, ORACLE_MAX_NM / (N * M)
+
+
 def cpu_baseline(cfg_name: str, seed: int, budget_s: float = 15.0) -> dict:
     """The fp64 oracle as it stands (OpenMP over pairs) on a bounded sample of the workload."""
     from oracle import OracleConfig, batch as oracle_batch
@@ -94,7 +106,8 @@ def cpu_baseline(cfg_name: str, seed: int, budget_s: float = 15.0) -> dict:
     c = CONFIGS[cfg_name]
     cores = os.cpu_count() or 1
     n = max(1, min(c["B"], cores))
-    x, y = clouds.batch(c["kind"], n, c["N"], c["M"], seed)
+    sN, sM, scale = _oracle_sample(c)
+    x, y = clouds.batch(c["kind"], n, sN, sM, seed)
     t0 = time.perf_counter()
     _, _, _, used = oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
     dt = time.perf_counter() - t0
@@ -104,8 +117,9 @@ def cpu_baseline(cfg_name: str, seed: int, budget_s: float = 15.0) -> dict:
         done += n
         reps += 1
     el = time.perf_counter() - t0
-    return {"value": done / el, "unit": "pairs/s", "cores": used, "kind": "oracle",
-            "sample": f"{reps} x {n} pairs of {cfg_name} ({c['kind']}, N={c['N']}, M={c['M']}), fwd+full bwd, fp64, {el:.1f} s"}
+    note = "" if scale == 1.0 else f" at N=M={sN}, scaled by the O(NM) cost x{scale:.3g}"
+    return {"value": done / el * scale, "unit": "pairs/s", "cores": used, "kind": "oracle",
+            "sample": f"{reps} x {n} pairs of {cfg_name} ({c['kind']}, N={c['N']}, M={c['M']}){note}, fwd+full bwd, fp64, {el:.1f} s"}
 
 
 def run_reference(args) -> None:
@@ -118,7 +132,8 @@ def run_reference(args) -> None:
     c = CONFIGS[args.config]
     cores = os.cpu_count() or 1
     n = max(1, min(c["B"], cores))
-    x, y = clouds.batch(c["kind"], n, c["N"], c["M"], args.seed)
+    sN, sM, scale = _oracle_sample(c)
+    x, y = clouds.batch(c["kind"], n, sN, sM, args.seed)
     for _ in range(args.warmup):
         oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
     t0 = time.perf_counter()
@@ -126,14 +141,16 @@ def run_reference(args) -> None:
     for _ in range(args.steps):
         _, _, _, used = oracle_batch(x, y, OracleConfig(), want_grad=True, nthreads=cores)
     el = time.perf_counter() - t0
-    val = n * args.steps / el
+    val = n * args.steps / el * scale
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "pairs/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": c["workload"], "B": c["B"], "N": c["N"], "M": c["M"],
                                            "kind": c["kind"], "step_sample_pairs": n},
            "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": used, "kind": "oracle",
-                            "sample": f"{n} pairs of {args.config} per step (bounded sample), fwd+full bwd, fp64"},
+                            "sample": f"{n} pairs of {args.config} per step (bounded sample)"
+                            + ("" if scale == 1.0 else f" at N=M={sN}, scaled by the O(NM) cost x{scale:.3g}")
+                            + ", fwd+full bwd, fp64"},
            "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -160,7 +177,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2512_19743_b200 import Config, forward, loss_grad_host
-    from paper_2512_19743_b200.parallel import sharded_reduce
+    from paper_2512_19743_b200.parallel import Collectives, forward_rowsharded, shard_rows, sharded_reduce
     from synth import clouds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -172,16 +189,29 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.config]
     B, N, M = c["B"], c["N"], c["M"]
-    x, y = clouds.batch(c["kind"], B, N, M, args.seed + 1000 * rank)
+    # C5 on several GPUs: one cloud, pred rows sharded (X2 all-gather + X3 column-sum
+    # all-reduces inside the call); every other config: batch sharding (weak scaling)
+    rowshard = args.config == "C5" and world > 1
+    if rowshard:
+        x, y = clouds.batch(c["kind"], B, N, M, args.seed)
+        r0, r1 = shard_rows(N, rank, world)
+        x = np.ascontiguousarray(x[:, r0:r1])
+        comm = Collectives(device=dev)
+    else:
+        x, y = clouds.batch(c["kind"], B, N, M, args.seed + 1000 * rank)
     pred = torch.tensor(x, device=dev)
     gt = torch.tensor(y, device=dev)
     ones = torch.ones(B, device=dev)
     loss_buf = torch.empty(B, device=dev)
-    grad_buf = torch.empty(B, N, 3, device=dev)
+    grad_buf = torch.empty(B, pred.shape[1], 3, device=dev)
     cfg = Config(grad_mode=args.grad_mode, sync_check=False, stage_timing=True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
+        if rowshard:
+            loss, ctx = forward_rowsharded(pred, gt, r0, N, cfg, comm, loss_out=loss_buf)
+            ctx.backward(ones, out=grad_buf)
+            return ctx
         loss, ctx = forward(pred, gt, cfg, loss_out=loss_buf)
         ctx.backward(ones, out=grad_buf)
         if world > 1:
@@ -221,7 +251,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     ms_per_step = tot_ms / args.steps
-    value = B * world / (ms_per_step / 1e3)
+    pairs_per_step = B if rowshard else B * world
+    value = pairs_per_step / (ms_per_step / 1e3)
 
     # per-stage medians and the roofline of the dominant kernel
     keys = list(stages[0].keys())
@@ -230,7 +261,7 @@ def main():
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     alu_peak = sms * 128 * f_max / 1e12  # FP32 lane-ops/s (FMA = 1), DESIGN.md "Roofline"
-    evals = B * N * M
+    evals = B * pred.shape[1] * M  # this rank's (i, j) evaluations per sweep
     dist_stages = ("passA_rows", "passA_cols", "emit")
     nnz = st0["nnz_total"]
     L = cfg.l_iter
@@ -264,7 +295,7 @@ def main():
 
     # end to end through the host entry point (pinned host buffers; copies inside the bracket)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not rowshard:
         ph = torch.tensor(x).pin_memory()
         gh = torch.tensor(y).pin_memory()
         lo = torch.empty(B, pin_memory=True)
@@ -285,7 +316,7 @@ def main():
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
-        e2e = {"value": B * world / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
+        e2e = {"value": pairs_per_step / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": 4 * B * 3 * (N + M), "d2h_bytes_per_step": 4 * B + 4 * B * N * 3,
                "api": "apml_loss_grad_host (host fp32 in, host loss + grad out)"}
 
@@ -298,12 +329,14 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if rowshard else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": c["workload"], "B": B, "N": N, "M": M, "kind": c["kind"], "tau": cfg.tau,
                        "l_iter": cfg.l_iter, "p_min": cfg.p_min, "grad_mode": args.grad_mode,
-                       "global_batch": B * world, "parallelism": f"batch-shard dp{world}" +
-                       (" + NCCL loss all-reduce" if world > 1 else ""),
+                       "global_batch": pairs_per_step,
+                       "parallelism": (f"row-shard x{world} (NCCL all-gather + per-iteration column-sum all-reduce)"
+                                       if rowshard else f"batch-shard dp{world}" +
+                                       (" + NCCL loss all-reduce" if world > 1 else "")),
                        "l2": "flushed between timed steps (256 MiB write outside the step bracket)"},
             "roofline": roof, "roofline_distance_pass": roof_dist,
             "stages_ms": med, "nnz_per_pair": nnz / B, "peak_gb": peak_gb,

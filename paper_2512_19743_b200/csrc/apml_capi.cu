@@ -179,17 +179,27 @@ size_t slice_bytes_h(int64_t nl, int64_t cnt, size_t idx, bool acc) {
   return a16(4 * (size_t)(nl + 1)) + a16(idx * (size_t)cnt) + a16(4 * (size_t)cnt) + (acc ? a16(4 * (size_t)cnt) : 0);
 }
 
+// Test / diagnostics overrides of the sparse-stage plan (exercise the fallback paths at sizes
+// the oracle can check): APML_FORCE_IDX32=1, APML_SMEM_LIMIT=<bytes>, APML_CL=<1|2|4|8>.
+long env_long(const char* name, long dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? strtol(e, nullptr, 10) : dflt;
+}
+
 // Sparse-stage plan: cluster size, replica placement, dynamic shared memory.
 void plan_sparse(apml_ctx* c) {
   const int64_t B = c->B, N = c->N, M = c->M;
-  c->idx16 = N <= 65536 && M <= 65536;
+  c->idx16 = N <= 65536 && M <= 65536 && !env_long("APML_FORCE_IDX32", 0);
   const size_t idx = c->idx16 ? 2 : 4;
-  const size_t mx = (size_t)max_smem_optin() - 12 * 1024;  // static shared memory (long-line lists)
+  const size_t mx = std::min<size_t>((size_t)max_smem_optin() - 12 * 1024,
+                                     (size_t)env_long("APML_SMEM_LIMIT", 1L << 30));
   // typical union support ~5 entries per point of the larger cloud
   const int64_t est = std::min<int64_t>((int64_t)c->cap, 5 * std::max(N, M) + 64);
   const int64_t nmin = std::min(N, M);
   int cl0 = 1;
   while (cl0 * 2 <= 8 && (int64_t)cl0 * 2 * B <= num_sms() && cl0 * 2 <= nmin) cl0 *= 2;
+  const long force_cl = env_long("APML_CL", 0);
+  if (force_cl > 0 && force_cl <= 8 && force_cl <= nmin) cl0 = (int)force_cl;
   auto need = [&](int cl, bool rep) {
     const int64_t nr = (N + cl - 1) / cl, nc = (M + cl - 1) / cl, e = (est + cl - 1) / cl;
     size_t r = rep ? 4 * (size_t)(N + M) + 8 * (size_t)M + 96 : 0;  // replicas + staged b^l (x2)

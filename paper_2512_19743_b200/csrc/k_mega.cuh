@@ -1173,8 +1173,17 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
       rcur = A.gvec + (size_t)b * 2 * (N + M);
       qcur = rcur + N;
     }
-    float* ab = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sr.hi - sr.lo)));
-    float* bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
+    // abar / bbar of the own slices: shared memory when they fit, else the second half of
+    // the pair's global scratch (the first half holds the replicas in global mode)
+    float *ab, *bb;
+    if ((size_t)(sm - shm) + 4 * (size_t)(sr.hi - sr.lo + sc.hi - sc.lo) + 64 <= A.smem_bytes) {
+      ab = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sr.hi - sr.lo)));
+      bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
+    } else {
+      float* g = A.gvec + (size_t)b * 2 * (N + M) + (N + M);
+      ab = g + sr.lo;
+      bb = g + N + sc.lo;
+    }
     Xchg xr{rcur, smem_addr(&s_mbar[0]), N, A.rep_smem != 0, 0u};
     Xchg xq{qcur, smem_addr(&s_mbar[1]), M, A.rep_smem != 0, 0u};
     xchg_arm(xr);

@@ -124,25 +124,33 @@ class Collectives:
             return 1
 
 
+def forward_rowsharded(pred_local: torch.Tensor, gt: torch.Tensor, row_offset: int, n_global: int,
+                       cfg=None, comm: "Collectives | None" = None, loss_out: torch.Tensor | None = None):
+    """apml_forward_rowsharded: GLOBAL per-pair losses [B] (every rank) and the Context whose
+    backward yields the gradient w.r.t. this rank's rows."""
+    from .apml import Context, _check_points, _ALLOC, Config
+    from . import _lib as A
+    cfg = cfg or Config()
+    comm = comm or Collectives(device=pred_local.device)
+    pred_local = _check_points(pred_local, "pred")
+    gt = _check_points(gt, "gt")
+    B, N, M = pred_local.shape[0], pred_local.shape[1], gt.shape[1]
+    loss = loss_out if loss_out is not None else torch.empty(B, device=pred_local.device, dtype=torch.float32)
+    h = C.c_void_p()
+    c = cfg.to_c()
+    s = torch.cuda.current_stream(pred_local.device).cuda_stream
+    A.check(A.lib().apml_forward_rowsharded(pred_local.data_ptr(), gt.data_ptr(), B, N, row_offset,
+                                            n_global, M, C.byref(c), C.byref(_ALLOC), C.byref(comm.c),
+                                            s, loss.data_ptr(), C.byref(h)))
+    ctx = Context(h.value, B, N, M, pred_local.device)
+    ctx.comm = comm  # keep the callbacks alive as long as the context
+    return loss, ctx
+
+
 class _RowShardedFunction(torch.autograd.Function):
     @staticmethod
     def forward(fctx, pred_local, gt, row_offset, n_global, cfg, comm):
-        from .apml import Context, _check_points, _ALLOC, Config
-        from . import _lib as A
-        cfg = cfg or Config()
-        pred_local = _check_points(pred_local, "pred")
-        gt = _check_points(gt, "gt")
-        B, N, M = pred_local.shape[0], pred_local.shape[1], gt.shape[1]
-        loss = torch.empty(B, device=pred_local.device, dtype=torch.float32)
-        h = C.c_void_p()
-        c = cfg.to_c()
-        s = torch.cuda.current_stream(pred_local.device).cuda_stream
-        st = A.lib().apml_forward_rowsharded(pred_local.data_ptr(), gt.data_ptr(), B, N, row_offset,
-                                             n_global, M, C.byref(c), C.byref(_ALLOC), C.byref(comm.c),
-                                             s, loss.data_ptr(), C.byref(h))
-        A.check(st)
-        fctx.apml = Context(h.value, B, N, M, pred_local.device)
-        fctx.comm = comm
+        loss, fctx.apml = forward_rowsharded(pred_local, gt, row_offset, n_global, cfg, comm)
         return loss
 
     @staticmethod
