@@ -253,3 +253,24 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     a.backward(); b.backward()
     assert a.item() == b.item()
     assert torch.equal(p1.grad, p2.grad)
+
+
+@pytest.mark.parametrize("env", [
+    {"APML_FORCE_IDX32": "1"},                                   # 32-bit indices in shared memory
+    {"APML_SMEM_LIMIT": "30000"},                                # replicas / slices in global memory
+    {"APML_SMEM_LIMIT": "30000", "APML_FORCE_IDX32": "1", "APML_CL": "8"},
+    {"APML_CL": "1"},                                            # one CTA per pair, no DSMEM peers
+    {"APML_CL": "2"},
+], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
+def test_sparse_stage_fallback_paths(env, monkeypatch):
+    """The plan the library picks depends on N, M, B and shared memory; force every variant at a
+    size the oracle checks (the large configs C4 / C5 run on these paths)."""
+    Config, _ = _gpu()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for kind, B, N, M in (("uniform", 2, 700, 650), ("mmfi", 2, 512, 1024)):
+        x, y = clouds.batch(kind, B, N, M, 17)
+        cfg = Config()
+        lg, gg, ctx = _run(x, y, cfg)
+        for b in range(B):
+            _check_pair(x, y, cfg, lg, gg, ctx, b)
