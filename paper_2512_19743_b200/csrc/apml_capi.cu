@@ -397,6 +397,22 @@ apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
 
 // ---------------------------------------------------------------- row-sharded mode
 
+// Single-GPU "collectives" (world 1): the grid-wide kernels of the row-sharded mode are also
+// the sparse stage of choice when there are too few pairs to fill the GPU with clusters.
+int local_allreduce(float*, int64_t, void*, void*) { return 0; }
+int local_allgather(const float* send, float* recv, int64_t n, void* stream, void*) {
+  return cudaMemcpyAsync(recv, send, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice,
+                         (cudaStream_t)stream) == cudaSuccess ? 0 : 1;
+}
+
+// Grid-wide sparse stage for few, large pairs: one cluster per pair would leave most SMs idle
+// (C5: B = 1 -> 8 of 148 SMs).  Override: APML_GRID=0/1.
+bool use_grid_path(int64_t B, int64_t N, int64_t M) {
+  const long f = env_long("APML_GRID", -1);
+  if (f >= 0) return f != 0;
+  return B * 8 < num_sms() && N + M >= 65536;
+}
+
 apml_status coll_sum(apml_ctx* c, float* buf, int64_t n) {
   if (c->comm.allreduce_sum_f32(buf, n, c->stream, c->comm.user) != 0)
     return fail(APML_ERR_CUDA, "allreduce_sum_f32 collective failed");
@@ -579,8 +595,14 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
     const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;  // ln(1/tau)
     x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
     x->rho_c = N > 1 ? (float)(lt / lambda_K(N, p)) : INFINITY;
+    if (use_grid_path(B, N, M)) {
+      x->rs = true;
+      x->comm = apml_comm{0, 1, local_allreduce, local_allgather, nullptr};
+      x->row_offset = 0;
+      x->N_global = N;
+    }
     st = build_ctx(x, (uint32_t)cap64);
-    if (st == APML_OK) st = launch_forward(x, pred, gt);
+    if (st == APML_OK) st = x->rs ? launch_forward_rs(x, pred, gt) : launch_forward(x, pred, gt);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
     if (c.flags & APML_FLAG_SYNC_CHECK) {
       std::vector<unsigned> cnt((size_t)B);
@@ -598,7 +620,7 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
         continue;
       }
     }
-    st = launch_sparse_fwd(x, loss);
+    st = x->rs ? launch_sparse_fwd_rs(x, loss) : launch_sparse_fwd(x, loss);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
     if (ctx_out) *ctx_out = x; else apml_ctx_destroy(x);
     return APML_OK;
