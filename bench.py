@@ -218,8 +218,15 @@ def main():
             sharded_reduce(loss)  # X1: NCCL all-reduce of the loss (batch sharding)
         return ctx
 
+    # warm-up with the timed loop's lifetime pattern (two contexts alive at a time), so the
+    # caching allocator already holds every block the timed steps need
+    prev = None
     for _ in range(args.warmup):
-        step().close()
+        ctx = step()
+        if prev is not None:
+            prev.close()
+        prev = ctx
+    prev.close()
     torch.cuda.synchronize()
     st0 = None
     if world > 1:

@@ -15,6 +15,7 @@
 
 #include "../../include/apml.h"
 #include "common.cuh"
+#include "k_cull.cuh"
 #include "k_dist.cuh"
 #include "k_mega.cuh"
 #include "k_rowshard.cuh"
@@ -78,6 +79,12 @@ struct apml_ctx {
   int rep_smem = 0;       // scaling-vector replicas in shared memory
   size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
+  // spatially culled sweeps (k_cull.cuh)
+  bool cull = false;
+  int cell_bits = 0;
+  float *pbb = nullptr, *ptb = nullptr, *gtb = nullptr, *ge2max = nullptr;
+  uint32_t *pkey = nullptr, *gkey = nullptr, *phist = nullptr, *ghist = nullptr, *pstart = nullptr, *gstart = nullptr;
+  int *pperm = nullptr, *gperm = nullptr;
   // row-sharded mode
   bool rs = false;
   apml_comm comm{};
@@ -224,6 +231,15 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->cap = cap;
   c->Np = round_up(N, kOwnTile);
   c->Mp = round_up(M, kOwnTile);
+  // exact spatial culling of the sweeps pays off once a 512-point block is a small part of
+  // the cloud (override: APML_CULL=0/1)
+  const long fc = env_long("APML_CULL", -1);
+  c->cull = fc >= 0 ? fc != 0 : std::min(N, M) >= 4096;
+  if (c->cull) {
+    int lg = 0;
+    while ((1LL << lg) < std::max(N, M)) ++lg;
+    c->cell_bits = std::min(7, std::max(2, (lg + 2) / 3));
+  }
   plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows);
   plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols);
   plan_sparse(c);
@@ -235,8 +251,10 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_part_c = k.take<float2>((int64_t)c->S_cols * B * c->Mp);
   size_t o_rowA = k.take<LineA>(B * N), o_colA = k.take<LineA>(B * M);
   size_t o_rowB = k.take<LineB>(B * N), o_colB = k.take<LineB>(B * M);
+  const int64_t cells1 = c->cull ? ((int64_t)1 << (3 * c->cell_bits)) + 1 : 0;
   // counters in one contiguous zeroed block
   size_t z0 = k.off;
+  size_t o_phist = k.take<uint32_t>(B * cells1), o_ghist = k.take<uint32_t>(B * cells1);
   size_t o_clamp = k.take<unsigned long long>(1);
   size_t o_cursor = k.take<unsigned>(B), o_aux = k.take<unsigned>(B);
   size_t o_row_cnt = k.take<unsigned>(B * (N + 1)), o_col_cnt = k.take<unsigned>(B * (M + 1));
@@ -256,6 +274,12 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_colred = k.take<float>(c->rs ? 3 * B * M : 0), o_qbuf = k.take<float>(c->rs ? B * M : 0);
   size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(3 * W * B * M);
   size_t o_flag = k.take<float>(16);
+  const bool cu = c->cull;
+  size_t o_pbb = k.take<float>(cu ? 6 * B : 0), o_ptb = k.take<float>(cu ? 6 * B * (c->Np / kTQ) : 0);
+  size_t o_gtb = k.take<float>(cu ? 6 * B * (c->Mp / kTQ) : 0), o_ge2 = k.take<float>(cu ? B * (c->Mp / kTQ) : 0);
+  size_t o_pkey = k.take<uint32_t>(cu ? B * N : 0), o_gkey = k.take<uint32_t>(cu ? B * M : 0);
+  size_t o_pstart = k.take<uint32_t>(B * cells1), o_gstart = k.take<uint32_t>(B * cells1);
+  size_t o_pperm = k.take<int>(cu ? B * c->Np : 0), o_gperm = k.take<int>(cu ? B * c->Mp : 0);
   c->bytes = k.off;
   c->base = (char*)ctx_alloc(c, c->bytes);
   if (!c->base) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->bytes) + " bytes failed");
@@ -280,6 +304,11 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->colpart = (float2*)(p + o_colpart); c->gath = (float2*)(p + o_gath);
   c->colred = (float*)(p + o_colred); c->qbuf = (float*)(p + o_qbuf);
   c->cand = (int*)(p + o_cand); c->gcand = (int*)(p + o_gcand); c->flag = (float*)(p + o_flag);
+  c->pbb = (float*)(p + o_pbb); c->ptb = (float*)(p + o_ptb); c->gtb = (float*)(p + o_gtb);
+  c->ge2max = (float*)(p + o_ge2); c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
+  c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
+  c->pstart = (uint32_t*)(p + o_pstart); c->gstart = (uint32_t*)(p + o_gstart);
+  c->pperm = (int*)(p + o_pperm); c->gperm = (int*)(p + o_gperm);
   CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
   return APML_OK;
 }
@@ -355,10 +384,65 @@ apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a0, cu
   return APML_OK;
 }
 
+// Culled sweeps: Morton-order both clouds, then Pass A over the sorted clouds
+// with tile culling.  Leaves part_r [B][N] and part_c [B][M] (original indices, S = 1).
+apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
+  cudaStream_t s = c->stream;
+  const int bits = c->cell_bits;
+  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, nullptr, c->pred4);
+  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, nullptr, c->gt4);
+  k_pair_bbox<<<B, 1024, 0, s>>>(pred, N, gt, M, c->pbb);
+  k_cell_count<<<dim3((N + 255) / 256, B), 256, 0, s>>>(pred, N, c->pbb, bits, c->pkey, c->phist);
+  k_cell_count<<<dim3((M + 255) / 256, B), 256, 0, s>>>(gt, M, c->pbb, bits, c->gkey, c->ghist);
+  k_cell_scan<<<dim3(B, 2), 1024, 0, s>>>(c->phist, c->pstart, c->ghist, c->gstart, (1 << (3 * bits)));
+  k_cell_scatter<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, bits, c->pkey, c->pstart,
+      c->phist, c->predS, c->pperm);
+  k_cell_scatter<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, bits, c->gkey, c->gstart,
+      c->ghist, c->gtS, c->gperm);
+  k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->ptb);
+  k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gtb);
+  mark(c, 1, s);
+  k_line_top2_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->ptb,
+      c->gtS, Mp, c->gtb, c->part_r);
+  mark(c, 2, s);
+  k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm, c->gtb,
+      c->predS, Np, c->ptb, c->part_c);
+  c->launches += 12;
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
+apml_status launch_emit_cull(apml_ctx* c) {
+  const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
+  cudaStream_t s = c->stream;
+  k_tile_e2max<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, c->ge2max);
+  k_emit_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
+      c->ptb, c->gtS, Mp, M, c->gperm, c->colA, c->gtb, c->ge2max, c->cap, c->ebuf, c->cursor, c->aux,
+      c->row_cnt, c->col_cnt);
+  c->launches += 2;
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
 apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   mark(c, 0, s);
+  if (c->cull) {
+    apml_status st = launch_passA_cull(c, pred, gt);
+    if (st != APML_OK) return st;
+    mark(c, 3, s);
+    k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, 1, B, N, N, M, c->lam_r, c->rho_r,
+        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+    k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, N, c->lam_c, c->rho_c,
+        c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+    mark(c, 4, s);
+    if ((st = launch_emit_cull(c)) != APML_OK) return st;
+    mark(c, 5, s);
+    c->launches += 2;
+    return APML_OK;
+  }
   // S0 staging
   k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
   k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
@@ -407,10 +491,14 @@ int local_allgather(const float* send, float* recv, int64_t n, void* stream, voi
 
 // Grid-wide sparse stage for few, large pairs: one cluster per pair would leave most SMs idle
 // (C5: B = 1 -> 8 of 148 SMs).  Override: APML_GRID=0/1.
-bool use_grid_path(int64_t B, int64_t N, int64_t M) {
+// Also when the per-pair cluster cannot keep its scaling-vector replicas in shared memory
+// (N + M too large): measured at C4 (B = 64, N = M = 16384) the grid-wide kernels win.
+bool use_grid_path(apml_ctx* c) {
   const long f = env_long("APML_GRID", -1);
   if (f >= 0) return f != 0;
-  return B * 8 < num_sms() && N + M >= 65536;
+  if (c->B * 8 < num_sms() && c->N + c->M >= 65536) return true;
+  plan_sparse(c);
+  return !c->rep_smem;
 }
 
 apml_status coll_sum(apml_ctx* c, float* buf, int64_t n) {
@@ -429,29 +517,43 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   mark(c, 0, s);
-  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
-  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
-  mark(c, 1, s);
-  k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
-  mark(c, 2, s);
-  k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
-      c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
-  k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, c->colpart);
+  apml_status st;
+  if (c->cull) {
+    if ((st = launch_passA_cull(c, pred, gt)) != APML_OK) return st;
+    k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, c->colpart);
+  } else {
+    k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
+    k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
+    mark(c, 1, s);
+    k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
+        c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
+    mark(c, 2, s);
+    k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
+        c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
+    k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, c->colpart);
+  }
   CK(cudaGetLastError());
-  apml_status st = coll_gather(c, (const float*)c->colpart, (float*)c->gath, 2LL * B * M);
+  st = coll_gather(c, (const float*)c->colpart, (float*)c->gath, 2LL * B * M);
   if (st != APML_OK) return st;
   mark(c, 3, s);
-  k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
-      c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+  if (c->cull)
+    k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, 1, B, N, N, M, c->lam_r, c->rho_r,
+        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+  else
+    k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
+        c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
   k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->gath, c->comm.world, B, M, M, (int)c->N_global,
       c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
   mark(c, 4, s);
-  k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
-      c->aux, c->row_cnt, c->col_cnt);
+  if (c->cull) {
+    if ((st = launch_emit_cull(c)) != APML_OK) return st;
+  } else {
+    k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
+        c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
+        c->aux, c->row_cnt, c->col_cnt);
+  }
   mark(c, 5, s);
-  c->launches += 9;
+  c->launches += 5;
   CK(cudaGetLastError());
   return APML_OK;
 }
@@ -595,7 +697,8 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
     const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;  // ln(1/tau)
     x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
     x->rho_c = N > 1 ? (float)(lt / lambda_K(N, p)) : INFINITY;
-    if (use_grid_path(B, N, M)) {
+    x->cap = (uint32_t)cap64;
+    if (use_grid_path(x)) {
       x->rs = true;
       x->comm = apml_comm{0, 1, local_allreduce, local_allgather, nullptr};
       x->row_offset = 0;

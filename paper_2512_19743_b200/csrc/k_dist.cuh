@@ -39,6 +39,7 @@ __global__ void k_stage(const float* __restrict__ pts, int n, int np, float sent
     x = p[0]; y = p[1]; z = p[2];
     p4[(size_t)b * n + k] = make_float4(x, y, z, 0.f);
   }
+  if (!soa) return;  // culled mode: the SoA copy is written in Morton order by k_cell_scatter
   float* s = soa + (size_t)b * 3 * np;
   s[k] = x; s[np + k] = y; s[2 * np + k] = z;
 }

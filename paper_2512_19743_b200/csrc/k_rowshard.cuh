@@ -459,4 +459,14 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_grad(const SparseArgs A) {
   grad_rows<32, 1>(A, b, s, ll);
 }
 
+// Per-pair exclusive scan of the Morton-cell histograms (k_cull.cuh); blockIdx.y = cloud.
+__global__ void __launch_bounds__(1024) k_cell_scan(uint32_t* phist, uint32_t* pstart, uint32_t* ghist,
+                                                    uint32_t* gstart, int cells) {
+  __shared__ unsigned s_warp[32];
+  const int b = blockIdx.x;
+  uint32_t* h = (blockIdx.y ? ghist : phist) + (size_t)b * (cells + 1);
+  uint32_t* st = (blockIdx.y ? gstart : pstart) + (size_t)b * (cells + 1);
+  block_scan(h, st, cells, s_warp);
+}
+
 }  // namespace apml

@@ -262,6 +262,8 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_CL": "1"},                                            # one CTA per pair, no DSMEM peers
     {"APML_CL": "2"},
     {"APML_GRID": "1"},                                          # grid-wide kernels (few, large pairs)
+    {"APML_CULL": "1"},                                          # spatially culled sweeps (NEXT-2)
+    {"APML_CULL": "1", "APML_GRID": "1"},
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_sparse_stage_fallback_paths(env, monkeypatch):
     """The plan the library picks depends on N, M, B and shared memory; force every variant at a

@@ -46,10 +46,16 @@ def _run_rank(rank, world, port, kind, B, N, M, mode, out):
     dist.destroy_process_group()
 
 
+@pytest.fixture(params=["0", "1"], ids=["brute", "culled"])
+def cull_env(request, monkeypatch):
+    monkeypatch.setenv("APML_CULL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("world", [1, 2])
 @pytest.mark.parametrize("mode", ["full", "plan_detached"])
 @pytest.mark.parametrize("case", [("shapenet", 2, 700, 650), ("uniform", 1, 333, 1000)])
-def test_rowsharded_matches_oracle(world, mode, case):
+def test_rowsharded_matches_oracle(world, mode, case, cull_env):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     kind, B, N, M = case
