@@ -82,7 +82,9 @@ struct apml_ctx {
   // spatially culled sweeps (k_cull.cuh)
   bool cull = false;
   int cell_bits = 0;
-  float *pbb = nullptr, *ptb = nullptr, *gtb = nullptr, *ge2max = nullptr;
+  float *pbb = nullptr, *pcb = nullptr, *pfb = nullptr, *gcb = nullptr, *gfb = nullptr;  // tile / sub-tile boxes
+  float *gce2 = nullptr, *gfe2 = nullptr;  // largest column emit radius per tile / sub-tile
+  float2* gre = nullptr;                   // column (R2, E2) in sorted order
   uint32_t *pkey = nullptr, *gkey = nullptr, *phist = nullptr, *ghist = nullptr, *pstart = nullptr, *gstart = nullptr;
   int *pperm = nullptr, *gperm = nullptr;
   // row-sharded mode
@@ -275,8 +277,10 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(3 * W * B * M);
   size_t o_flag = k.take<float>(16);
   const bool cu = c->cull;
-  size_t o_pbb = k.take<float>(cu ? 6 * B : 0), o_ptb = k.take<float>(cu ? 6 * B * (c->Np / kTQ) : 0);
-  size_t o_gtb = k.take<float>(cu ? 6 * B * (c->Mp / kTQ) : 0), o_ge2 = k.take<float>(cu ? B * (c->Mp / kTQ) : 0);
+  size_t o_pbb = k.take<float>(cu ? 6 * B : 0), o_pcb = k.take<float>(cu ? 6 * B * (c->Np / kTQ) : 0);
+  size_t o_gcb = k.take<float>(cu ? 6 * B * (c->Mp / kTQ) : 0), o_gce2 = k.take<float>(cu ? B * (c->Mp / kTQ) : 0);
+  size_t o_pfb = k.take<float>(cu ? 6 * B * (c->Np / kSub) : 0), o_gfb = k.take<float>(cu ? 6 * B * (c->Mp / kSub) : 0);
+  size_t o_gfe2 = k.take<float>(cu ? B * (c->Mp / kSub) : 0), o_gre = k.take<float2>(cu ? B * c->Mp : 0);
   size_t o_pkey = k.take<uint32_t>(cu ? B * N : 0), o_gkey = k.take<uint32_t>(cu ? B * M : 0);
   size_t o_pstart = k.take<uint32_t>(B * cells1), o_gstart = k.take<uint32_t>(B * cells1);
   size_t o_pperm = k.take<int>(cu ? B * c->Np : 0), o_gperm = k.take<int>(cu ? B * c->Mp : 0);
@@ -304,8 +308,10 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->colpart = (float2*)(p + o_colpart); c->gath = (float2*)(p + o_gath);
   c->colred = (float*)(p + o_colred); c->qbuf = (float*)(p + o_qbuf);
   c->cand = (int*)(p + o_cand); c->gcand = (int*)(p + o_gcand); c->flag = (float*)(p + o_flag);
-  c->pbb = (float*)(p + o_pbb); c->ptb = (float*)(p + o_ptb); c->gtb = (float*)(p + o_gtb);
-  c->ge2max = (float*)(p + o_ge2); c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
+  c->pbb = (float*)(p + o_pbb); c->pcb = (float*)(p + o_pcb); c->gcb = (float*)(p + o_gcb);
+  c->pfb = (float*)(p + o_pfb); c->gfb = (float*)(p + o_gfb);
+  c->gce2 = (float*)(p + o_gce2); c->gfe2 = (float*)(p + o_gfe2); c->gre = (float2*)(p + o_gre);
+  c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
   c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
   c->pstart = (uint32_t*)(p + o_pstart); c->gstart = (uint32_t*)(p + o_gstart);
   c->pperm = (int*)(p + o_pperm); c->gperm = (int*)(p + o_gperm);
@@ -400,14 +406,14 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
       c->phist, c->predS, c->pperm);
   k_cell_scatter<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, bits, c->gkey, c->gstart,
       c->ghist, c->gtS, c->gperm);
-  k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->ptb);
-  k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gtb);
+  k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->pcb, c->pfb);
+  k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
   mark(c, 1, s);
-  k_line_top2_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->ptb,
-      c->gtS, Mp, c->gtb, c->part_r);
+  k_line_top2_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
+      c->gtS, Mp, c->gcb, c->gfb, c->part_r);
   mark(c, 2, s);
-  k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm, c->gtb,
-      c->predS, Np, c->ptb, c->part_c);
+  k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
+      c->predS, Np, c->pcb, c->pfb, c->part_c);
   c->launches += 12;
   CK(cudaGetLastError());
   return APML_OK;
@@ -416,9 +422,9 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
 apml_status launch_emit_cull(apml_ctx* c) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
-  k_tile_e2max<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, c->ge2max);
+  k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, c->gre, c->gce2, c->gfe2);
   k_emit_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
-      c->ptb, c->gtS, Mp, M, c->gperm, c->colA, c->gtb, c->ge2max, c->cap, c->ebuf, c->cursor, c->aux,
+      c->gtS, Mp, M, c->gperm, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor, c->aux,
       c->row_cnt, c->col_cnt);
   c->launches += 2;
   CK(cudaGetLastError());

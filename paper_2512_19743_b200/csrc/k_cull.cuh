@@ -20,6 +20,8 @@
 namespace apml {
 
 constexpr float kCullMargin = 1.0f - 1e-5f;
+constexpr int kSub = 32;                   // culling granularity of the streamed side
+constexpr int kSubPerTile = kTQ / kSub;
 
 // Joint bounding box of pred and gt of each pair: bb[b] = {lo x,y,z, hi x,y,z}.
 __global__ void __launch_bounds__(1024)
@@ -102,8 +104,11 @@ __global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, flo
   perm[(size_t)b * np + pos] = k;
 }
 
-// Bounding box of every kTQ-point tile of a sorted cloud (pads excluded): tb[b][t] = 6 floats.
-__global__ void k_tile_bbox(const float* __restrict__ soa, int np, int n, float* __restrict__ tb) {
+// Bounding boxes of every kTQ-point tile (cb[b][t]) and of its kSub-point sub-tiles
+// (fb[b][t * kSubPerTile + q]) of a sorted cloud, pads excluded (an all-pad box is empty:
+// lo = +3e38, hi = -3e38, so its distance to anything is +inf).
+__global__ void __launch_bounds__(kTQ)
+k_tile_bbox(const float* __restrict__ soa, int np, int n, float* __restrict__ cb, float* __restrict__ fb) {
   const int b = blockIdx.y, t = blockIdx.x;
   const int k = t * kTQ + threadIdx.x;
   const float* s = soa + (size_t)b * 3 * np;
@@ -114,40 +119,56 @@ __global__ void k_tile_bbox(const float* __restrict__ soa, int np, int n, float*
     lo[d] = k < n ? v : 3e38f;
     hi[d] = k < n ? v : -3e38f;
   }
-  __shared__ float red[6][kTQ / 32];
 #pragma unroll
   for (int d = 0; d < 3; ++d)
     for (int o = 16; o > 0; o >>= 1) {
       lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
       hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
     }
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0)
-    for (int d = 0; d < 3; ++d) { red[d][w] = lo[d]; red[3 + d][w] = hi[d]; }
+  __shared__ float red[6][kTQ / 32];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  static_assert(kSub == 32, "a sub-tile is one warp's worth of points");
+  if (lane < 6) {
+    const float v = lane < 3 ? lo[lane] : hi[lane - 3];
+    fb[((size_t)b * (np / kSub) + t * kSubPerTile + w) * 6 + lane] = v;
+    red[lane][w] = v;
+  }
   __syncthreads();
   if (threadIdx.x < 6) {
     float v = threadIdx.x < 3 ? 3e38f : -3e38f;
     for (int q = 0; q < kTQ / 32; ++q)
       v = threadIdx.x < 3 ? fminf(v, red[threadIdx.x][q]) : fmaxf(v, red[threadIdx.x][q]);
-    tb[((size_t)b * (np / kTQ) + t) * 6 + threadIdx.x] = v;
+    cb[((size_t)b * (np / kTQ) + t) * 6 + threadIdx.x] = v;
   }
 }
 
-// Largest emit radius E2 of the columns of each gt tile (-1 for pads).
-__global__ void k_tile_e2max(const int* __restrict__ gperm, int mp, const LineA* __restrict__ colA, int M,
-                             float* __restrict__ e2max) {
+// Column radii in SORTED order (gre[b][k] = (R2, E2) of the gt point at sorted position k,
+// (-1, -1) for pads) and the largest E2 of every tile (ce2) and sub-tile (fe2).
+__global__ void __launch_bounds__(kTQ)
+k_tile_re(const int* __restrict__ gperm, int mp, const LineA* __restrict__ colA, int M,
+          float2* __restrict__ gre, float* __restrict__ ce2, float* __restrict__ fe2) {
   const int b = blockIdx.y, t = blockIdx.x;
   const int k = t * kTQ + threadIdx.x;
   const int j = gperm[(size_t)b * mp + k];
-  float e = j >= 0 ? colA[(size_t)b * M + j].E2 : -1.f;
+  float2 re = make_float2(-1.f, -1.f);
+  if (j >= 0) {
+    const LineA a = colA[(size_t)b * M + j];
+    re = make_float2(a.R2, a.E2);
+  }
+  gre[(size_t)b * mp + k] = re;
+  float e = re.y;
   for (int o = 16; o > 0; o >>= 1) e = fmaxf(e, __shfl_xor_sync(0xffffffffu, e, o));
   __shared__ float red[kTQ / 32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[w] = e;
+    fe2[(size_t)b * (mp / kSub) + t * kSubPerTile + w] = e;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     float v = -1.f;
     for (int q = 0; q < kTQ / 32; ++q) v = fmaxf(v, red[q]);
-    e2max[(size_t)b * (mp / kTQ) + t] = v;
+    ce2[(size_t)b * (mp / kTQ) + t] = v;
   }
 }
 
@@ -161,22 +182,12 @@ __device__ __forceinline__ float box_dist2(const float* a, const float* b) {
   return s;
 }
 
-// Own block bounding box = union of its 4 (= kSweepThreads * R / kTQ) tiles.
-template <int R>
-__device__ __forceinline__ void own_block_box(const float* tb, int blk, float* box) {
-  if (threadIdx.x < 6) {
-    float v = threadIdx.x < 3 ? 3e38f : -3e38f;
-    for (int q = 0; q < kSweepThreads * R / kTQ; ++q) {
-      const float u = tb[(size_t)(blk * (kSweepThreads * R / kTQ) + q) * 6 + threadIdx.x];
-      v = threadIdx.x < 3 ? fminf(v, u) : fmaxf(v, u);
-    }
-    box[threadIdx.x] = v;
-  }
-}
-
-// Warp-level culling: in the culled kernels a warp owns R*32 CONSECUTIVE sorted points
-// (idx = block base + warp*32R + r*32 + lane), i.e. a compact piece of the Morton curve, and
-// skips a tile on its own bounds; the CTA loads a tile only if some warp may need it.
+// Warp-autonomous culling.  A warp owns R groups of 32 CONSECUTIVE sorted points (group r =
+// positions base + 32 r + lane, a compact piece of the Morton curve) and walks the streamed
+// tiles on its own, without block barriers: a candidate tile is tested against the warp's
+// box (one tile per lane, 32 tiles per ballot), then each of its 4 sub-tiles against each
+// group's box (one (group, sub-tile) pair per lane); only the surviving (group, sub-tile)
+// pairs are evaluated, from the tile staged in the warp's own shared memory.
 template <int R>
 __device__ __forceinline__ int cull_idx(int blk, int r) {
   return blk * kSweepThreads * R + (threadIdx.x >> 5) * 32 * R + r * 32 + (threadIdx.x & 31);
@@ -193,6 +204,10 @@ __device__ __forceinline__ void warp_box(const float* lo_in, const float* hi_in,
     box[3 + d] = hi;
   }
 }
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 
 // Ring order around t0: t0, t0 + 1, t0 - 1, t0 + 2, ...; returns -1 for out-of-range steps.
 __device__ __forceinline__ int ring_tile(int t0, int step, int nt) {
@@ -201,208 +216,264 @@ __device__ __forceinline__ int ring_tile(int t0, int step, int nt) {
   return (t >= 0 && t < nt) ? t : -1;
 }
 
+// Box of one group (the lane's point if valid) and its union into the warp box.
+__device__ __forceinline__ void group_box(float x, float y, float z, bool valid, float* gb, float* wbox) {
+  const float lo[3] = {valid ? x : 3e38f, valid ? y : 3e38f, valid ? z : 3e38f};
+  const float hi[3] = {valid ? x : -3e38f, valid ? y : -3e38f, valid ? z : -3e38f};
+  warp_box(lo, hi, gb);
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    wbox[d] = fminf(wbox[d], gb[d]);
+    wbox[3 + d] = fmaxf(wbox[3 + d], gb[3 + d]);
+  }
+}
+
+// Stage streamed tile t (coordinates, SoA) into the warp's shared memory: one float4 per lane.
+__device__ __forceinline__ void stage_tile_xyz(const float* __restrict__ str, int str_np, int t, float* tx,
+                                               float* ty, float* tz) {
+  const int lane = threadIdx.x & 31;
+  const size_t o = (size_t)t * kTQ;
+  reinterpret_cast<float4*>(tx)[lane] = __ldg(reinterpret_cast<const float4*>(str + o) + lane);
+  reinterpret_cast<float4*>(ty)[lane] = __ldg(reinterpret_cast<const float4*>(str + str_np + o) + lane);
+  reinterpret_cast<float4*>(tz)[lane] = __ldg(reinterpret_cast<const float4*>(str + 2 * (size_t)str_np + o) + lane);
+}
+
 // Culled Pass A: (min, second) of d2 for every owned point, written at its ORIGINAL index.
+// Tiles are visited in a ring around the warp's own position in Morton order so the bounds
+// (largest current second minimum of each group) tighten after the first few tiles.
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const int* __restrict__ own_perm,
-                 const float* __restrict__ own_tb, const float* __restrict__ str_soa, int str_np,
-                 const float* __restrict__ str_tb, float2* __restrict__ out) {
-  const int b = blockIdx.y, blk = blockIdx.x;
+                 const float* __restrict__ str_soa, int str_np, const float* __restrict__ str_cb,
+                 const float* __restrict__ str_fb, float2* __restrict__ out) {
+  constexpr int kW = kSweepThreads / 32;
+  const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = own_soa + (size_t)b * 3 * own_np;
   const float* str = str_soa + (size_t)b * 3 * str_np;
   const int nt = str_np / kTQ;
-  const float* stb = str_tb + (size_t)b * nt * 6;
-  constexpr int kW = kSweepThreads / 32;
-  const int w = threadIdx.x >> 5;
-  __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ];
-  __shared__ float s_box[6], s_wbox[kW][6], s_wmax[kW];
-  own_block_box<R>(own_tb + (size_t)b * (own_np / kTQ) * 6, blk, s_box);
+  const float* cb = str_cb + (size_t)b * nt * 6;
+  const float* fb = str_fb + (size_t)b * nt * kSubPerTile * 6;
+  __shared__ __align__(16) float s_t[kW][3][kTQ];
+  __shared__ float s_gbox[kW][R][6], s_gmax[kW][R];
+  float* tx = s_t[w][0];
+  float* ty = s_t[w][1];
+  float* tz = s_t[w][2];
 
   f2_t nx[R], ny[R], nz[R];
-  float m[R], s[R];
+  float m[R], s[R], gmax[R];
   bool valid[R];
-  float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+  float wbox[6] = {3e38f, 3e38f, 3e38f, -3e38f, -3e38f, -3e38f};
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int idx = cull_idx<R>(blk, r);
+    const int idx = cull_idx<R>(blockIdx.x, r);
     valid[r] = idx < own_n;
     const float x = __ldg(own + idx), y = __ldg(own + own_np + idx), z = __ldg(own + 2 * own_np + idx);
-    if (valid[r]) {
-      lo[0] = fminf(lo[0], x); lo[1] = fminf(lo[1], y); lo[2] = fminf(lo[2], z);
-      hi[0] = fmaxf(hi[0], x); hi[1] = fmaxf(hi[1], y); hi[2] = fmaxf(hi[2], z);
-    }
     nx[r] = f2_pack(-x, -x); ny[r] = f2_pack(-y, -y); nz[r] = f2_pack(-z, -z);
     m[r] = __int_as_float(0x7f800000); s[r] = m[r];
+    float gb[6];
+    group_box(x, y, z, valid[r], gb, wbox);
+    gmax[r] = __any_sync(0xffffffffu, valid[r]) ? 3e38f : -1.f;  // empty groups need nothing
+#pragma unroll
+    for (int d = 0; d < 6; ++d)
+      if (lane == d) s_gbox[w][r][d] = gb[d];
+    if (lane == 0) s_gmax[w][r] = gmax[r];
   }
-  float wbox[6];
-  warp_box(lo, hi, wbox);
-  float wmax = __int_as_float(0x7f800000);  // this warp's largest current second minimum
-  if ((threadIdx.x & 31) == 0) {
-    for (int d = 0; d < 6; ++d) s_wbox[w][d] = wbox[d];
-    s_wmax[w] = wmax;
-  }
-  __syncthreads();
-  const int t0 = min(nt - 1, (int)(((long long)blk * kSweepThreads * R * str_np / own_np) / kTQ));
-  for (int step = 0; step < 2 * nt; ++step) {
-    const int t = ring_tile(t0, step, nt);
-    if (t < 0) continue;
-    const float* tbox = stb + (size_t)t * 6;
-    // CTA: load the tile if any warp may need it (uniform decision from shared state)
-    bool any = false;
-    if (box_dist2(s_box, tbox) * kCullMargin <= 3e38f)
-      for (int k = 0; k < kW; ++k) any |= box_dist2(s_wbox[k], tbox) * kCullMargin <= s_wmax[k];
-    if (!any) continue;
-    __syncthreads();
-    load_tile(str, str_np, t * kTQ, sx, sy, sz);
-    __syncthreads();
-    if (box_dist2(wbox, tbox) * kCullMargin <= wmax) {  // warp-uniform
-      const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
-      const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
-      const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
-#pragma unroll 4
-      for (int q = 0; q < kTQ / 4; ++q) {
-        const ulonglong2 qx = px[q], qy = py[q], qz = pz[q];
+  __syncwarp();
+  float wmax = -1.f;
+#pragma unroll
+  for (int r = 0; r < R; ++r) wmax = fmaxf(wmax, gmax[r]);
+
+  const int own_base = blockIdx.x * kSweepThreads * R + w * 32 * R;
+  const int t0 = min(nt - 1, (int)((long long)own_base * nt / own_np));
+  for (int base = 0; base < 2 * nt; base += 32) {
+    const int T = ring_tile(t0, base + lane, nt);
+    const bool cand = T >= 0 && box_dist2(wbox, cb + (size_t)T * 6) * kCullMargin <= wmax;
+    unsigned cm = __ballot_sync(0xffffffffu, cand);
+    while (cm) {
+      const int l = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const int t = __shfl_sync(0xffffffffu, T, l);
+      bool need = false;
+      if (lane < kSubPerTile * R) {
+        const int r = lane / kSubPerTile, q = lane % kSubPerTile;
+        need = box_dist2(s_gbox[w][r], fb + ((size_t)t * kSubPerTile + q) * 6) * kCullMargin <= s_gmax[w][r];
+      }
+      const unsigned fm = __ballot_sync(0xffffffffu, need);
+      if (!fm) continue;
+      stage_tile_xyz(str, str_np, t, tx, ty, tz);
+      __syncwarp();
+      for (int q = 0; q < kSubPerTile; ++q) {
+        const ulonglong2* px = reinterpret_cast<const ulonglong2*>(tx + q * kSub);
+        const ulonglong2* py = reinterpret_cast<const ulonglong2*>(ty + q * kSub);
+        const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(tz + q * kSub);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
-          const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
-          float d0, d1, d2, d3;
-          f2_unpack(d01, d0, d1);
-          f2_unpack(d23, d2, d3);
-          top2_pair(m[r], s[r], d0, d1);
-          top2_pair(m[r], s[r], d2, d3);
+          if (!((fm >> (r * kSubPerTile + q)) & 1u)) continue;  // warp-uniform
+#pragma unroll
+          for (int k = 0; k < kSub / 4; ++k) {
+            const ulonglong2 qx = px[k], qy = py[k], qz = pz[k];
+            const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
+            const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
+            float d0, d1, d2, d3;
+            f2_unpack(d01, d0, d1);
+            f2_unpack(d23, d2, d3);
+            top2_pair(m[r], s[r], d0, d1);
+            top2_pair(m[r], s[r], d2, d3);
+          }
         }
       }
-      float mx = -1.f;
+      wmax = -1.f;
 #pragma unroll
-      for (int r = 0; r < R; ++r) mx = valid[r] ? fmaxf(mx, s[r]) : mx;
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      wmax = mx;
+      for (int r = 0; r < R; ++r) {
+        if ((fm >> (r * kSubPerTile)) & ((1u << kSubPerTile) - 1u)) gmax[r] = warp_max(valid[r] ? s[r] : -1.f);
+        wmax = fmaxf(wmax, gmax[r]);
+      }
+      __syncwarp();  // every lane is done with the staged tile and the old bounds
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (lane == r) s_gmax[w][r] = gmax[r];
+      __syncwarp();
     }
-    __syncthreads();  // every warp has finished reading the tile and the old bounds
-    if ((threadIdx.x & 31) == 0) s_wmax[w] = wmax;
-    __syncthreads();
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int idx = cull_idx<R>(blk, r);
+    const int idx = cull_idx<R>(blockIdx.x, r);
     if (valid[r]) out[(size_t)b * own_n + own_perm[(size_t)b * own_np + idx]] = make_float2(m[r], s[r]);
   }
 }
 
-// Culled Pass B: as k_emit over the sorted clouds, skipping tiles beyond the emit radii;
+// Culled Pass B: as k_emit over the sorted clouds, evaluating only the (group, sub-tile)
+// pairs within max(group's largest row emit radius, sub-tile's largest column emit radius);
 // entries are emitted with ORIGINAL indices.
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __restrict__ pperm,
-            const LineA* __restrict__ rowA, const float* __restrict__ ptb,
-            const float* __restrict__ gt_soa, int mp, int M, const int* __restrict__ gperm,
-            const LineA* __restrict__ colA, const float* __restrict__ gtb, const float* __restrict__ ge2max,
+            const LineA* __restrict__ rowA, const float* __restrict__ gt_soa, int mp, int M,
+            const int* __restrict__ gperm, const float2* __restrict__ gre, const float* __restrict__ gcb,
+            const float* __restrict__ gfb, const float* __restrict__ gce2, const float* __restrict__ gfe2,
             uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
             unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt, unsigned* __restrict__ col_cnt) {
-  const int b = blockIdx.y, blk = blockIdx.x;
+  constexpr int kW = kSweepThreads / 32;
+  const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = pred_soa + (size_t)b * 3 * np;
   const float* str = gt_soa + (size_t)b * 3 * mp;
   const int nt = mp / kTQ;
-  const float* stb = gtb + (size_t)b * nt * 6;
-  const float* se2 = ge2max + (size_t)b * nt;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ], sR[kTQ], sE[kTQ];
-  __shared__ int sJ[kTQ];
-  __shared__ uint2 wbuf_all[kSweepThreads / 32][kWarpBuf];
-  __shared__ float s_box[6], s_wmax[kSweepThreads / 32], s_rmax;
+  const float* cb = gcb + (size_t)b * nt * 6;
+  const float* fb = gfb + (size_t)b * nt * kSubPerTile * 6;
+  const float* ce2 = gce2 + (size_t)b * nt;
+  const float* fe2 = gfe2 + (size_t)b * nt * kSubPerTile;
+  const float2* re = gre + (size_t)b * mp;
+  const int* jp = gperm + (size_t)b * mp;
+  __shared__ __align__(16) float s_t[kW][5][kTQ];
+  __shared__ __align__(16) int s_j[kW][kTQ];
+  __shared__ uint2 wbuf_all[kW][kWarpBuf];
+  __shared__ float s_gbox[kW][R][6], s_ge[kW][R];
+  float* tx = s_t[w][0];
+  float* ty = s_t[w][1];
+  float* tz = s_t[w][2];
+  float* sR = s_t[w][3];
+  float* sE = s_t[w][4];
+  int* sJ = s_j[w];
   uint2* wbuf = wbuf_all[w];
   int wcnt = 0;
-  own_block_box<R>(ptb + (size_t)b * (np / kTQ) * 6, blk, s_box);
 
   f2_t nx[R], ny[R], nz[R];
   float rR2[R], rE2[R];
   int oi[R];
-  float emax = -1.f;
-  float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+  float wE = -1.f;
+  float wbox[6] = {3e38f, 3e38f, 3e38f, -3e38f, -3e38f, -3e38f};
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int idx = cull_idx<R>(blk, r);
+    const int idx = cull_idx<R>(blockIdx.x, r);
     const float x = __ldg(own + idx), y = __ldg(own + np + idx), z = __ldg(own + 2 * np + idx);
     nx[r] = f2_pack(-x, -x); ny[r] = f2_pack(-y, -y); nz[r] = f2_pack(-z, -z);
     oi[r] = pperm[(size_t)b * np + idx];
+    rR2[r] = -1.f; rE2[r] = -1.f;
     if (oi[r] >= 0) {
       const LineA a = rowA[(size_t)b * N + oi[r]];
       rR2[r] = a.R2; rE2[r] = a.E2;
-      emax = fmaxf(emax, a.E2);
-      lo[0] = fminf(lo[0], x); lo[1] = fminf(lo[1], y); lo[2] = fminf(lo[2], z);
-      hi[0] = fmaxf(hi[0], x); hi[1] = fmaxf(hi[1], y); hi[2] = fmaxf(hi[2], z);
-    } else {
-      rR2[r] = -1.f; rE2[r] = -1.f;
     }
+    float gb[6];
+    group_box(x, y, z, oi[r] >= 0, gb, wbox);
+    const float ge = warp_max(rE2[r]);
+    wE = fmaxf(wE, ge);
+#pragma unroll
+    for (int d = 0; d < 6; ++d)
+      if (lane == d) s_gbox[w][r][d] = gb[d];
+    if (lane == 0) s_ge[w][r] = ge;
   }
-  float wbox[6];
-  warp_box(lo, hi, wbox);
-  for (int o = 16; o > 0; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-  if (lane == 0) s_wmax[w] = emax;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    float v = -1.f;
-    for (int k = 0; k < kSweepThreads / 32; ++k) v = fmaxf(v, s_wmax[k]);
-    s_rmax = v;
-  }
-  __syncthreads();
-  const float rmax = s_rmax;
+  __syncwarp();
   const unsigned lt_mask = (1u << lane) - 1u;
-  for (int t = 0; t < nt; ++t) {
-    if (box_dist2(s_box, stb + (size_t)t * 6) * kCullMargin > fmaxf(rmax, se2[t])) continue;  // uniform
-    const bool wneed = box_dist2(wbox, stb + (size_t)t * 6) * kCullMargin <= fmaxf(emax, se2[t]);
-    const int jt = t * kTQ;
-    __syncthreads();
-    load_tile(str, mp, jt, sx, sy, sz);
-    for (int q = threadIdx.x; q < kTQ; q += kSweepThreads) {
-      const int j = gperm[(size_t)b * mp + jt + q];
-      sJ[q] = j;
-      if (j >= 0) {
-        const LineA a = colA[(size_t)b * M + j];
-        sR[q] = a.R2; sE[q] = a.E2;
-      } else {
-        sR[q] = -1.f; sE[q] = -1.f;
-      }
+  for (int base = 0; base < nt; base += 32) {
+    const int T = base + lane;
+    bool cand = false;
+    if (T < nt) {
+      const float lb = box_dist2(wbox, cb + (size_t)T * 6) * kCullMargin;
+      cand = lb <= fmaxf(wE, ce2[T]) && lb < 3e38f;
     }
-    __syncthreads();
-    const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
-    const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
-    const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
-    const float4* pE = reinterpret_cast<const float4*>(sE);
+    unsigned cm = __ballot_sync(0xffffffffu, cand);
+    while (cm) {
+      const int l = __ffs(cm) - 1;
+      cm &= cm - 1;
+      const int t = __shfl_sync(0xffffffffu, T, l);
+      bool need = false;
+      if (lane < kSubPerTile * R) {
+        const int r = lane / kSubPerTile, sq = t * kSubPerTile + lane % kSubPerTile;
+        need = box_dist2(s_gbox[w][r], fb + (size_t)sq * 6) * kCullMargin <= fmaxf(s_ge[w][r], fe2[sq]);
+      }
+      const unsigned fm = __ballot_sync(0xffffffffu, need);
+      if (!fm) continue;
+      stage_tile_xyz(str, mp, t, tx, ty, tz);
+      {
+        const float4* src = reinterpret_cast<const float4*>(re + (size_t)t * kTQ);
+        const float4 a0 = __ldg(src + 2 * lane), a1 = __ldg(src + 2 * lane + 1);
+        reinterpret_cast<float4*>(sR)[lane] = make_float4(a0.x, a0.z, a1.x, a1.z);
+        reinterpret_cast<float4*>(sE)[lane] = make_float4(a0.y, a0.w, a1.y, a1.w);
+        reinterpret_cast<int4*>(sJ)[lane] = __ldg(reinterpret_cast<const int4*>(jp + (size_t)t * kTQ) + lane);
+      }
+      __syncwarp();
+      for (int q = 0; q < kSubPerTile; ++q) {
+        const ulonglong2* px = reinterpret_cast<const ulonglong2*>(tx + q * kSub);
+        const ulonglong2* py = reinterpret_cast<const ulonglong2*>(ty + q * kSub);
+        const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(tz + q * kSub);
+        const float4* pE = reinterpret_cast<const float4*>(sE + q * kSub);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!((fm >> (r * kSubPerTile + q)) & 1u)) continue;  // warp-uniform
 #pragma unroll 2
-    for (int q = 0; q < (wneed ? kTQ / 4 : 0); ++q) {  // warp-uniform trip count
-      const ulonglong2 qx = px[q], qy = py[q], qz = pz[q];
-      const float4 ce = pE[q];
+          for (int k = 0; k < kSub / 4; ++k) {
+            const ulonglong2 qx = px[k], qy = py[k], qz = pz[k];
+            const float4 ce = pE[k];
+            const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
+            const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
+            float d[4];
+            f2_unpack(d01, d[0], d[1]);
+            f2_unpack(d23, d[2], d[3]);
+            const bool hit = (d[0] <= fmaxf(rE2[r], ce.x)) | (d[1] <= fmaxf(rE2[r], ce.y)) |
+                             (d[2] <= fmaxf(rE2[r], ce.z)) | (d[3] <= fmaxf(rE2[r], ce.w));
+            if (__any_sync(0xffffffffu, hit)) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
-        const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
-        float d[4];
-        f2_unpack(d01, d[0], d[1]);
-        f2_unpack(d23, d[2], d[3]);
-        const bool hit = (d[0] <= fmaxf(rE2[r], ce.x)) | (d[1] <= fmaxf(rE2[r], ce.y)) |
-                         (d[2] <= fmaxf(rE2[r], ce.z)) | (d[3] <= fmaxf(rE2[r], ce.w));
-        if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int qq = 4 * q + c;
-            const int j = sJ[qq];
-            const bool h = d[c] <= fmaxf(rE2[r], sE[qq]) && oi[r] >= 0 && j >= 0;
-            const unsigned bal = __ballot_sync(0xffffffffu, h);
-            if (h) {
-              const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= sR[qq] ? kFlagCol : 0u);
-              wbuf[wcnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)oi[r], (uint32_t)j | fl);
+              for (int c = 0; c < 4; ++c) {
+                const int qq = q * kSub + 4 * k + c;
+                const int j = sJ[qq];
+                const bool h = d[c] <= fmaxf(rE2[r], sE[qq]) && oi[r] >= 0 && j >= 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, h);
+                if (h) {
+                  const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= sR[qq] ? kFlagCol : 0u);
+                  wbuf[wcnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)oi[r], (uint32_t)j | fl);
+                }
+                wcnt += __popc(bal);
+              }
+              if (wcnt > kFlushAt) {
+                __syncwarp();
+                warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+                wcnt = 0;
+              }
             }
-            wcnt += __popc(bal);
-          }
-          if (wcnt > kFlushAt) {
-            __syncwarp();
-            warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
-            wcnt = 0;
           }
         }
       }
+      __syncwarp();  // every lane is done with the staged tile
     }
   }
   __syncwarp();
