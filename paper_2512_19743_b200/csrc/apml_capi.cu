@@ -44,6 +44,8 @@ constexpr int kR = APML_SWEEP_R;             // owned points per thread in the s
 constexpr int kOwnTile = kSweepThreads * kR; // owned points per CTA (512)
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+constexpr int kBoxParts = 64;  // partial boxes per pair (k_pair_bbox_part)
+inline int64_t scan_tiles(int64_t len) { return (len + kScanTile - 1) / kScanTile; }
 
 // Workspace carve-out (256-byte aligned sub-buffers of one allocation).
 struct Carve {
@@ -85,6 +87,10 @@ struct apml_ctx {
   float *pbb = nullptr, *pcb = nullptr, *pfb = nullptr, *gcb = nullptr, *gfb = nullptr;  // tile / sub-tile boxes
   float *gce2 = nullptr, *gfe2 = nullptr;  // largest column emit radius per tile / sub-tile
   float2* gre = nullptr;                   // column (R2, E2) in sorted order
+  float* bbpart = nullptr;                 // partial pair boxes [B][kBoxParts][6]
+  // batched scans (CSR/CSC pointers, Morton cells) and the grid-wide loss
+  unsigned* tsum = nullptr;
+  double* lossp = nullptr;
   uint32_t *pkey = nullptr, *gkey = nullptr, *phist = nullptr, *ghist = nullptr, *pstart = nullptr, *gstart = nullptr;
   int *pperm = nullptr, *gperm = nullptr;
   // row-sharded mode
@@ -281,6 +287,10 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_gcb = k.take<float>(cu ? 6 * B * (c->Mp / kTQ) : 0), o_gce2 = k.take<float>(cu ? B * (c->Mp / kTQ) : 0);
   size_t o_pfb = k.take<float>(cu ? 6 * B * (c->Np / kSub) : 0), o_gfb = k.take<float>(cu ? 6 * B * (c->Mp / kSub) : 0);
   size_t o_gfe2 = k.take<float>(cu ? B * (c->Mp / kSub) : 0), o_gre = k.take<float2>(cu ? B * c->Mp : 0);
+  size_t o_bbpart = k.take<float>(cu ? 6 * B * kBoxParts : 0);
+  const int64_t tiles_rc = scan_tiles(N + 1) + scan_tiles(M + 1), tiles_cells = 2 * scan_tiles(cells1);
+  size_t o_tsum = k.take<unsigned>(B * std::max(tiles_rc, tiles_cells));
+  size_t o_lossp = k.take<double>(B * ((N + kLossThreads - 1) / kLossThreads));
   size_t o_pkey = k.take<uint32_t>(cu ? B * N : 0), o_gkey = k.take<uint32_t>(cu ? B * M : 0);
   size_t o_pstart = k.take<uint32_t>(B * cells1), o_gstart = k.take<uint32_t>(B * cells1);
   size_t o_pperm = k.take<int>(cu ? B * c->Np : 0), o_gperm = k.take<int>(cu ? B * c->Mp : 0);
@@ -311,6 +321,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->pbb = (float*)(p + o_pbb); c->pcb = (float*)(p + o_pcb); c->gcb = (float*)(p + o_gcb);
   c->pfb = (float*)(p + o_pfb); c->gfb = (float*)(p + o_gfb);
   c->gce2 = (float*)(p + o_gce2); c->gfe2 = (float*)(p + o_gfe2); c->gre = (float2*)(p + o_gre);
+  c->bbpart = (float*)(p + o_bbpart); c->tsum = (unsigned*)(p + o_tsum); c->lossp = (double*)(p + o_lossp);
   c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
   c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
   c->pstart = (uint32_t*)(p + o_pstart); c->gstart = (uint32_t*)(p + o_gstart);
@@ -390,6 +401,19 @@ apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a0, cu
   return APML_OK;
 }
 
+ScanJob scan_job(unsigned* cnt, unsigned* ptr, size_t stride, int len, unsigned* tsum) {
+  return ScanJob{cnt, ptr, tsum, stride, len, (int)scan_tiles(len)};
+}
+// Exclusive scans of two batched count arrays (k_scan_* in k_rowshard.cuh): 3 launches.
+void launch_scan(apml_ctx* c, const ScanJob& j0, const ScanJob& j1) {
+  const ScanJobs J{{j0, j1}};
+  const int B = (int)c->B, mt = std::max(j0.ntiles, j1.ntiles);
+  k_scan_reduce<<<dim3(mt, B, 2), kScanThreads, 0, c->stream>>>(J);
+  k_scan_tiles<<<dim3(1, B, 2), 1024, 0, c->stream>>>(J);
+  k_scan_apply<<<dim3(mt, B, 2), kScanThreads, 0, c->stream>>>(J);
+  c->launches += 3;
+}
+
 // Culled sweeps: Morton-order both clouds, then Pass A over the sorted clouds
 // with tile culling.  Leaves part_r [B][N] and part_c [B][M] (original indices, S = 1).
 apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
@@ -398,10 +422,13 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   const int bits = c->cell_bits;
   k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, nullptr, c->pred4);
   k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, nullptr, c->gt4);
-  k_pair_bbox<<<B, 1024, 0, s>>>(pred, N, gt, M, c->pbb);
+  k_pair_bbox_part<<<dim3(kBoxParts, B), kBoxThreads, 0, s>>>(pred, N, gt, M, c->bbpart);
+  k_pair_bbox_fin<<<B, 32, 0, s>>>(c->bbpart, kBoxParts, c->pbb);
   k_cell_count<<<dim3((N + 255) / 256, B), 256, 0, s>>>(pred, N, c->pbb, bits, c->pkey, c->phist);
   k_cell_count<<<dim3((M + 255) / 256, B), 256, 0, s>>>(gt, M, c->pbb, bits, c->gkey, c->ghist);
-  k_cell_scan<<<dim3(B, 2), 1024, 0, s>>>(c->phist, c->pstart, c->ghist, c->gstart, (1 << (3 * bits)));
+  const int cells1 = (1 << (3 * bits)) + 1;
+  launch_scan(c, scan_job(c->phist, c->pstart, cells1, cells1, c->tsum),
+              scan_job(c->ghist, c->gstart, cells1, cells1, c->tsum + (size_t)B * scan_tiles(cells1)));
   k_cell_scatter<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, bits, c->pkey, c->pstart,
       c->phist, c->predS, c->pperm);
   k_cell_scatter<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, bits, c->gkey, c->gstart,
@@ -414,7 +441,7 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 2, s);
   k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
       c->predS, Np, c->pcb, c->pfb, c->part_c);
-  c->launches += 12;
+  c->launches += 13;  // + the scan's own
   CK(cudaGetLastError());
   return APML_OK;
 }
@@ -572,7 +599,8 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
   const dim3 gr((N + kRsThreads - 1) / kRsThreads, B), gc((M + kRsThreads - 1) / kRsThreads, B);
   const dim3 gr256((N + 255) / 256, B), gc256((M + 255) / 256, B);
   apml_status st;
-  k_rs_scan<<<B, 1024, 0, s>>>(a);
+  launch_scan(c, scan_job(c->row_cnt, c->row_ptr, N + 1, N + 1, c->tsum),
+              scan_job(c->col_cnt, c->col_ptr, M + 1, M + 1, c->tsum + (size_t)B * scan_tiles(N + 1)));
   k_rs_scatter<<<dim3((c->cap + 255) / 256, B), 256, 0, s>>>(a);
   k_rs_rows<<<gr, kRsThreads, 0, s>>>(a);
   k_rs_cols_a<<<gc, kRsThreads, 0, s>>>(a);
@@ -582,7 +610,7 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
   k_rs_cols_b<<<gc, kRsThreads, 0, s>>>(a, c->gcand, c->comm.world);
   k_rs_bstep<<<gc256, 256, 0, s>>>(a, 0, nullptr);
   k_rs_astep<<<gr256, 256, 0, s>>>(a, 0);
-  c->launches += 7;
+  c->launches += 6;  // + the scan's own
   for (int l = 1; l <= L; ++l) {  // Eq. (3) column sums all-reduced (X3), Eq. (4) local
     k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
     CK(cudaGetLastError());
@@ -591,7 +619,12 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
     k_rs_astep<<<gr256, 256, 0, s>>>(a, l);
     c->launches += 3;
   }
-  k_rs_loss<<<B, 1024, 0, s>>>(a);
+  {
+    const int nblk = (N + kLossThreads - 1) / kLossThreads;
+    k_rs_loss_part<<<dim3(nblk, B), kLossThreads, 0, s>>>(a, c->lossp);
+    k_rs_loss_fin<<<B, 256, 0, s>>>(a, c->lossp, nblk);
+    c->launches += 1;
+  }
   CK(cudaGetLastError());
   if ((st = coll_sum(c, loss, B)) != APML_OK) return st;
   mark(c, 6, s);

@@ -23,17 +23,19 @@ constexpr float kCullMargin = 1.0f - 1e-5f;
 constexpr int kSub = 32;                   // culling granularity of the streamed side
 constexpr int kSubPerTile = kTQ / kSub;
 
-// Joint bounding box of pred and gt of each pair: bb[b] = {lo x,y,z, hi x,y,z}.
-__global__ void __launch_bounds__(1024)
-k_pair_bbox(const float* __restrict__ pred, int N, const float* __restrict__ gt, int M, float* __restrict__ bb) {
-  const int b = blockIdx.x;
+// Joint bounding box of pred and gt of each pair: partial boxes over P chunks of the points
+// (grid (P, B)), then bb[b] = {lo x,y,z, hi x,y,z} (min / max are exact in any order).
+constexpr int kBoxThreads = 256;
+__global__ void __launch_bounds__(kBoxThreads)
+k_pair_bbox_part(const float* __restrict__ pred, int N, const float* __restrict__ gt, int M, float* __restrict__ part) {
+  const int b = blockIdx.y, P = gridDim.x;
   float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
-  for (int k = threadIdx.x; k < N + M; k += blockDim.x) {
+  for (int k = blockIdx.x * kBoxThreads + threadIdx.x; k < N + M; k += P * kBoxThreads) {
     const float* p = k < N ? pred + ((size_t)b * N + k) * 3 : gt + ((size_t)b * M + (k - N)) * 3;
 #pragma unroll
     for (int d = 0; d < 3; ++d) { lo[d] = fminf(lo[d], p[d]); hi[d] = fmaxf(hi[d], p[d]); }
   }
-  __shared__ float red[6][32];
+  __shared__ float red[6][kBoxThreads / 32];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     for (int o = 16; o > 0; o >>= 1) {
@@ -47,10 +49,21 @@ k_pair_bbox(const float* __restrict__ pred, int N, const float* __restrict__ gt,
   __syncthreads();
   if (threadIdx.x < 6) {
     float v = threadIdx.x < 3 ? 3e38f : -3e38f;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k)
+    for (int k = 0; k < kBoxThreads / 32; ++k)
       v = threadIdx.x < 3 ? fminf(v, red[threadIdx.x][k]) : fmaxf(v, red[threadIdx.x][k]);
-    bb[b * 6 + threadIdx.x] = v;
+    part[((size_t)b * P + blockIdx.x) * 6 + threadIdx.x] = v;
   }
+}
+
+__global__ void k_pair_bbox_fin(const float* __restrict__ part, int P, float* __restrict__ bb) {
+  const int b = blockIdx.x, d = threadIdx.x;
+  if (d >= 6) return;
+  float v = d < 3 ? 3e38f : -3e38f;
+  for (int k = 0; k < P; ++k) {
+    const float u = part[((size_t)b * P + k) * 6 + d];
+    v = d < 3 ? fminf(v, u) : fmaxf(v, u);
+  }
+  bb[b * 6 + d] = v;
 }
 
 __device__ __forceinline__ uint32_t spread_bits3(uint32_t v) {  // 10-bit v -> every third bit

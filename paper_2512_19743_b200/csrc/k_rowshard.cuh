@@ -32,19 +32,27 @@ __global__ void k_top2_collapse(const float2* __restrict__ part, int S, int B, i
 
 // ---------------------------------------------------------------- CSR / CSC (local entries)
 
-// Single-CTA exclusive scan of cnt[0..n] -> ptr (zeroes cnt for the scatter cursors).
-__device__ void block_scan(unsigned* cnt, unsigned* ptr, int n, unsigned* s_warp) {
-  const int len = n + 1;
-  const int per = (len + blockDim.x - 1) / blockDim.x;
-  const int beg = threadIdx.x * per, end = min(len, beg + per);
-  unsigned sum = 0;
-  for (int k = beg; k < end; ++k) sum += cnt[k];
+// Batched multi-CTA exclusive scan of count arrays (CSR/CSC pointers, Morton-cell starts):
+// per-tile sums, a per-array scan of the tile sums, then a rescan of every tile with its
+// offset.  Loads and stores are coalesced; blockIdx.z selects one of two jobs, blockIdx.y
+// the pair.  The counts are zeroed on the way (they are reused as scatter cursors).
+constexpr int kScanThreads = 256, kScanPer = 8, kScanTile = kScanThreads * kScanPer;
+struct ScanJob {
+  unsigned* cnt;   // [B][stride], len used
+  unsigned* ptr;   // [B][stride] exclusive prefix sums
+  unsigned* tsum;  // [B][ntiles] tile sums, then tile offsets
+  size_t stride;
+  int len, ntiles;
+};
+struct ScanJobs { ScanJob j[2]; };
+
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* s_warp, unsigned* total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned inc = sum;
+  unsigned inc = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const unsigned v = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += v;
+    const unsigned u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
   }
   if (lane == 31) s_warp[w] = inc;
   __syncthreads();
@@ -52,28 +60,97 @@ __device__ void block_scan(unsigned* cnt, unsigned* ptr, int n, unsigned* s_warp
     unsigned t = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += v;
+      const unsigned u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
     }
     s_warp[lane] = t;
   }
   __syncthreads();
-  unsigned run = inc - sum + (w ? s_warp[w - 1] : 0u);
-  for (int k = beg; k < end; ++k) {
-    const unsigned v = cnt[k];
-    ptr[k] = run;
-    run += v;
-    cnt[k] = 0u;
-  }
+  const unsigned r = inc - v + (w ? s_warp[w - 1] : 0u);
+  if (total) *total = s_warp[(blockDim.x >> 5) - 1];
   __syncthreads();
+  return r;
 }
 
-__global__ void __launch_bounds__(1024) k_rs_scan(const SparseArgs A) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const ScanJobs J) {
+  const ScanJob jb = blockIdx.z ? J.j[1] : J.j[0];
+  const int b = blockIdx.y, tile = blockIdx.x;
+  if (tile >= jb.ntiles) return;
+  const unsigned* c = jb.cnt + (size_t)b * jb.stride;
+  unsigned v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int idx = tile * kScanTile + k * kScanThreads + threadIdx.x;
+    if (idx < jb.len) v += c[idx];
+  }
+  v = __reduce_add_sync(0xffffffffu, v);
+  __shared__ unsigned s_w[kScanThreads / 32];
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) t += s_w[w];
+    jb.tsum[(size_t)b * jb.ntiles + tile] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_scan_tiles(const ScanJobs J) {
+  const ScanJob jb = blockIdx.z ? J.j[1] : J.j[0];
   __shared__ unsigned s_warp[32];
-  const int b = blockIdx.x;
-  if (A.cursor[b] > A.cap) return;
-  block_scan(A.row_cnt + (size_t)b * (A.N + 1), A.row_ptr + (size_t)b * (A.N + 1), A.N, s_warp);
-  block_scan(A.col_cnt + (size_t)b * (A.M + 1), A.col_ptr + (size_t)b * (A.M + 1), A.M, s_warp);
+  unsigned* t = jb.tsum + (size_t)blockIdx.y * jb.ntiles;
+  unsigned carry = 0;
+  for (int base = 0; base < jb.ntiles; base += blockDim.x) {
+    const int k = base + threadIdx.x;
+    const unsigned v = k < jb.ntiles ? t[k] : 0u;
+    unsigned tot;
+    const unsigned e = block_excl_scan(v, s_warp, &tot);
+    if (k < jb.ntiles) t[k] = carry + e;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_apply(const ScanJobs J) {
+  const ScanJob jb = blockIdx.z ? J.j[1] : J.j[0];
+  const int b = blockIdx.y, tile = blockIdx.x;
+  if (tile >= jb.ntiles) return;
+  __shared__ unsigned s_v[kScanTile + kScanTile / 32];
+  __shared__ unsigned s_warp[32];
+  unsigned* c = jb.cnt + (size_t)b * jb.stride;
+  unsigned* out = jb.ptr + (size_t)b * jb.stride;
+  const int base = tile * kScanTile;
+  const int len = jb.len;
+  unsigned v[kScanPer];
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {  // all loads in flight before any store
+    const int idx = base + k * kScanThreads + threadIdx.x;
+    v[k] = idx < len ? c[idx] : 0u;
+  }
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int e = k * kScanThreads + threadIdx.x;
+    if (base + e < len) c[base + e] = 0u;
+    s_v[e + (e >> 5)] = v[k];
+  }
+  __syncthreads();
+  unsigned loc[kScanPer], sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int e = threadIdx.x * kScanPer + k;
+    loc[k] = sum;
+    sum += s_v[e + (e >> 5)];
+  }
+  const unsigned off = block_excl_scan(sum, s_warp, nullptr) + jb.tsum[(size_t)b * jb.ntiles + tile];
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int e = threadIdx.x * kScanPer + k;
+    s_v[e + (e >> 5)] = off + loc[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int e = k * kScanThreads + threadIdx.x, idx = base + e;
+    if (idx < jb.len) out[idx] = s_v[e + (e >> 5)];
+  }
 }
 
 __global__ void k_rs_scatter(const SparseArgs A) {
@@ -205,20 +282,78 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_b(const SparseArgs A, co
   }
 }
 
+// ---------------------------------------------------------------- warp-cooperative lines
+// The per-iteration kernels below run 256-thread blocks, one warp per 32 consecutive lines:
+// the warp walks the lines' contiguous entry range in chunks of kWChunk entries, staging the
+// per-entry factors with coalesced loads (entry-parallel), then every lane folds its own
+// line's staged factors in entry order -- the same sequential fma chain as a thread-per-line
+// loop, without its uncoalesced, latency-serialised loads.
+constexpr int kWChunk = 128;
+constexpr int kWWarps = 8;  // warps per 256-thread block
+
+struct WarpLines {
+  uint32_t beg, end;  // this lane's line [beg, end) (empty past the last line)
+  uint32_t e0, e1;    // the warp's entry range
+};
+__device__ __forceinline__ WarpLines warp_lines(const unsigned* ptr, int line, int n) {
+  WarpLines w;
+  w.beg = ptr[min(line, n)];
+  w.end = ptr[min(line + 1, n)];
+  w.e0 = __shfl_sync(0xffffffffu, w.beg, 0);
+  w.e1 = __shfl_sync(0xffffffffu, w.end, 31);
+  return w;
+}
+
+// stage(k, q): entry-parallel, k = slot in the chunk, q = entry; line(k): the owning lane,
+// in entry order; post(k, q): entry-parallel again with s_own[k] = owning lane.
+template <class Stage, class Line, class Post>
+__device__ __forceinline__ void warp_walk(const WarpLines& w, unsigned char* s_own, Stage stage, Line line,
+                                          Post post) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = w.e0; base < w.e1; base += kWChunk) {
+#pragma unroll
+    for (int k0 = 0; k0 < kWChunk; k0 += 32) {
+      const uint32_t q = base + k0 + lane;
+      if (q < w.e1) stage(k0 + lane, q);
+    }
+    __syncwarp();
+    const uint32_t lo = max(w.beg, base), hi = min(w.end, base + kWChunk);
+    for (uint32_t q = lo; q < hi; ++q) {
+      if (s_own) s_own[q - base] = (unsigned char)lane;
+      line((int)(q - base));
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k0 = 0; k0 < kWChunk; k0 += 32) {
+      const uint32_t q = base + k0 + lane;
+      if (q < w.e1) post(k0 + lane, q);
+    }
+    __syncwarp();
+  }
+}
+struct NoPost {
+  __device__ void operator()(int, uint32_t) const {}
+};
+
 // ---------------------------------------------------------------- Sinkhorn (X3)
 
 // out[b][j] = sum over this rank's entries of column j of w[i] * P0_ij  (w: N-vector).
-__global__ void k_rs_colsum(const SparseArgs A, const float* __restrict__ w, size_t w_stride,
-                            float* __restrict__ out, size_t out_stride) {
-  const int b = blockIdx.y, M = A.M;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (A.cursor[b] > A.cap || j >= M) return;
+__global__ void __launch_bounds__(256) k_rs_colsum(const SparseArgs A, const float* __restrict__ w,
+                                                   size_t w_stride, float* __restrict__ out, size_t out_stride) {
+  __shared__ float s_x[kWWarps][kWChunk], s_y[kWWarps][kWChunk];
+  const int b = blockIdx.y, M = A.M, wid = threadIdx.x >> 5;
+  const int j = (blockIdx.x * kWWarps + wid) * 32 + (threadIdx.x & 31);
+  if (A.cursor[b] > A.cap || j - (threadIdx.x & 31) >= M) return;  // warp-uniform
   const size_t pb = (size_t)b * A.cap;
-  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
   const float* wb = w + (size_t)b * w_stride;
+  const WarpLines wl = warp_lines(A.col_ptr + (size_t)b * (M + 1), j, M);
+  float* sx = s_x[wid];
+  float* sy = s_y[wid];
   float t = 0.f;
-  for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) t = __fmaf_rn(wb[A.csc_i[pb + q]], A.P0c[pb + q], t);
-  out[(size_t)b * out_stride + j] = t;
+  warp_walk(wl, nullptr,
+            [&](int k, uint32_t q) { sx[k] = wb[A.csc_i[pb + q]]; sy[k] = A.P0c[pb + q]; },
+            [&](int k) { t = __fmaf_rn(sx[k], sy[k], t); }, NoPost{});
+  if (j < M) out[(size_t)b * out_stride + j] = t;
 }
 
 // Column step of Eq. (3) on the all-reduced Q: b_j <- b_j / (b_j Q_j + eps) (every rank).
@@ -237,43 +372,51 @@ __global__ void k_rs_bstep(const SparseArgs A, int l, const float* __restrict__ 
 }
 
 // Row step of Eq. (4) (local rows): a_i <- a_i / (a_i R_i + eps), R_i = sum_j P0_ij b_j.
-__global__ void k_rs_astep(const SparseArgs A, int l) {
-  const int b = blockIdx.y, N = A.N;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N || A.cursor[b] > A.cap) return;
+__global__ void __launch_bounds__(256) k_rs_astep(const SparseArgs A, int l) {
+  __shared__ float s_x[kWWarps][kWChunk], s_y[kWWarps][kWChunk];
+  const int b = blockIdx.y, N = A.N, wid = threadIdx.x >> 5;
+  const int i = (blockIdx.x * kWWarps + wid) * 32 + (threadIdx.x & 31);
+  if (A.cursor[b] > A.cap || i - (threadIdx.x & 31) >= N) return;  // warp-uniform
   const size_t pb = (size_t)b * A.cap;
   float* a = A.gvec + (size_t)b * 2 * (N + A.M);
   const float* bv = a + N;
   float na = 1.f;
   if (l > 0) {
-    const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+    const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
+    float* sx = s_x[wid];
+    float* sy = s_y[wid];
     float Rs = 0.f;
-    for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) Rs = __fmaf_rn(A.P0[pb + p], bv[A.csr_jf[pb + p] & kIdxMask], Rs);
-    const float ai = a[i];
-    na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+    warp_walk(wl, nullptr,
+              [&](int k, uint32_t q) { sx[k] = A.P0[pb + q]; sy[k] = bv[A.csr_jf[pb + q] & kIdxMask]; },
+              [&](int k) { Rs = __fmaf_rn(sx[k], sy[k], Rs); }, NoPost{});
+    if (i < N) {
+      const float ai = a[i];
+      na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+    }
   }
-  a[i] = na;
-  A.a_hist[((size_t)b * (A.L + 1) + l) * N + i] = na;
+  if (i < N) {
+    a[i] = na;
+    A.a_hist[((size_t)b * (A.L + 1) + l) * N + i] = na;
+  }
 }
 
-// This rank's part of loss_b = sum_i a_i sum_j P0_ij b_j c_ij (deterministic block sum).
-__global__ void __launch_bounds__(1024) k_rs_loss(const SparseArgs A) {
-  __shared__ double red[32];
-  const int b = blockIdx.x, N = A.N;
-  if (A.cursor[b] > A.cap) {
-    if (threadIdx.x == 0) A.loss[b] = __int_as_float(0x7fc00000);
-    return;
-  }
-  const size_t pb = (size_t)b * A.cap;
-  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
-  const float* a = A.gvec + (size_t)b * 2 * (N + A.M);
-  const float* bv = a + N;
+// This rank's part of loss_b = sum_i a_i sum_j P0_ij b_j c_ij: per-block partials in fp64
+// (k_rs_loss_part, grid over rows), then a fixed-order per-pair sum (k_rs_loss_fin).
+constexpr int kLossThreads = 256;
+__global__ void __launch_bounds__(kLossThreads) k_rs_loss_part(const SparseArgs A, double* __restrict__ part) {
+  __shared__ double red[kLossThreads / 32];
+  const int b = blockIdx.y, N = A.N;
+  const int i = blockIdx.x * kLossThreads + threadIdx.x;
   double acc = 0.0;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+  if (A.cursor[b] <= A.cap && i < N) {
+    const size_t pb = (size_t)b * A.cap;
+    const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+    const float* a = A.gvec + (size_t)b * 2 * (N + A.M);
+    const float* bv = a + N;
     float t = 0.f;
     for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
       t = __fmaf_rn(__fmul_rn(A.P0[pb + p], bv[A.csr_jf[pb + p] & kIdxMask]), A.cs[pb + p], t);
-    acc += (double)a[i] * (double)t;
+    acc = (double)a[i] * (double)t;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
@@ -281,8 +424,24 @@ __global__ void __launch_bounds__(1024) k_rs_loss(const SparseArgs A) {
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
+    for (int w = 0; w < kLossThreads / 32; ++w) t += red[w];
+    part[(size_t)b * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_rs_loss_fin(const SparseArgs A, const double* __restrict__ part, int nblk) {
+  __shared__ double red[8];
+  const int b = blockIdx.x;
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < nblk; k += blockDim.x) acc += part[(size_t)b * nblk + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    A.loss[b] = (float)t;
+    A.loss[b] = A.cursor[b] > A.cap ? __int_as_float(0x7fc00000) : (float)t;
   }
 }
 
@@ -329,22 +488,31 @@ __global__ void k_rs_bwd_set_bbar(const SparseArgs A, const float* __restrict__ 
 }
 
 // Row step reverse at iteration l (local rows): Rbar, abar, P0bar += Rbar^l_i b^l_j.
-__global__ void k_rs_bwd_rowrev(const SparseArgs A, int l) {
-  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N || A.cursor[b] > A.cap) return;
+__global__ void __launch_bounds__(256) k_rs_bwd_rowrev(const SparseArgs A, int l) {
+  __shared__ float s_v[kWWarps][32];
+  __shared__ unsigned char s_own[kWWarps][kWChunk];
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || i - lane >= N) return;  // warp-uniform
   const size_t pb = (size_t)b * A.cap;
   float* ab = A.gvec + (size_t)b * 2 * (N + M);
   float* rcur = ab + N + M;
-  const float al = A.a_hist[((size_t)b * (L + 1) + l) * N + i];
-  const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
-  const float r = al / alm;
-  const float Rb = -ab[i] * al * al;
-  ab[i] = ab[i] * A.eps * r * r;
-  rcur[i] = Rb;
-  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  float Rb = 0.f;
+  if (i < N) {
+    const float al = A.a_hist[((size_t)b * (L + 1) + l) * N + i];
+    const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
+    const float r = al / alm;
+    Rb = -ab[i] * al * al;
+    ab[i] = ab[i] * A.eps * r * r;
+    rcur[i] = Rb;
+  }
+  s_v[wid][lane] = Rb;
   const float* bl = A.b_hist + ((size_t)b * (L + 1) + l) * M;
-  for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) A.pbar[pb + p] += Rb * bl[A.csr_jf[pb + p] & kIdxMask];
+  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
+  unsigned char* own = s_own[wid];
+  const float* v = s_v[wid];
+  warp_walk(wl, own, [&](int, uint32_t) {}, [&](int) {},
+            [&](int k, uint32_t q) { A.pbar[pb + q] += v[own[k]] * bl[A.csr_jf[pb + q] & kIdxMask]; });
 }
 
 // Column step reverse (every rank, all columns) on the all-reduced t = P0^T Rbar^l.
@@ -363,22 +531,27 @@ __global__ void k_rs_bwd_colrev(const SparseArgs A, int l, const float* __restri
 }
 
 // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (local rows).
-__global__ void k_rs_bwd_rowrev2(const SparseArgs A, int l) {
-  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= N || A.cursor[b] > A.cap) return;
+__global__ void __launch_bounds__(256) k_rs_bwd_rowrev2(const SparseArgs A, int l) {
+  __shared__ float s_x[kWWarps][kWChunk], s_y[kWWarps][kWChunk], s_v[kWWarps][32];
+  __shared__ unsigned char s_own[kWWarps][kWChunk];
+  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || i - lane >= N) return;  // warp-uniform
   const size_t pb = (size_t)b * A.cap;
   float* ab = A.gvec + (size_t)b * 2 * (N + M);
   const float* qcur = ab + N + M + N;
-  const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
-  const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
+  s_v[wid][lane] = i < N ? A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i] : 0.f;
+  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
+  float* sx = s_x[wid];
+  float* sy = s_y[wid];
+  unsigned char* own = s_own[wid];
+  const float* alm = s_v[wid];
   float t = 0.f;
-  for (uint32_t p = rp[i]; p < rp[i + 1]; ++p) {
-    const float qv = qcur[A.csr_jf[pb + p] & kIdxMask];
-    t = __fmaf_rn(qv, A.P0[pb + p], t);
-    A.pbar[pb + p] += qv * alm;
-  }
-  ab[i] += t;
+  warp_walk(wl, own,
+            [&](int k, uint32_t q) { sx[k] = qcur[A.csr_jf[pb + q] & kIdxMask]; sy[k] = A.P0[pb + q]; },
+            [&](int k) { t = __fmaf_rn(sx[k], sy[k], t); },
+            [&](int k, uint32_t q) { A.pbar[pb + q] += sx[k] * alm[own[k]]; });
+  if (i < N) ab[i] += t;
 }
 
 // Row softmax reverse (local rows).
@@ -457,16 +630,6 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_grad(const SparseArgs A) {
   const LongList ll = collect_long(A.row_ptr + (size_t)b * (A.N + 1), s, s_long, &s_n);
   grad_rows<1, 4>(A, b, s, ll);
   grad_rows<32, 1>(A, b, s, ll);
-}
-
-// Per-pair exclusive scan of the Morton-cell histograms (k_cull.cuh); blockIdx.y = cloud.
-__global__ void __launch_bounds__(1024) k_cell_scan(uint32_t* phist, uint32_t* pstart, uint32_t* ghist,
-                                                    uint32_t* gstart, int cells) {
-  __shared__ unsigned s_warp[32];
-  const int b = blockIdx.x;
-  uint32_t* h = (blockIdx.y ? ghist : phist) + (size_t)b * (cells + 1);
-  uint32_t* st = (blockIdx.y ? gstart : pstart) + (size_t)b * (cells + 1);
-  block_scan(h, st, cells, s_warp);
 }
 
 }  // namespace apml
