@@ -337,54 +337,44 @@ struct NoPost {
 
 // ---------------------------------------------------------------- Sinkhorn (X3)
 
-// out[b][j] = sum over this rank's entries of column j of w[i] * P0_ij  (w: N-vector).
-__global__ void __launch_bounds__(256) k_rs_colsum(const SparseArgs A, const float* __restrict__ w,
-                                                   size_t w_stride, float* __restrict__ out, size_t out_stride) {
-  __shared__ float s_x[kWWarps][kWChunk], s_y[kWWarps][kWChunk];
-  const int b = blockIdx.y, M = A.M, wid = threadIdx.x >> 5;
-  const int j = (blockIdx.x * kWWarps + wid) * 32 + (threadIdx.x & 31);
-  if (A.cursor[b] > A.cap || j - (threadIdx.x & 31) >= M) return;  // warp-uniform
+// Per-group bodies (one warp, 32 consecutive lines of pair b; `line` = this lane's line),
+// shared by the per-step kernels (row sharding: a collective between the steps) and the
+// persistent single-GPU kernels further down.  sx / sy / sv / own: the warp's shared memory.
+
+// sum over this rank's entries of column j of w[i] * P0_ij  (w: pair b's N-vector)
+__device__ __forceinline__ float grp_colsum(const SparseArgs& A, int b, int j, const float* wb, float* sx,
+                                            float* sy) {
   const size_t pb = (size_t)b * A.cap;
-  const float* wb = w + (size_t)b * w_stride;
-  const WarpLines wl = warp_lines(A.col_ptr + (size_t)b * (M + 1), j, M);
-  float* sx = s_x[wid];
-  float* sy = s_y[wid];
+  const WarpLines wl = warp_lines(A.col_ptr + (size_t)b * (A.M + 1), j, A.M);
   float t = 0.f;
   warp_walk(wl, nullptr,
             [&](int k, uint32_t q) { sx[k] = wb[A.csc_i[pb + q]]; sy[k] = A.P0c[pb + q]; },
             [&](int k) { t = __fmaf_rn(sx[k], sy[k], t); }, NoPost{});
-  if (j < M) out[(size_t)b * out_stride + j] = t;
+  return t;
 }
 
-// Column step of Eq. (3) on the all-reduced Q: b_j <- b_j / (b_j Q_j + eps) (every rank).
-__global__ void k_rs_bstep(const SparseArgs A, int l, const float* __restrict__ Q) {
-  const int b = blockIdx.y, M = A.M;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= M) return;
-  float* bv = A.gvec + (size_t)b * 2 * (A.N + M) + A.N;
+// Column step of Eq. (3): b_j <- b_j / (b_j Q_j + eps)
+__device__ __forceinline__ void grp_bstep(const SparseArgs& A, int b, int j, int l, float Q) {
+  if (j >= A.M) return;
+  float* bv = A.gvec + (size_t)b * 2 * (A.N + A.M) + A.N;
   float nb = 1.f;
   if (l > 0) {
     const float bj = bv[j];
-    nb = __fdividef(bj, __fmaf_rn(bj, Q[(size_t)b * M + j], A.eps));
+    nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
   }
   bv[j] = nb;
-  A.b_hist[((size_t)b * (A.L + 1) + l) * M + j] = nb;
+  A.b_hist[((size_t)b * (A.L + 1) + l) * A.M + j] = nb;
 }
 
-// Row step of Eq. (4) (local rows): a_i <- a_i / (a_i R_i + eps), R_i = sum_j P0_ij b_j.
-__global__ void __launch_bounds__(256) k_rs_astep(const SparseArgs A, int l) {
-  __shared__ float s_x[kWWarps][kWChunk], s_y[kWWarps][kWChunk];
-  const int b = blockIdx.y, N = A.N, wid = threadIdx.x >> 5;
-  const int i = (blockIdx.x * kWWarps + wid) * 32 + (threadIdx.x & 31);
-  if (A.cursor[b] > A.cap || i - (threadIdx.x & 31) >= N) return;  // warp-uniform
+// Row step of Eq. (4) (local rows): a_i <- a_i / (a_i R_i + eps), R_i = sum_j P0_ij b_j
+__device__ __forceinline__ void grp_astep(const SparseArgs& A, int b, int i, int l, float* sx, float* sy) {
+  const int N = A.N;
   const size_t pb = (size_t)b * A.cap;
   float* a = A.gvec + (size_t)b * 2 * (N + A.M);
   const float* bv = a + N;
   float na = 1.f;
   if (l > 0) {
     const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
-    float* sx = s_x[wid];
-    float* sy = s_y[wid];
     float Rs = 0.f;
     warp_walk(wl, nullptr,
               [&](int k, uint32_t q) { sx[k] = A.P0[pb + q]; sy[k] = bv[A.csr_jf[pb + q] & kIdxMask]; },
@@ -398,6 +388,92 @@ __global__ void __launch_bounds__(256) k_rs_astep(const SparseArgs A, int l) {
     a[i] = na;
     A.a_hist[((size_t)b * (A.L + 1) + l) * N + i] = na;
   }
+}
+
+// Reverse of the row step at iteration l (local rows): Rbar, abar, P0bar += Rbar^l_i b^l_j
+__device__ __forceinline__ void grp_rowrev(const SparseArgs& A, int b, int i, int l, float* sv,
+                                           unsigned char* own) {
+  const int N = A.N, M = A.M, L = A.L, lane = threadIdx.x & 31;
+  const size_t pb = (size_t)b * A.cap;
+  float* ab = A.gvec + (size_t)b * 2 * (N + M);
+  float* rcur = ab + N + M;
+  float Rb = 0.f;
+  if (i < N) {
+    const float al = A.a_hist[((size_t)b * (L + 1) + l) * N + i];
+    const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
+    const float r = al / alm;
+    Rb = -ab[i] * al * al;
+    ab[i] = ab[i] * A.eps * r * r;
+    rcur[i] = Rb;
+  }
+  sv[lane] = Rb;
+  const float* bl = A.b_hist + ((size_t)b * (L + 1) + l) * M;
+  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
+  warp_walk(wl, own, [&](int, uint32_t) {}, [&](int) {},
+            [&](int k, uint32_t q) { A.pbar[pb + q] += sv[own[k]] * bl[A.csr_jf[pb + q] & kIdxMask]; });
+}
+
+// Column step reverse on t = P0^T Rbar^l (summed over the ranks)
+__device__ __forceinline__ void grp_colrev(const SparseArgs& A, int b, int j, int l, float t) {
+  const int N = A.N, M = A.M, L = A.L;
+  if (j >= M) return;
+  float* bb = A.gvec + (size_t)b * 2 * (N + M) + N;
+  float* qcur = bb + M + N;
+  const float bsum = bb[j] + t;
+  const float bl = A.b_hist[((size_t)b * (L + 1) + l) * M + j];
+  const float blm = A.b_hist[((size_t)b * (L + 1) + l - 1) * M + j];
+  const float r = bl / blm;
+  bb[j] = bsum * A.eps * r * r;
+  qcur[j] = -bsum * bl * bl;
+}
+
+// abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (local rows)
+__device__ __forceinline__ void grp_rowrev2(const SparseArgs& A, int b, int i, int l, float* sx, float* sy,
+                                            float* sv, unsigned char* own) {
+  const int N = A.N, M = A.M, L = A.L, lane = threadIdx.x & 31;
+  const size_t pb = (size_t)b * A.cap;
+  float* ab = A.gvec + (size_t)b * 2 * (N + M);
+  const float* qcur = ab + N + M + N;
+  sv[lane] = i < N ? A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i] : 0.f;
+  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
+  float t = 0.f;
+  warp_walk(wl, own,
+            [&](int k, uint32_t q) { sx[k] = qcur[A.csr_jf[pb + q] & kIdxMask]; sy[k] = A.P0[pb + q]; },
+            [&](int k) { t = __fmaf_rn(sx[k], sy[k], t); },
+            [&](int k, uint32_t q) { A.pbar[pb + q] += sx[k] * sv[own[k]]; });
+  if (i < N) ab[i] += t;
+}
+
+// Shared memory of one 256-thread block of the group kernels.
+struct GrpSmem {
+  float x[kWWarps][kWChunk], y[kWWarps][kWChunk], v[kWWarps][32];
+  unsigned char own[kWWarps][kWChunk];
+};
+
+// ---- per-step kernels (grid (lines / 256, B); a collective may follow each one)
+
+__global__ void __launch_bounds__(256) k_rs_colsum(const SparseArgs A, const float* __restrict__ w,
+                                                   size_t w_stride, float* __restrict__ out, size_t out_stride) {
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || j - lane >= A.M) return;  // warp-uniform
+  const float t = grp_colsum(A, b, j, w + (size_t)b * w_stride, S.x[wid], S.y[wid]);
+  if (j < A.M) out[(size_t)b * out_stride + j] = t;
+}
+
+// Column step of Eq. (3) on the all-reduced Q (every rank).
+__global__ void k_rs_bstep(const SparseArgs A, int l, const float* __restrict__ Q) {
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  grp_bstep(A, b, j, l, (l > 0 && j < A.M) ? Q[(size_t)b * A.M + j] : 0.f);
+}
+
+__global__ void __launch_bounds__(256) k_rs_astep(const SparseArgs A, int l) {
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || i - lane >= A.N) return;  // warp-uniform
+  grp_astep(A, b, i, l, S.x[wid], S.y[wid]);
 }
 
 // This rank's part of loss_b = sum_i a_i sum_j P0_ij b_j c_ij: per-block partials in fp64
@@ -487,71 +563,25 @@ __global__ void k_rs_bwd_set_bbar(const SparseArgs A, const float* __restrict__ 
   A.gvec[(size_t)b * 2 * (N + M) + N + j] = A.grad_loss[b] * red[(size_t)b * M + j];
 }
 
-// Row step reverse at iteration l (local rows): Rbar, abar, P0bar += Rbar^l_i b^l_j.
 __global__ void __launch_bounds__(256) k_rs_bwd_rowrev(const SparseArgs A, int l) {
-  __shared__ float s_v[kWWarps][32];
-  __shared__ unsigned char s_own[kWWarps][kWChunk];
-  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
-  if (A.cursor[b] > A.cap || i - lane >= N) return;  // warp-uniform
-  const size_t pb = (size_t)b * A.cap;
-  float* ab = A.gvec + (size_t)b * 2 * (N + M);
-  float* rcur = ab + N + M;
-  float Rb = 0.f;
-  if (i < N) {
-    const float al = A.a_hist[((size_t)b * (L + 1) + l) * N + i];
-    const float alm = A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i];
-    const float r = al / alm;
-    Rb = -ab[i] * al * al;
-    ab[i] = ab[i] * A.eps * r * r;
-    rcur[i] = Rb;
-  }
-  s_v[wid][lane] = Rb;
-  const float* bl = A.b_hist + ((size_t)b * (L + 1) + l) * M;
-  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
-  unsigned char* own = s_own[wid];
-  const float* v = s_v[wid];
-  warp_walk(wl, own, [&](int, uint32_t) {}, [&](int) {},
-            [&](int k, uint32_t q) { A.pbar[pb + q] += v[own[k]] * bl[A.csr_jf[pb + q] & kIdxMask]; });
+  if (A.cursor[b] > A.cap || i - lane >= A.N) return;  // warp-uniform
+  grp_rowrev(A, b, i, l, S.v[wid], S.own[wid]);
 }
 
-// Column step reverse (every rank, all columns) on the all-reduced t = P0^T Rbar^l.
 __global__ void k_rs_bwd_colrev(const SparseArgs A, int l, const float* __restrict__ t) {
-  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= M) return;
-  float* bb = A.gvec + (size_t)b * 2 * (N + M) + N;
-  float* qcur = bb + M + N;
-  const float bsum = bb[j] + t[(size_t)b * M + j];
-  const float bl = A.b_hist[((size_t)b * (L + 1) + l) * M + j];
-  const float blm = A.b_hist[((size_t)b * (L + 1) + l - 1) * M + j];
-  const float r = bl / blm;
-  bb[j] = bsum * A.eps * r * r;
-  qcur[j] = -bsum * bl * bl;
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < A.M) grp_colrev(A, b, j, l, t[(size_t)b * A.M + j]);
 }
 
-// abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (local rows).
 __global__ void __launch_bounds__(256) k_rs_bwd_rowrev2(const SparseArgs A, int l) {
-  __shared__ float s_x[kWWarps][kWChunk], s_y[kWWarps][kWChunk], s_v[kWWarps][32];
-  __shared__ unsigned char s_own[kWWarps][kWChunk];
-  const int b = blockIdx.y, N = A.N, M = A.M, L = A.L, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
-  if (A.cursor[b] > A.cap || i - lane >= N) return;  // warp-uniform
-  const size_t pb = (size_t)b * A.cap;
-  float* ab = A.gvec + (size_t)b * 2 * (N + M);
-  const float* qcur = ab + N + M + N;
-  s_v[wid][lane] = i < N ? A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i] : 0.f;
-  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
-  float* sx = s_x[wid];
-  float* sy = s_y[wid];
-  unsigned char* own = s_own[wid];
-  const float* alm = s_v[wid];
-  float t = 0.f;
-  warp_walk(wl, own,
-            [&](int k, uint32_t q) { sx[k] = qcur[A.csr_jf[pb + q] & kIdxMask]; sy[k] = A.P0[pb + q]; },
-            [&](int k) { t = __fmaf_rn(sx[k], sy[k], t); },
-            [&](int k, uint32_t q) { A.pbar[pb + q] += sx[k] * alm[own[k]]; });
-  if (i < N) ab[i] += t;
+  if (A.cursor[b] > A.cap || i - lane >= A.N) return;  // warp-uniform
+  grp_rowrev2(A, b, i, l, S.x[wid], S.y[wid], S.v[wid], S.own[wid]);
 }
 
 // Row softmax reverse (local rows).
