@@ -12,6 +12,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <array>
 
 #include "../../include/apml.h"
 #include "common.cuh"
@@ -91,6 +92,10 @@ struct apml_ctx {
   // batched scans (CSR/CSC pointers, Morton cells) and the grid-wide loss
   unsigned* tsum = nullptr;
   double* lossp = nullptr;
+  // Morton-relabelled sparse stage (culled, not row-sharded over ranks): line indices are
+  // sorted positions from Pass A on; ipperm [B][N] = sorted position of each original pred
+  bool relabel = false;
+  int* ipperm = nullptr;
   uint32_t *pkey = nullptr, *gkey = nullptr, *phist = nullptr, *ghist = nullptr, *pstart = nullptr, *gstart = nullptr;
   int *pperm = nullptr, *gperm = nullptr;
   // row-sharded mode
@@ -243,6 +248,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   // the cloud (override: APML_CULL=0/1)
   const long fc = env_long("APML_CULL", -1);
   c->cull = fc >= 0 ? fc != 0 : std::min(N, M) >= 4096;
+  c->relabel = c->cull && (!c->rs || (c->comm.world == 1 && c->row_offset == 0)) && env_long("APML_RELABEL", 1) != 0;
   if (c->cull) {
     int lg = 0;
     while ((1LL << lg) < std::max(N, M)) ++lg;
@@ -291,6 +297,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   const int64_t tiles_rc = scan_tiles(N + 1) + scan_tiles(M + 1), tiles_cells = 2 * scan_tiles(cells1);
   size_t o_tsum = k.take<unsigned>(B * std::max(tiles_rc, tiles_cells));
   size_t o_lossp = k.take<double>(B * ((N + kLossThreads - 1) / kLossThreads));
+  size_t o_ipperm = k.take<int>(c->relabel ? B * N : 0);
   size_t o_pkey = k.take<uint32_t>(cu ? B * N : 0), o_gkey = k.take<uint32_t>(cu ? B * M : 0);
   size_t o_pstart = k.take<uint32_t>(B * cells1), o_gstart = k.take<uint32_t>(B * cells1);
   size_t o_pperm = k.take<int>(cu ? B * c->Np : 0), o_gperm = k.take<int>(cu ? B * c->Mp : 0);
@@ -321,6 +328,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->pbb = (float*)(p + o_pbb); c->pcb = (float*)(p + o_pcb); c->gcb = (float*)(p + o_gcb);
   c->pfb = (float*)(p + o_pfb); c->gfb = (float*)(p + o_gfb);
   c->gce2 = (float*)(p + o_gce2); c->gfe2 = (float*)(p + o_gfe2); c->gre = (float2*)(p + o_gre);
+  c->ipperm = c->relabel ? (int*)(p + o_ipperm) : nullptr;
   c->bbpart = (float*)(p + o_bbpart); c->tsum = (unsigned*)(p + o_tsum); c->lossp = (double*)(p + o_lossp);
   c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
   c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
@@ -345,6 +353,10 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.smem_bytes = c->smem_bytes; a.rep_smem = c->rep_smem;
   a.dbg = nullptr;
   a.row_offset = (int)c->row_offset; a.colred = c->colred; a.cand = c->cand;
+  a.pperm = c->relabel ? c->pperm : nullptr;
+  a.gperm = c->relabel ? c->gperm : nullptr;
+  a.ipperm = c->relabel ? c->ipperm : nullptr;
+  a.perm_np = (int)c->Np; a.perm_mp = (int)c->Mp;
   return a;
 }
 
@@ -420,8 +432,11 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   const int bits = c->cell_bits;
-  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, nullptr, c->pred4);
-  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, nullptr, c->gt4);
+  if (!c->relabel) {  // float4 copies at original positions (relabelled: by k_cell_scatter)
+    k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, nullptr, c->pred4);
+    k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, nullptr, c->gt4);
+    c->launches += 2;
+  }
   k_pair_bbox_part<<<dim3(kBoxParts, B), kBoxThreads, 0, s>>>(pred, N, gt, M, c->bbpart);
   k_pair_bbox_fin<<<B, 32, 0, s>>>(c->bbpart, kBoxParts, c->pbb);
   k_cell_count<<<dim3((N + 255) / 256, B), 256, 0, s>>>(pred, N, c->pbb, bits, c->pkey, c->phist);
@@ -430,18 +445,18 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   launch_scan(c, scan_job(c->phist, c->pstart, cells1, cells1, c->tsum),
               scan_job(c->ghist, c->gstart, cells1, cells1, c->tsum + (size_t)B * scan_tiles(cells1)));
   k_cell_scatter<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, bits, c->pkey, c->pstart,
-      c->phist, c->predS, c->pperm);
+      c->phist, c->predS, c->pperm, c->relabel ? c->pred4 : nullptr, c->ipperm);
   k_cell_scatter<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, bits, c->gkey, c->gstart,
-      c->ghist, c->gtS, c->gperm);
+      c->ghist, c->gtS, c->gperm, c->relabel ? c->gt4 : nullptr, nullptr);
   k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->pcb, c->pfb);
   k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
   mark(c, 1, s);
   k_line_top2_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
-      c->gtS, Mp, c->gcb, c->gfb, c->part_r);
+      c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r);
   mark(c, 2, s);
   k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
-      c->predS, Np, c->pcb, c->pfb, c->part_c);
-  c->launches += 13;  // + the scan's own
+      c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c);
+  c->launches += 11;  // + the scan's own
   CK(cudaGetLastError());
   return APML_OK;
 }
@@ -449,9 +464,10 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
 apml_status launch_emit_cull(apml_ctx* c) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
-  k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, c->gre, c->gce2, c->gfe2);
+  k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
+                                               c->gfe2);
   k_emit_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
-      c->gtS, Mp, M, c->gperm, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor, c->aux,
+      c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor, c->aux,
       c->row_cnt, c->col_cnt);
   c->launches += 2;
   CK(cudaGetLastError());
@@ -922,16 +938,34 @@ apml_status apml_ctx_support(const apml_ctx* x, int64_t b, int64_t* count, int32
   }
   CK(cudaMemcpyAsync(aL.data(), x->a_hist + ((size_t)b * (L + 1) + L) * N, sizeof(float) * N, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaMemcpyAsync(bL.data(), x->b_hist + ((size_t)b * (L + 1) + L) * M, sizeof(float) * M, cudaMemcpyDeviceToHost, x->stream));
+  std::vector<int> pp, gp;  // relabelled: sorted position -> original index
+  if (x->relabel) {
+    pp.resize((size_t)x->Np);
+    gp.resize((size_t)x->Mp);
+    CK(cudaMemcpyAsync(pp.data(), x->pperm + (size_t)b * x->Np, sizeof(int) * x->Np, cudaMemcpyDeviceToHost, x->stream));
+    CK(cudaMemcpyAsync(gp.data(), x->gperm + (size_t)b * x->Mp, sizeof(int) * x->Mp, cudaMemcpyDeviceToHost, x->stream));
+  }
   CK(cudaStreamSynchronize(x->stream));
+  // (original i, original j, position) in CSR order of the original indices
+  std::vector<std::array<int64_t, 3>> ord;
+  ord.reserve(cur);
   for (int64_t i = 0; i < N; ++i)
     for (unsigned p = rp[i]; p < rp[i + 1]; ++p) {
       const uint32_t j = jf[p] & kIdxMask;
-      if (oi) oi[p] = (int32_t)i;
-      if (oj) oj[p] = (int32_t)j;
-      if (ofl) ofl[p] = ((jf[p] & kFlagRow) ? 1 : 0) | ((jf[p] & kFlagCol) ? 2 : 0);
-      if (op0) op0[p] = p0[p];
-      if (ov) ov[p] = aL[i] * p0[p] * bL[j];
+      ord.push_back({x->relabel ? pp[i] : i, x->relabel ? gp[j] : (int64_t)j, (int64_t)p});
     }
+  if (x->relabel) std::sort(ord.begin(), ord.end());
+  for (size_t k = 0; k < ord.size(); ++k) {
+    const unsigned p = (unsigned)ord[k][2];
+    const uint32_t j = jf[p] & kIdxMask;
+    int64_t i = 0;  // sorted row of entry p (for the plan value)
+    i = std::upper_bound(rp.begin(), rp.end(), p) - rp.begin() - 1;
+    if (oi) oi[k] = (int32_t)ord[k][0];
+    if (oj) oj[k] = (int32_t)ord[k][1];
+    if (ofl) ofl[k] = ((jf[p] & kFlagRow) ? 1 : 0) | ((jf[p] & kFlagCol) ? 2 : 0);
+    if (op0) op0[k] = p0[p];
+    if (ov) ov[k] = aL[i] * p0[p] * bL[j];
+  }
   return APML_OK;
 }
 
@@ -946,13 +980,24 @@ apml_status apml_ctx_lines(const apml_ctx* x, int64_t b, int32_t dir, float* om,
   CK(cudaMemcpyAsync(la.data(), (dir ? x->colA : x->rowA) + (size_t)b * n, sizeof(LineA) * n, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaMemcpyAsync(lb.data(), (dir ? x->colB : x->rowB) + (size_t)b * n, sizeof(LineB) * n, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaMemcpyAsync(idx.data(), (dir ? x->colidx : x->rowidx) + (size_t)b * n, sizeof(int2) * n, cudaMemcpyDeviceToHost, x->stream));
+  std::vector<int> pp, gp;  // relabelled: sorted position -> original index
+  if (x->relabel) {
+    pp.resize((size_t)x->Np);
+    gp.resize((size_t)x->Mp);
+    CK(cudaMemcpyAsync(pp.data(), x->pperm + (size_t)b * x->Np, sizeof(int) * x->Np, cudaMemcpyDeviceToHost, x->stream));
+    CK(cudaMemcpyAsync(gp.data(), x->gperm + (size_t)b * x->Mp, sizeof(int) * x->Mp, cudaMemcpyDeviceToHost, x->stream));
+  }
   CK(cudaStreamSynchronize(x->stream));
+  const std::vector<int>& own = dir ? gp : pp;
+  const std::vector<int>& oth = dir ? pp : gp;
   for (int64_t k = 0; k < n; ++k) {
-    if (om) om[k] = lb[k].m;
-    if (oc2) oc2[k] = std::sqrt(la[k].s2);
-    if (oT) oT[k] = lb[k].T;
-    if (oa) oa[k] = idx[k].x;
-    if (ob) ob[k] = idx[k].y;
+    const int64_t o = x->relabel ? own[k] : k;
+    auto map = [&](int v) { return (x->relabel && v >= 0) ? oth[v] : v; };
+    if (om) om[o] = lb[k].m;
+    if (oc2) oc2[o] = std::sqrt(la[k].s2);
+    if (oT) oT[o] = lb[k].T;
+    if (oa) oa[o] = map(idx[k].x);
+    if (ob) ob[o] = map(idx[k].y);
   }
   return APML_OK;
 }

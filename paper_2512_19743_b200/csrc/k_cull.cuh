@@ -97,9 +97,12 @@ __global__ void k_cell_count(const float* __restrict__ pts, int n, const float* 
 }
 
 // Place every point at its sorted position: SoA coordinates (pads = sentinel) + perm.
+// Relabelled mode (p4 != NULL): also the float4 copy and the inverse permutation (original
+// -> sorted) at sorted positions.
 __global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, float sentinel, int bits,
                                const uint32_t* __restrict__ key, const uint32_t* __restrict__ start,
-                               uint32_t* __restrict__ fill, float* __restrict__ soa, int* __restrict__ perm) {
+                               uint32_t* __restrict__ fill, float* __restrict__ soa, int* __restrict__ perm,
+                               float4* __restrict__ p4, int* __restrict__ iperm) {
   const int b = blockIdx.y;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= np) return;
@@ -115,6 +118,10 @@ __global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, flo
   const float* p = pts + ((size_t)b * n + k) * 3;
   s[pos] = p[0]; s[np + pos] = p[1]; s[2 * np + pos] = p[2];
   perm[(size_t)b * np + pos] = k;
+  if (p4) {
+    p4[(size_t)b * n + pos] = make_float4(p[0], p[1], p[2], 0.f);
+    if (iperm) iperm[(size_t)b * n + k] = (int)pos;
+  }
 }
 
 // Bounding boxes of every kTQ-point tile (cb[b][t]) and of its kSub-point sub-tiles
@@ -158,14 +165,14 @@ k_tile_bbox(const float* __restrict__ soa, int np, int n, float* __restrict__ cb
 // Column radii in SORTED order (gre[b][k] = (R2, E2) of the gt point at sorted position k,
 // (-1, -1) for pads) and the largest E2 of every tile (ce2) and sub-tile (fe2).
 __global__ void __launch_bounds__(kTQ)
-k_tile_re(const int* __restrict__ gperm, int mp, const LineA* __restrict__ colA, int M,
+k_tile_re(const int* __restrict__ gperm, int mp, const LineA* __restrict__ colA, int M, int relabel,
           float2* __restrict__ gre, float* __restrict__ ce2, float* __restrict__ fe2) {
   const int b = blockIdx.y, t = blockIdx.x;
   const int k = t * kTQ + threadIdx.x;
   const int j = gperm[(size_t)b * mp + k];
   float2 re = make_float2(-1.f, -1.f);
   if (j >= 0) {
-    const LineA a = colA[(size_t)b * M + j];
+    const LineA a = colA[(size_t)b * M + (relabel ? k : j)];
     re = make_float2(a.R2, a.E2);
   }
   gre[(size_t)b * mp + k] = re;
@@ -258,7 +265,7 @@ template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const int* __restrict__ own_perm,
                  const float* __restrict__ str_soa, int str_np, const float* __restrict__ str_cb,
-                 const float* __restrict__ str_fb, float2* __restrict__ out) {
+                 const float* __restrict__ str_fb, int relabel, float2* __restrict__ out) {
   constexpr int kW = kSweepThreads / 32;
   const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = own_soa + (size_t)b * 3 * own_np;
@@ -351,7 +358,8 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int idx = cull_idx<R>(blockIdx.x, r);
-    if (valid[r]) out[(size_t)b * own_n + own_perm[(size_t)b * own_np + idx]] = make_float2(m[r], s[r]);
+    if (valid[r])
+      out[(size_t)b * own_n + (relabel ? idx : own_perm[(size_t)b * own_np + idx])] = make_float2(m[r], s[r]);
   }
 }
 
@@ -362,7 +370,7 @@ template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __restrict__ pperm,
             const LineA* __restrict__ rowA, const float* __restrict__ gt_soa, int mp, int M,
-            const int* __restrict__ gperm, const float2* __restrict__ gre, const float* __restrict__ gcb,
+            const int* __restrict__ gperm, int relabel, const float2* __restrict__ gre, const float* __restrict__ gcb,
             const float* __restrict__ gfb, const float* __restrict__ gce2, const float* __restrict__ gfe2,
             uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
             unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt, unsigned* __restrict__ col_cnt) {
@@ -401,6 +409,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
     const float x = __ldg(own + idx), y = __ldg(own + np + idx), z = __ldg(own + 2 * np + idx);
     nx[r] = f2_pack(-x, -x); ny[r] = f2_pack(-y, -y); nz[r] = f2_pack(-z, -z);
     oi[r] = pperm[(size_t)b * np + idx];
+    if (relabel && oi[r] >= 0) oi[r] = idx;  // emit sorted positions
     rR2[r] = -1.f; rE2[r] = -1.f;
     if (oi[r] >= 0) {
       const LineA a = rowA[(size_t)b * N + oi[r]];
@@ -442,7 +451,12 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
         const float4 a0 = __ldg(src + 2 * lane), a1 = __ldg(src + 2 * lane + 1);
         reinterpret_cast<float4*>(sR)[lane] = make_float4(a0.x, a0.z, a1.x, a1.z);
         reinterpret_cast<float4*>(sE)[lane] = make_float4(a0.y, a0.w, a1.y, a1.w);
-        reinterpret_cast<int4*>(sJ)[lane] = __ldg(reinterpret_cast<const int4*>(jp + (size_t)t * kTQ) + lane);
+        int4 jj = __ldg(reinterpret_cast<const int4*>(jp + (size_t)t * kTQ) + lane);
+        if (relabel) {  // sorted positions of the real points
+          const int k0 = t * kTQ + 4 * lane;
+          jj = make_int4(jj.x >= 0 ? k0 : -1, jj.y >= 0 ? k0 + 1 : -1, jj.z >= 0 ? k0 + 2 : -1, jj.w >= 0 ? k0 + 3 : -1);
+        }
+        reinterpret_cast<int4*>(sJ)[lane] = jj;
       }
       __syncwarp();
       for (int q = 0; q < kSubPerTile; ++q) {

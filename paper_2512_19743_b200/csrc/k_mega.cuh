@@ -81,7 +81,22 @@ struct SparseArgs {
   int row_offset;
   float* colred;  // [B][M][3]
   int* cand;      // [B][M][3]
+  // Morton-relabelled index space (culled sweeps, one GPU per cloud): every line index in
+  // the sparse stage is a SORTED position; pperm / gperm [B][perm_np / perm_mp] give the
+  // original index (lines are still ordered, and ties broken, by ORIGINAL index, so the
+  // results equal the unrelabelled ones), ipperm [B][N] the inverse for pred.  NULL: identity.
+  const int* pperm;
+  const int* gperm;
+  const int* ipperm;
+  int perm_np, perm_mp;
 };
+
+__device__ __forceinline__ uint32_t orig_row(const SparseArgs& A, int b, uint32_t i) {
+  return A.pperm ? (uint32_t)A.pperm[(size_t)b * A.perm_np + i] : i;
+}
+__device__ __forceinline__ uint32_t orig_col(const SparseArgs& A, int b, uint32_t j) {
+  return A.gperm ? (uint32_t)A.gperm[(size_t)b * A.perm_mp + j] : j;
+}
 
 __device__ __forceinline__ void phase(const SparseArgs& A, int k) {
   if (A.dbg && threadIdx.x == 0) {
@@ -200,7 +215,9 @@ __device__ void sort_lines(const SparseArgs& A, int b, Slice s, const LongList& 
   APML_FOR_LINES(32, s, ll, line) {
     const uint32_t beg = ptr[line], end = ptr[line + 1], L = end - beg;
     if (L <= kRegLine) continue;
-    auto key_of = [&](uint32_t t) -> uint32_t { return kRows ? (e[t].y & kIdxMask) : e[t].x; };
+    auto key_of = [&](uint32_t t) -> uint32_t {  // ORIGINAL index of the other cloud
+      return kRows ? orig_col(A, b, e[t].y & kIdxMask) : orig_row(A, b, e[t].x);
+    };
     auto place = [&](uint32_t t, uint32_t rank) {
       const uint32_t pos = beg + rank;
       if (kRows) {
@@ -349,17 +366,19 @@ __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
     const uint32_t beg = rp[i], L = rp[i + 1] - beg;
     if (L > kRegLine) continue;
-    uint32_t t[kRegLine], jf[kRegLine], rk[kRegLine], sj[kRegLine];
+    uint32_t t[kRegLine], jf[kRegLine], rk[kRegLine], sj[kRegLine], ok[kRegLine];
 #pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
 #pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? A.ebuf[pb + t[k]].y : 0xffffffffu;
 #pragma unroll
+    for (uint32_t k = 0; k < kRegLine; ++k) ok[k] = k < L ? orig_col(A, b, jf[k] & kIdxMask) : 0xffffffffu;
+#pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k) {
       uint32_t r = 0;
 #pragma unroll
-      for (uint32_t f = 0; f < kRegLine; ++f) r += ((jf[f] & kIdxMask) < (jf[k] & kIdxMask)) ? 1u : 0u;
-      rk[k] = r;  // padded entries (key = mask) rank L and never precede a real key
+      for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
+      rk[k] = r;  // padded entries (key = ~0) rank L and never precede a real key
     }
 #pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k)
@@ -418,19 +437,20 @@ __device__ void col_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
     const uint32_t beg = cp[j], L = cp[j + 1] - beg;
     if (L > kRegLine) continue;
-    uint32_t t[kRegLine], key[kRegLine], pp[kRegLine], rk[kRegLine];
+    uint32_t t[kRegLine], key[kRegLine], pp[kRegLine], rk[kRegLine], ok[kRegLine];
 #pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csc_t[pb + beg + k] : 0u;
 #pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k) {
       key[k] = k < L ? A.ebuf[pb + t[k]].x : 0xffffffffu;
       pp[k] = k < L ? A.inv[pb + t[k]] : 0u;
+      ok[k] = k < L ? orig_row(A, b, key[k]) : 0xffffffffu;
     }
 #pragma unroll
     for (uint32_t k = 0; k < kRegLine; ++k) {
       uint32_t r = 0;
 #pragma unroll
-      for (uint32_t f = 0; f < kRegLine; ++f) r += (key[f] < key[k]) ? 1u : 0u;
+      for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
       rk[k] = r;
     }
     uint32_t si[kRegLine], sp[kRegLine];
@@ -1059,7 +1079,7 @@ __device__ void grad_rows(const SparseArgs& A, int b, Slice s, const LongList& l
     gy = gsum<G>(gy);
     gz = gsum<G>(gz);
     if (mem == 0) {
-      float* g = A.grad_pred + ((size_t)b * N + i) * 3;
+      float* g = A.grad_pred + ((size_t)b * N + orig_row(A, b, (uint32_t)i)) * 3;
       g[0] = (float)gx; g[1] = (float)gy; g[2] = (float)gz;
     }
   }

@@ -205,9 +205,9 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
     const size_t pb = (size_t)b * A.cap;
     for (uint32_t q = beg + 1; q < end; ++q) {
       const uint32_t t = A.csc_t[pb + q];
-      const uint32_t key = A.ebuf[pb + t].x;
+      const uint32_t key = orig_row(A, b, A.ebuf[pb + t].x);
       uint32_t r = q;
-      while (r > beg && A.ebuf[pb + A.csc_t[pb + r - 1]].x > key) {
+      while (r > beg && orig_row(A, b, A.ebuf[pb + A.csc_t[pb + r - 1]].x) > key) {
         A.csc_t[pb + r] = A.csc_t[pb + r - 1];
         --r;
       }
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
     for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
       const uint32_t p = A.csc_perm[pb + q];
       const float d2 = A.d2s[pb + p];
-      const int gi = A.row_offset + (int)A.csc_i[pb + q];
+      const int gi = A.row_offset + (int)orig_row(A, b, A.csc_i[pb + q]);  // global ORIGINAL row
       if (d2 == la.m2) { if (x1 < 0) x1 = gi; else if (x2 < 0) x2 = gi; }
       if (d2 == la.s2 && y1 < 0) y1 = gi;
       if (A.csr_jf[pb + p] & kFlagCol) Z += (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + p] - lb.m));
@@ -268,7 +268,11 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_b(const SparseArgs A, co
     ins(c[1]);
     if (c[2] >= 0 && (y < 0 || c[2] < y)) y = c[2];
   }
-  const int second = (la.s2 == la.m2) ? a2 : y;
+  int second = (la.s2 == la.m2) ? a2 : y;
+  if (A.ipperm) {  // relabelled (one rank, row_offset 0): back to sorted positions
+    a1 = a1 >= 0 ? A.ipperm[(size_t)b * A.N + a1] : -1;
+    second = second >= 0 ? A.ipperm[(size_t)b * A.N + second] : -1;
+  }
   A.colidx[(size_t)b * M + j] = make_int2(a1, second);
   const float iz = 1.f / A.colred[((size_t)b * M + j) * 3];
   for (uint32_t q = cp[j]; q < cp[j + 1]; ++q) {
