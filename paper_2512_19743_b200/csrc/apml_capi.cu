@@ -371,10 +371,16 @@ void print_phases(const char* name, const unsigned long long* d, int grid, int n
   std::vector<unsigned long long> h((size_t)grid * 16);
   cudaMemcpy(h.data(), d, h.size() * 8, cudaMemcpyDeviceToHost);
   std::string out = std::string("[apml phases] ") + name + " us:";
-  for (int k = 1; k < n; ++k) {
-    double s = 0;
-    for (int g = 0; g < grid; ++g) s += (double)(h[g * 16 + k] - h[g * 16 + k - 1]);
-    out += " " + std::to_string(s / grid / 1e3);
+  char buf[64];
+  for (int k = 1; k < n; ++k) {  // per phase: mean / max over CTAs
+    double s = 0, mx = 0;
+    for (int g = 0; g < grid; ++g) {
+      const double d = (double)(h[g * 16 + k] - h[g * 16 + k - 1]);
+      s += d;
+      mx = d > mx ? d : mx;
+    }
+    snprintf(buf, sizeof buf, " %.1f/%.1f", s / grid / 1e3, mx / 1e3);
+    out += buf;
   }
   fprintf(stderr, "%s\n", out.c_str());
 }
@@ -521,8 +527,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
 
 apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
   const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
-  apml_status st = c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream, "fwd", 9)
-                            : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream, "fwd", 9);
+  apml_status st = c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream, "fwd", 13)
+                            : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream, "fwd", 13);
   mark(c, 6, c->stream);
   c->launches += 1;
   return st;

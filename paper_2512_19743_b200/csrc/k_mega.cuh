@@ -357,8 +357,18 @@ __device__ void col_norm(const SparseArgs& A, int b, Slice s, const LongList& ll
   }
 }
 
-// Thread per row, row length <= kRegLine: rank-sort the row's entries by j in registers,
-// write the CSR row (+ entry -> CSR position), then the row softmax in sorted order.
+// Register paths (thread per line, length <= kRegLine), in two passes that each keep at
+// most ~3 arrays of kRegLine registers live (no spills under the 128-register cap):
+//   pass 1  the entries, in the order the scatter left them (csr_t / csc_t, arbitrary), are
+//           ranked in the line by ORIGINAL index of the other cloud and their index arrays
+//           written at beg + rank (CSR / CSC order);
+//   pass 2  the line is re-read in sorted order (same thread: its own stores are visible),
+//           every gather is issued before any store (stores could alias them as far as the
+//           compiler knows, which would serialise one L2 round trip per entry), then the
+//           softmax runs in sorted order (deterministic sums; argmin / second argmin = the
+//           first matches, R12).
+
+// Row softmax on the kept support (S5) + CSR order by j.
 __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   const int N = A.N, M = A.M;
   const size_t pb = (size_t)b * A.cap;
@@ -366,33 +376,31 @@ __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
     const uint32_t beg = rp[i], L = rp[i + 1] - beg;
     if (L > kRegLine) continue;
-    uint32_t t[kRegLine], jf[kRegLine], rk[kRegLine], sj[kRegLine], ok[kRegLine];
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? A.ebuf[pb + t[k]].y : 0xffffffffu;
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) ok[k] = k < L ? orig_col(A, b, jf[k] & kIdxMask) : 0xffffffffu;
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) {
-      uint32_t r = 0;
-#pragma unroll
-      for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
-      rk[k] = r;  // padded entries (key = ~0) rank L and never precede a real key
-    }
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k)
-      if (k < L) { A.csr_jf[pb + beg + rk[k]] = jf[k]; A.inv[pb + t[k]] = beg + rk[k]; }
-#pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) {
-      uint32_t v = 0u;
-#pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) v = rk[k] == r ? jf[k] : v;
-      sj[r] = v;
-    }
     const float4 x = A.pred4[(size_t)b * N + i];
     const LineA la = A.rowA[(size_t)b * N + i];
     const LineB lb = A.rowB[(size_t)b * N + i];
+    {
+      uint32_t t[kRegLine], jf[kRegLine], ok[kRegLine];
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? A.ebuf[pb + t[k]].y : 0u;
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) ok[k] = k < L ? orig_col(A, b, jf[k] & kIdxMask) : 0xffffffffu;
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) {
+        uint32_t r = 0;
+#pragma unroll
+        for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
+        if (k < L) {  // padded entries (key = ~0) never precede a real key
+          A.csr_jf[pb + beg + r] = jf[k];
+          A.inv[pb + t[k]] = beg + r;
+        }
+      }
+    }
+    uint32_t sj[kRegLine];
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) sj[r] = r < L ? A.csr_jf[pb + beg + r] : 0u;
     float d2v[kRegLine], cv[kRegLine];
 #pragma unroll
     for (uint32_t r = 0; r < kRegLine; ++r) {
@@ -428,8 +436,8 @@ __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   }
 }
 
-// Thread per column, length <= kRegLine: rank-sort by i in registers, write the CSC column
-// (+ CSR position of each entry), column softmax, P0 = (P_row + P_col)/2 in both orders.
+// Column softmax + symmetrisation P0 = (P_row + P_col)/2 in both orders + CSC
+// order by i (+ CSR position of each entry).
 __device__ void col_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   const int M = A.M;
   const size_t pb = (size_t)b * A.cap;
@@ -437,68 +445,72 @@ __device__ void col_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
     const uint32_t beg = cp[j], L = cp[j + 1] - beg;
     if (L > kRegLine) continue;
-    uint32_t t[kRegLine], key[kRegLine], pp[kRegLine], rk[kRegLine], ok[kRegLine];
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csc_t[pb + beg + k] : 0u;
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) {
-      key[k] = k < L ? A.ebuf[pb + t[k]].x : 0xffffffffu;
-      pp[k] = k < L ? A.inv[pb + t[k]] : 0u;
-      ok[k] = k < L ? orig_row(A, b, key[k]) : 0xffffffffu;
-    }
-#pragma unroll
-    for (uint32_t k = 0; k < kRegLine; ++k) {
-      uint32_t r = 0;
-#pragma unroll
-      for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
-      rk[k] = r;
-    }
-    uint32_t si[kRegLine], sp[kRegLine];
-#pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) {
-      uint32_t vi = 0u, vp = 0u;
-#pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) {
-        vi = rk[k] == r ? key[k] : vi;
-        vp = rk[k] == r ? pp[k] : vp;
-      }
-      si[r] = vi;
-      sp[r] = vp;
-    }
     const LineA la = A.colA[(size_t)b * M + j];
     const LineB lb = A.colB[(size_t)b * M + j];
-    float sv[kRegLine];
-    int ia = -1, ib = -1;
+    {
+      uint32_t t[kRegLine], key[kRegLine], pp[kRegLine];
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csc_t[pb + beg + k] : 0u;
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) {
+        key[k] = k < L ? A.ebuf[pb + t[k]].x : 0xffffffffu;
+        pp[k] = k < L ? A.inv[pb + t[k]] : 0u;
+      }
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? orig_row(A, b, key[k]) : 0xffffffffu;  // t <- ok
+#pragma unroll
+      for (uint32_t k = 0; k < kRegLine; ++k) {
+        uint32_t r = 0;
+#pragma unroll
+        for (uint32_t f = 0; f < kRegLine; ++f) r += (t[f] < t[k]) ? 1u : 0u;
+        if (k < L) {
+          A.csc_i[pb + beg + r] = key[k];
+          A.csc_perm[pb + beg + r] = pp[k];
+        }
+      }
+    }
+    uint32_t sp[kRegLine];
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) sp[r] = r < L ? A.csc_perm[pb + beg + r] : 0u;
+    float d2v[kRegLine], prv[kRegLine];
+    uint32_t colf = 0u;  // bit r: entry r kept by the column softmax
+#pragma unroll
+    for (uint32_t r = 0; r < kRegLine; ++r) {
+      if (r < L) {
+        d2v[r] = A.d2s[pb + sp[r]];
+        prv[r] = A.prow[pb + sp[r]];
+        colf |= (A.csr_jf[pb + sp[r]] & kFlagCol) ? (1u << r) : 0u;
+      }
+    }
+    int ra = -1, rb = -1;
     float Z = 0.f;
 #pragma unroll
     for (uint32_t r = 0; r < kRegLine; ++r) {
       if (r < L) {
-        const float d2 = A.d2s[pb + sp[r]];
-        const uint32_t fl = A.csr_jf[pb + sp[r]];
-        A.csc_i[pb + beg + r] = si[r];
-        A.csc_perm[pb + beg + r] = sp[r];
-        if (ia < 0 && d2 == la.m2) ia = (int)si[r];
-        else if (ib < 0 && d2 == la.s2) ib = (int)si[r];
+        const float d2 = d2v[r];
+        if (ra < 0 && d2 == la.m2) ra = (int)r;
+        else if (rb < 0 && d2 == la.s2) rb = (int)r;
         float e = 0.f;
-        if (fl & kFlagCol) {
-          e = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (A.cs[pb + sp[r]] - lb.m));
+        if (colf >> r & 1u) {
+          e = (lb.flags & kLineK1) ? 1.f : expf(-lb.T * (__fsqrt_rn(d2) - lb.m));
           Z += e;
         }
-        sv[r] = e;
+        d2v[r] = e;  // reuse: unnormalised similarity
       }
     }
     const float iz = 1.f / Z;
 #pragma unroll
     for (uint32_t r = 0; r < kRegLine; ++r) {
       if (r < L) {
-        const float pc = sv[r] * iz;
+        const float pc = d2v[r] * iz;
+        const float p0 = 0.5f * (prv[r] + pc);
         A.pcol[pb + sp[r]] = pc;
-        const float p0 = 0.5f * (A.prow[pb + sp[r]] + pc);
         A.P0[pb + sp[r]] = p0;
         A.P0c[pb + beg + r] = p0;
       }
     }
-    A.colidx[(size_t)b * M + j] = make_int2(ia, ib);
+    A.colidx[(size_t)b * M + j] = make_int2(ra >= 0 ? (int)A.csc_i[pb + beg + ra] : -1,
+                                            rb >= 0 ? (int)A.csc_i[pb + beg + rb] : -1);
   }
 }
 
@@ -521,21 +533,59 @@ __device__ __forceinline__ uint8_t* carve(uint8_t*& sm, size_t bytes) {
   return p;
 }
 
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Global -> shared copy of n floats by the whole CTA with cp.async (LDGSTS): every thread
+// keeps all of its copies in flight, no register round trip per element.  16-byte copies
+// when both ends are 16-byte aligned.  Completion: cp_async_wait_all() in every thread,
+// then a CTA (or cluster) barrier.
+__device__ __forceinline__ void g2s_async(float* dst, const float* src, size_t n) {
+  size_t k0 = 0;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const size_t n4 = n / 4;
+    for (size_t k = threadIdx.x; k < n4; k += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst + 4 * k)), "l"(src + 4 * k)
+                   : "memory");
+    k0 = n4 * 4;
+  }
+  for (size_t k = k0 + threadIdx.x; k < n; k += blockDim.x)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + k)), "l"(src + k) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Stage a line slice [s.lo, s.hi) of a CSR/CSC structure into shared memory (relative offsets).
+// Values by cp.async; offsets and indices (converted) with kU loads in flight per thread.
 template <typename IdxT>
 __device__ SliceView<IdxT> stage_slice(uint8_t*& sm, const unsigned* ptr, Slice s,
                                        const uint32_t* idx_g, const float* val_g, bool with_acc) {
+  constexpr int kU = 8;
   const int nl = s.hi - s.lo;
   const uint32_t base = ptr[s.lo], cnt = ptr[s.hi] - base;
   unsigned* off = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)(nl + 1)));
   IdxT* idx = reinterpret_cast<IdxT*>(carve(sm, sizeof(IdxT) * (size_t)cnt));
   float* val = reinterpret_cast<float*>(carve(sm, 4 * (size_t)cnt));
   float* acc = with_acc ? reinterpret_cast<float*>(carve(sm, 4 * (size_t)cnt)) : nullptr;
-  for (int k = threadIdx.x; k <= nl; k += blockDim.x) off[k] = ptr[s.lo + k] - base;
-  for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
-    idx[k] = (IdxT)(idx_g[base + k] & kIdxMask);
-    val[k] = val_g[base + k];
+  g2s_async(val, val_g + base, cnt);
+  const uint32_t bd = blockDim.x;
+  for (uint32_t k0 = threadIdx.x; k0 <= (uint32_t)nl; k0 += kU * bd) {
+    unsigned v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = k0 + u * bd <= (uint32_t)nl ? ptr[s.lo + k0 + u * bd] : 0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (k0 + u * bd <= (uint32_t)nl) off[k0 + u * bd] = v[u] - base;
   }
+  for (uint32_t k0 = threadIdx.x; k0 < cnt; k0 += kU * bd) {
+    uint32_t v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = k0 + u * bd < cnt ? idx_g[base + k0 + u * bd] : 0u;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (k0 + u * bd < cnt) idx[k0 + u * bd] = (IdxT)(v[u] & kIdxMask);
+  }
+  cp_async_wait_all();
   return SliceView<IdxT>{off, idx, val, acc};
 }
 
@@ -555,9 +605,6 @@ __device__ __forceinline__ size_t slice_bytes(int nl, uint32_t cnt, size_t idx_b
 // When the replicas live in global memory the exchange degrades to a store + cluster
 // barrier.
 
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ uint32_t map_rank(uint32_t addr, int rank) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
@@ -610,9 +657,31 @@ __device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x, int CL,
 
 // Segment dot product sum_{p in [p0, p1)} vec[col(p)] * val[p] with four independent
 // accumulators (4x shorter dependent chain on long lines; fixed order -> deterministic).
+// Segments of up to kDotShort entries are loaded with one predicated, fully unrolled batch
+// (every gather in flight at once: one dependent chain off -> idx -> vec instead of one per 4
+// entries); same accumulator assignment (entry u -> s[u % 4]) and final combination, so the
+// result is bit-identical to the loop.
+constexpr uint32_t kDotShort = 16;
 template <typename IdxT>
 __device__ __forceinline__ float seg_dot(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* vec) {
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (p1 - p0 <= kDotShort) {
+    const uint32_t L = p1 - p0;
+    float g[kDotShort], v[kDotShort];
+#pragma unroll
+    for (uint32_t u = 0; u < kDotShort; ++u) {
+      g[u] = u < L ? vec[V.col(p0 + u)] : 0.f;
+      v[u] = u < L ? V.val[p0 + u] : 0.f;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kDotShort; u += 4) {
+      if (u < L) s0 = __fmaf_rn(g[u], v[u], s0);
+      if (u + 1 < L) s1 = __fmaf_rn(g[u + 1], v[u + 1], s1);
+      if (u + 2 < L) s2 = __fmaf_rn(g[u + 2], v[u + 2], s2);
+      if (u + 3 < L) s3 = __fmaf_rn(g[u + 3], v[u + 3], s3);
+    }
+    return (s0 + s1) + (s2 + s3);
+  }
   uint32_t p = p0;
   for (; p + 4 <= p1; p += 4) {
     s0 = __fmaf_rn(vec[V.col(p)], V.val[p], s0);
@@ -627,32 +696,87 @@ __device__ __forceinline__ float seg_dot(const SliceView<IdxT>& V, uint32_t p0, 
 }
 
 // ---------------------------------------------------------------- forward Sinkhorn + loss
+//
+// A half-step costs one replica exchange (~0.6 us, scripts/micro/xchg_bench.cu) plus the
+// slowest line of any CTA of the cluster.  Lines of up to kRegLine entries are one thread's
+// (seg_dot: one batched gather); longer lines -- the CTA's long-line list -- are done by a
+// warp each (lane-strided gathers, butterfly sum), so one long line no longer gates the step.
+
+static_assert(kDotShort == kRegLine, "short-line threshold of the Sinkhorn loops = long-line list threshold");
 
 template <typename IdxT>
+__device__ __forceinline__ float warp_dot(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* vec) {
+  float s = 0.f;
+  for (uint32_t p = p0 + (threadIdx.x & 31); p < p1; p += 32) s = __fmaf_rn(vec[V.col(p)], V.val[p], s);
+  return gsum<32>(s);  // every lane holds the same bits
+}
+
+// kSm: slices and replicas are all in shared memory -- asserted to the compiler so that the
+// gathers through these (struct-held, generic) pointers compile to LDS rather than generic
+// LD, whose long-scoreboard latency dominated the half-steps.
+#define APML_ASSUME_SMEM(p) __builtin_assume(__isShared((const void*)(p)))
+template <typename IdxT>
+__device__ __forceinline__ void assume_smem(const SliceView<IdxT>& V) {
+  APML_ASSUME_SMEM(V.off);
+  APML_ASSUME_SMEM(V.idx);
+  APML_ASSUME_SMEM(V.val);
+}
+
+template <typename IdxT, bool kSm>
 __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
-                             const SliceView<IdxT>& R, const SliceView<IdxT>& C, Xchg& xa, Xchg& xb) {
+                             const SliceView<IdxT>& R, const SliceView<IdxT>& C, Xchg& xa, Xchg& xb,
+                             const LongList& llr, const LongList& llc) {
   const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks(), me = cl.block_rank();
   float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   float* bh = A.b_hist + (size_t)b * (L + 1) * M;
   const float* a = xa.rep;
   const float* bv = xb.rep;
+  if (kSm) {
+    assume_smem(R);
+    assume_smem(C);
+    APML_ASSUME_SMEM(a);
+    APML_ASSUME_SMEM(bv);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // Eq. (3): colsum_j = b_j Q_j, b_j <- b_j / (colsum_j + eps)
+  auto col_upd = [&](int j, float Q, int l) {
+    const float bj = bv[j];
+    const float nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
+    xchg_put(xb, CL, j, nb);
+    bh[(size_t)l * M + j] = nb;
+  };
+  // Eq. (4): rowsum_i = a_i R_i, a_i <- a_i / (rowsum_i + eps)
+  auto row_upd = [&](int i, float Rs, int l) {
+    const float ai = a[i];
+    const float na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+    xchg_put(xa, CL, i, na);
+    ah[(size_t)l * N + i] = na;
+  };
   for (int l = 1; l <= L; ++l) {
-    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {  // Eq. (3): colsum = b_j Q_j
+    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
       const int k = j - sc.lo;
-      const float Q = seg_dot(C, C.off[k], C.off[k + 1], a);
-      const float bj = bv[j];
-      const float nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
-      xchg_put(xb, CL, j, nb);
-      bh[(size_t)l * M + j] = nb;
+      const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
+      if (p1 - p0 <= kRegLine) col_upd(j, seg_dot(C, p0, p1, a), l);
+    }
+    for (int q = w; q < llc.count(); q += nw) {
+      const int j = llc.line(q), k = j - sc.lo;
+      const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
+      if (p1 - p0 <= kRegLine) continue;  // (overflowed list: whole slice)
+      const float Q = warp_dot(C, p0, p1, a);
+      if (lane == 0) col_upd(j, Q, l);
     }
     xchg_end(cl, xb, CL, me);
-    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {  // Eq. (4): rowsum = a_i R_i
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
-      const float Rs = seg_dot(R, R.off[k], R.off[k + 1], bv);
-      const float ai = a[i];
-      const float na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
-      xchg_put(xa, CL, i, na);
-      ah[(size_t)l * N + i] = na;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 <= kRegLine) row_upd(i, seg_dot(R, p0, p1, bv), l);
+    }
+    for (int q = w; q < llr.count(); q += nw) {
+      const int i = llr.line(q), k = i - sr.lo;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 <= kRegLine) continue;
+      const float Rs = warp_dot(R, p0, p1, bv);
+      if (lane == 0) row_upd(i, Rs, l);
     }
     xchg_end(cl, xa, CL, me);
   }
@@ -689,11 +813,36 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   cluster_scan(cl, cc, cp, M, sc, s_tot_c, s_warp);
   cl.sync();
   phase(A, 1);
-  for (uint32_t t = rank * blockDim.x + threadIdx.x; t < total; t += CL * blockDim.x) {
-    const uint2 e = A.ebuf[pb + t];
-    const uint32_t i = e.x, j = e.y & kIdxMask;
-    A.csr_t[pb + rp[i] + atomicAdd(rc + i, 1u)] = t;
-    A.csc_t[pb + cp[j] + atomicAdd(cc + j, 1u)] = t;
+  {
+    // kSc entries per thread per step: loads, then all atomics, then the stores, so a step
+    // costs ~3 L2 round trips instead of 3 per entry
+    constexpr int kSc = 4;
+    const uint32_t stride = CL * blockDim.x;
+    for (uint32_t t0 = rank * blockDim.x + threadIdx.x; t0 < total; t0 += kSc * stride) {
+      uint32_t ii[kSc], jj[kSc], pr[kSc], pc[kSc];
+#pragma unroll
+      for (int u = 0; u < kSc; ++u) {
+        const uint32_t t = t0 + u * stride;
+        const uint2 e = t < total ? A.ebuf[pb + t] : make_uint2(0u, 0u);
+        ii[u] = e.x;
+        jj[u] = e.y & kIdxMask;
+      }
+#pragma unroll
+      for (int u = 0; u < kSc; ++u) {
+        if (t0 + u * stride < total) {
+          pr[u] = rp[ii[u]] + atomicAdd(rc + ii[u], 1u);
+          pc[u] = cp[jj[u]] + atomicAdd(cc + jj[u], 1u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kSc; ++u) {
+        const uint32_t t = t0 + u * stride;
+        if (t < total) {
+          A.csr_t[pb + pr[u]] = t;
+          A.csc_t[pb + pc[u]] = t;
+        }
+      }
+    }
   }
   cl.sync();
   phase(A, 2);
@@ -701,22 +850,26 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   // softmax (S5) on the kept support
   const LongList llr = collect_long(rp, sr, s_long_r, &s_nlong[0]);
   const LongList llc = collect_long(cp, sc, s_long_c, &s_nlong[1]);
+  phase(A, 3);
   row_sort_norm_regs(A, b, sr);
   __syncthreads();
+  phase(A, 4);
   sort_lines<true>(A, b, sr, llr);
   __syncthreads();
+  phase(A, 5);
   row_norm(A, b, sr, llr);
   cl.sync();
-  phase(A, 3);
+  phase(A, 6);
   // columns: sort by i, column softmax, symmetrisation P0 = (P_row + P_col)/2
   col_sort_norm_regs(A, b, sc);
   __syncthreads();
+  phase(A, 7);
   sort_lines<false>(A, b, sc, llc);
   __syncthreads();
+  phase(A, 8);
   col_norm(A, b, sc, llc);
   cl.sync();
-  phase(A, 4);
-  phase(A, 5);
+  phase(A, 9);
   // S6: Sinkhorn.  Replicas of a and b (full length) + own CSR / CSC slices in shared memory.
   uint8_t* sm = shm;
   float *a, *bv;
@@ -752,16 +905,17 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     const SliceView<IdxT> R = stage_slice<IdxT>(sm, rp, sr, A.csr_jf + pb, A.P0 + pb, false);
     const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
     cl.sync();
-    phase(A, 6);
-    sinkhorn_fwd<IdxT>(cl, A, b, sr, sc, R, C, xa, xb);
+    phase(A, 10);
+    if (A.rep_smem) sinkhorn_fwd<IdxT, true>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
+    else sinkhorn_fwd<IdxT, false>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
   } else {
     const SliceView<uint32_t> R{rp + sr.lo, A.csr_jf + pb, A.P0 + pb, nullptr};
     const SliceView<uint32_t> C{cp + sc.lo, A.csc_i + pb, A.P0c + pb, nullptr};
     cl.sync();
-    phase(A, 6);
-    sinkhorn_fwd<uint32_t>(cl, A, b, sr, sc, R, C, xa, xb);
+    phase(A, 10);
+    sinkhorn_fwd<uint32_t, false>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
   }
-  phase(A, 7);
+  phase(A, 11);
   // S7: loss_b = sum_i a_i sum_j P0_ij b_j c_ij over own rows, then cluster reduction in rank order
   double acc = 0.0;
   for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
@@ -786,18 +940,71 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     for (int r = 0; r < CL; ++r) t += s_part[r];
     A.loss[b] = (float)t;
   }
-  phase(A, 8);
+  phase(A, 12);
 }
 
 // ---------------------------------------------------------------- backward
 
 constexpr int kPf = 8;  // b^l prefetch registers per thread (bls staging needs M <= kPf * blockDim)
 
+// acc[p] += s * vec[col(p)] over a short segment (<= kRegLine entries): one batched gather.
 template <typename IdxT>
+__device__ __forceinline__ void seg_axpy(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, float s, const float* vec) {
+  const uint32_t n = p1 - p0;
+  float g[kRegLine], c[kRegLine];
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u) {
+    g[u] = u < n ? vec[V.col(p0 + u)] : 0.f;
+    c[u] = u < n ? V.acc[p0 + u] : 0.f;
+  }
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u)
+    if (u < n) V.acc[p0 + u] = c[u] + s * g[u];
+}
+// Returns sum_p vec[col(p)] val[p] (accumulators as seg_dot) and does acc[p] += vec[col(p)] * s,
+// over a short segment.
+template <typename IdxT>
+__device__ __forceinline__ float seg_dot_axpy(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* vec,
+                                              float s) {
+  const uint32_t n = p1 - p0;
+  float g[kRegLine], v[kRegLine], c[kRegLine];
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u) {
+    g[u] = u < n ? vec[V.col(p0 + u)] : 0.f;
+    v[u] = u < n ? V.val[p0 + u] : 0.f;
+    c[u] = u < n ? V.acc[p0 + u] : 0.f;
+  }
+  float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u)
+    if (u < n) t[u & 3] = __fmaf_rn(g[u], v[u], t[u & 3]);
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u)
+    if (u < n) V.acc[p0 + u] = c[u] + g[u] * s;
+  return (t[0] + t[1]) + (t[2] + t[3]);
+}
+
+// Reverse Sinkhorn in scaling form; P0bar accumulated per CSR entry of the own
+// rows in shared memory (R.acc).  Short lines by a thread, long lines by a warp (as forward).
+template <typename IdxT, bool kSm>
 __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* ab, float* bb,
-                             Xchg& xr, Xchg& xq, float* bls, const float* ahs, const float* bhs) {
+                             Xchg& xr, Xchg& xq, float* bls, const float* ahs, const float* bhs,
+                             const LongList& llr, const LongList& llc) {
+  // kSm: slices (+ acc), replicas, abar / bbar and the staged history all in shared memory
+  if (kSm) {
+    assume_smem(R);
+    assume_smem(C);
+    APML_ASSUME_SMEM(R.acc);
+    APML_ASSUME_SMEM(xr.rep);
+    APML_ASSUME_SMEM(xq.rep);
+    APML_ASSUME_SMEM(ab);
+    APML_ASSUME_SMEM(bb);
+    APML_ASSUME_SMEM(ahs);
+    APML_ASSUME_SMEM(bhs);
+  }
   const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks(), me = cl.block_rank();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // ahs: own rows' a history [L+1][nr] and bhs: full b history [L+1][M], staged in shared
   // memory when they fit (else read from global memory, b^l optionally staged via bls).
   const int nr = sr.hi - sr.lo;
@@ -825,37 +1032,78 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;  // b^l
     // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
     // P0bar_ij += Rbar^l_i b^l_j
-    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
-      const int k = i - sr.lo;
+    auto row_rev = [&](int i, int k, float abk, bool writer) -> float {
       const float al = ah[(size_t)l * ald + i], alm = ah[(size_t)(l - 1) * ald + i];
       const float r = al / alm;
-      const float Rb = -ab[k] * al * al;
-      ab[k] = ab[k] * A.eps * r * r;
-      xchg_put(xr, CL, i, Rb);
-      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += Rb * bcur[R.col(p)];
+      const float Rb = -abk * al * al;
+      if (writer) {
+        ab[k] = abk * A.eps * r * r;
+        xchg_put(xr, CL, i, Rb);
+      }
+      return Rb;
+    };
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+      const int k = i - sr.lo;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 > kRegLine) continue;
+      seg_axpy(R, p0, p1, row_rev(i, k, ab[k], true), bcur);
+    }
+    for (int q = w; q < llr.count(); q += nw) {
+      const int i = llr.line(q), k = i - sr.lo;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 <= kRegLine) continue;
+      const float abk = ab[k];
+      __syncwarp();
+      const float Rb = row_rev(i, k, abk, lane == 0);
+      for (uint32_t p = p0 + lane; p < p1; p += 32) R.acc[p] += Rb * bcur[R.col(p)];
+      __syncwarp();
     }
     xchg_end(cl, xr, CL, me);
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
-    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
-      const int k = j - sc.lo;
-      const float t = seg_dot(C, C.off[k], C.off[k + 1], rcur);
+    auto col_rev = [&](int j, int k, float t) {
       const float bsum = bb[k] + t;
       const float bl = bh[(size_t)l * M + j], blm = bh[(size_t)(l - 1) * M + j];
       const float r = bl / blm;
       bb[k] = bsum * A.eps * r * r;
       xchg_put(xq, CL, j, -bsum * bl * bl);
+    };
+    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
+      const int k = j - sc.lo;
+      const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
+      if (p1 - p0 <= kRegLine) col_rev(j, k, seg_dot(C, p0, p1, rcur));
+    }
+    for (int q = w; q < llc.count(); q += nw) {
+      const int j = llc.line(q), k = j - sc.lo;
+      const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
+      if (p1 - p0 <= kRegLine) continue;
+      const float t = warp_dot(C, p0, p1, rcur);
+      if (lane == 0) col_rev(j, k, t);
     }
     xchg_end(cl, xq, CL, me);
-    // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i
+    // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (one pass)
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
-      const float alm = ah[(size_t)(l - 1) * ald + i];
-      const float t = seg_dot(R, R.off[k], R.off[k + 1], qcur);
-      for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p) R.acc[p] += qcur[R.col(p)] * alm;
-      ab[k] += t;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 > kRegLine) continue;
+      ab[k] += seg_dot_axpy(R, p0, p1, qcur, ah[(size_t)(l - 1) * ald + i]);
     }
-    // the next row step touches only this thread's rows; only the staged b^{l-1} needs a
-    // CTA barrier
+    for (int q = w; q < llr.count(); q += nw) {
+      const int i = llr.line(q), k = i - sr.lo;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 <= kRegLine) continue;
+      const float alm = ah[(size_t)(l - 1) * ald + i];
+      float t = 0.f;
+      for (uint32_t p = p0 + lane; p < p1; p += 32) {
+        const float qv = qcur[R.col(p)];
+        t = __fmaf_rn(qv, R.val[p], t);
+        R.acc[p] += qv * alm;
+      }
+      t = gsum<32>(t);
+      if (lane == 0) ab[k] += t;
+      __syncwarp();
+    }
+    // the next row step touches only the rows this thread (warp) owns; only the staged
+    // b^{l-1} needs a CTA barrier
     if (bls && l > 1) {
 #pragma unroll
       for (int u = 0; u < kPf; ++u) {
@@ -1196,7 +1444,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     // abar / bbar of the own slices: shared memory when they fit, else the second half of
     // the pair's global scratch (the first half holds the replicas in global mode)
     float *ab, *bb;
-    if ((size_t)(sm - shm) + 4 * (size_t)(sr.hi - sr.lo + sc.hi - sc.lo) + 64 <= A.smem_bytes) {
+    const bool ab_sm = (size_t)(sm - shm) + 4 * (size_t)(sr.hi - sr.lo + sc.hi - sc.lo) + 64 <= A.smem_bytes;
+    if (ab_sm) {
       ab = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sr.hi - sr.lo)));
       bb = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(sc.hi - sc.lo)));
     } else {
@@ -1223,10 +1472,21 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
       const SliceView<IdxT> R = stage_slice<IdxT>(sm, rp, sr, A.csr_jf + pb, A.P0 + pb, true);
       const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
       __syncthreads();  // offsets staged by other threads
+      const float* csl = A.cs + pb + rp[sr.lo];
       for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
         const int k = i - sr.lo;
-        for (uint32_t p = R.off[k]; p < R.off[k + 1]; ++p)
-          R.acc[p] = gl * aL[i] * bL[R.col(p)] * A.cs[pb + rp[sr.lo] + p];
+        const float ga = gl * aL[i];
+        for (uint32_t p0 = R.off[k], p1 = R.off[k + 1]; p0 < p1; p0 += 8) {
+          float bv[8], cv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            bv[u] = p0 + u < p1 ? bL[R.col(p0 + u)] : 0.f;
+            cv[u] = p0 + u < p1 ? csl[p0 + u] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p0 + u < p1) R.acc[p0 + u] = ga * bv[u] * cv[u];
+        }
       }
       // stage the Sinkhorn history (own rows of a, all of b) when it fits
       float *ahs = nullptr, *bhs = nullptr;
@@ -1236,13 +1496,15 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
         bhs = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(L + 1) * M));
         const float* ahg = A.a_hist + (size_t)b * (L + 1) * N;
         const float* bhg = A.b_hist + (size_t)b * (L + 1) * M;
-        for (int k = threadIdx.x; k < (L + 1) * nr; k += blockDim.x)
-          ahs[k] = ahg[(size_t)(k / nr) * N + sr.lo + k % nr];
-        for (int k = threadIdx.x; k < (L + 1) * M; k += blockDim.x) bhs[k] = bhg[k];
+        for (int l = 0; l <= L; ++l) g2s_async(ahs + (size_t)l * nr, ahg + (size_t)l * N + sr.lo, nr);
+        g2s_async(bhs, bhg, (size_t)(L + 1) * M);
+        cp_async_wait_all();
       }
       cl.sync();
       phase(A, 1);
-      sinkhorn_bwd<IdxT>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, ahs, bhs);
+      const bool all_sm = A.rep_smem && ahs && bhs && ab_sm;
+      if (all_sm) sinkhorn_bwd<IdxT, true>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, ahs, bhs, llr, llc);
+      else sinkhorn_bwd<IdxT, false>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, ahs, bhs, llr, llc);
       const uint32_t base = rp[sr.lo], cnt = rp[sr.hi] - base;
       for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) A.pbar[pb + base + k] = R.acc[k];
     } else {
@@ -1253,7 +1515,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
           A.pbar[pb + p] = gl * aL[i] * bL[A.csr_jf[pb + p] & kIdxMask] * A.cs[pb + p];
       cl.sync();
       phase(A, 1);
-      sinkhorn_bwd<uint32_t>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, nullptr, nullptr);
+      sinkhorn_bwd<uint32_t, false>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, nullptr, nullptr, llr, llc);
     }
     __syncthreads();
     phase(A, 2);
