@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define APML_ABI_VERSION 1
+#define APML_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define APML_API __attribute__((visibility("default")))
@@ -124,6 +124,10 @@ typedef struct {
     int64_t overflow_pairs; /* pairs whose support exceeded capacity (their loss is NaN) */
     int64_t bytes_ctx;      /* device bytes owned by the context */
     int64_t launches;       /* kernels launched so far by this context (forward + backward) */
+    int64_t sweep_evals[3]; /* (i, j) distance evaluations executed by the sweeps of the last
+                               forward: [0] Pass A rows, [1] Pass A columns, [2] emit.  Full
+                               sweeps: every padded pair (B Np Mp); spatially culled sweeps:
+                               counted on the device (32 x 32 blocks actually evaluated) */
 } apml_stats;
 
 /* Caller-supplied, stream-ordered collectives for the row-sharded mode (torch.distributed /

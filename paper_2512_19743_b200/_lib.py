@@ -54,7 +54,7 @@ class ApmlComm(C.Structure):
 class ApmlStats(C.Structure):
     _fields_ = [("nnz_total", C.c_int64), ("emitted_total", C.c_int64), ("clamp_count", C.c_int64),
                 ("capacity", C.c_int64), ("overflow_pairs", C.c_int64), ("bytes_ctx", C.c_int64),
-                ("launches", C.c_int64)]
+                ("launches", C.c_int64), ("sweep_evals", C.c_int64 * 3)]
 
 
 class ApmlError(RuntimeError):
@@ -103,7 +103,7 @@ def lib() -> C.CDLL:
                                           C.POINTER(ApmlAllocator), vp, vp, vp]
         L.apml_last_error.restype = C.c_char_p
         L.apml_last_error.argtypes = []
-        if L.apml_abi_version() != 1:
+        if L.apml_abi_version() != 2:
             raise ImportError("libapml.so ABI version mismatch")
         _lib = L
     return _lib

@@ -77,7 +77,8 @@ class Context:
         A.check(A.lib().apml_ctx_stats(self._h, C.cast(nnz, C.c_void_p), C.byref(st)))
         return dict(nnz=list(nnz), nnz_total=st.nnz_total, emitted_total=st.emitted_total,
                     clamp_count=st.clamp_count, capacity=st.capacity,
-                    overflow_pairs=st.overflow_pairs, bytes_ctx=st.bytes_ctx, launches=st.launches)
+                    overflow_pairs=st.overflow_pairs, bytes_ctx=st.bytes_ctx, launches=st.launches,
+                    sweep_evals=list(st.sweep_evals))
 
     def stage_times(self) -> dict:
         """Per-stage device milliseconds (needs Config(stage_timing=True)); synchronises."""

@@ -17,6 +17,7 @@
 #include "../../include/apml.h"
 #include "common.cuh"
 #include "k_cull.cuh"
+#include "k_fwd2.cuh"
 #include "k_dist.cuh"
 #include "k_mega.cuh"
 #include "k_rowshard.cuh"
@@ -81,6 +82,7 @@ struct apml_ctx {
   bool idx16 = false;     // 16-bit indices in shared memory
   int rep_smem = 0;       // scaling-vector replicas in shared memory
   size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
+  bool fwd2 = false;      // sparse forward built in shared memory (k_fwd2.cuh)
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // spatially culled sweeps (k_cull.cuh)
   bool cull = false;
@@ -109,7 +111,7 @@ struct apml_ctx {
   float *predS, *gtS; float4 *pred4, *gt4;
   float2 *part_r, *part_c;
   LineA *rowA, *colA; LineB *rowB, *colB;
-  unsigned long long* clamp;
+  unsigned long long* clamp;  // [0] clamped lines, [1..3] evaluations of the culled sweeps
   uint2* ebuf; unsigned *cursor, *aux;
   unsigned *row_cnt, *col_cnt, *row_ptr, *col_ptr;
   uint32_t *csr_t, *csc_t, *inv, *csr_jf, *csc_i, *csc_perm;
@@ -237,6 +239,13 @@ void plan_sparse(apml_ctx* c) {
   // slice falls back to global memory.  Otherwise leave ~30% headroom over the estimate.
   if (B * c->cl <= num_sms()) c->smem_bytes = mx;
   else c->smem_bytes = std::min(mx, need(c->cl, c->rep_smem != 0) * 13 / 10);
+  // k_sparse_fwd2 (default; APML_FWD2=0: k_sparse_fwd): its 4 replicated line vectors and
+  // offsets must fit; per-entry arrays fall back to global memory per CTA at run time.  512
+  // threads x 128 registers fill an SM's register file, so the whole shared memory is free.
+  const size_t vec4 = 8 * (size_t)((N + 3) / 4 * 4 + 4) + 8 * (size_t)((M + 3) / 4 * 4 + 4);
+  const int64_t nr = (N + c->cl - 1) / c->cl, nc = (M + c->cl - 1) / c->cl;
+  c->fwd2 = c->rep_smem && env_long("APML_FWD2", 1) != 0 && vec4 + 8 * (size_t)(nr + nc) + 256 <= mx;
+  if (c->fwd2) c->smem_bytes = mx;
 }
 
 apml_status build_ctx(apml_ctx* c, uint32_t cap) {
@@ -269,7 +278,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   // counters in one contiguous zeroed block
   size_t z0 = k.off;
   size_t o_phist = k.take<uint32_t>(B * cells1), o_ghist = k.take<uint32_t>(B * cells1);
-  size_t o_clamp = k.take<unsigned long long>(1);
+  size_t o_clamp = k.take<unsigned long long>(4);  // clamp count + culled-sweep evaluations [3]
   size_t o_cursor = k.take<unsigned>(B), o_aux = k.take<unsigned>(B);
   size_t o_row_cnt = k.take<unsigned>(B * (N + 1)), o_col_cnt = k.take<unsigned>(B * (M + 1));
   size_t z1 = k.off;
@@ -458,10 +467,10 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
   mark(c, 1, s);
   k_line_top2_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
-      c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r);
+      c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r, c->clamp + 1);
   mark(c, 2, s);
   k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
-      c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c);
+      c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c, c->clamp + 2);
   c->launches += 11;  // + the scan's own
   CK(cudaGetLastError());
   return APML_OK;
@@ -474,7 +483,7 @@ apml_status launch_emit_cull(apml_ctx* c) {
                                                c->gfe2);
   k_emit_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
       c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor, c->aux,
-      c->row_cnt, c->col_cnt);
+      c->row_cnt, c->col_cnt, c->clamp + 3);
   c->launches += 2;
   CK(cudaGetLastError());
   return APML_OK;
@@ -527,8 +536,9 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
 
 apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
   const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
-  apml_status st = c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream, "fwd", 13)
-                            : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream, "fwd", 13);
+  apml_status st = c->fwd2    ? launch_cluster(c, k_sparse_fwd2, a, c->stream, "fwd2", 9)
+                   : c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream, "fwd", 13)
+                              : launch_cluster(c, k_sparse_fwd<uint32_t>, a, c->stream, "fwd", 13);
   mark(c, 6, c->stream);
   c->launches += 1;
   return st;
@@ -899,10 +909,10 @@ apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats*
   if (!x) return fail(APML_ERR_STATE, "NULL context");
   const int64_t B = x->B;
   std::vector<unsigned> cur((size_t)B), aux((size_t)B);
-  unsigned long long clamp = 0;
+  unsigned long long cnt[4] = {0, 0, 0, 0};
   CK(cudaMemcpyAsync(cur.data(), x->cursor, sizeof(unsigned) * B, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaMemcpyAsync(aux.data(), x->aux, sizeof(unsigned) * B, cudaMemcpyDeviceToHost, x->stream));
-  CK(cudaMemcpyAsync(&clamp, x->clamp, sizeof(clamp), cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaMemcpyAsync(cnt, x->clamp, sizeof(cnt), cudaMemcpyDeviceToHost, x->stream));
   CK(cudaStreamSynchronize(x->stream));
   apml_stats st{};
   for (int64_t b = 0; b < B; ++b) {
@@ -912,7 +922,9 @@ apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats*
     st.emitted_total += cur[b];
     if (cur[b] > x->cap) st.overflow_pairs++;
   }
-  st.clamp_count = (int64_t)clamp;
+  st.clamp_count = (int64_t)cnt[0];
+  for (int k = 0; k < 3; ++k)  // culled: counted on the device; otherwise every padded (i, j)
+    st.sweep_evals[k] = x->cull ? (int64_t)cnt[1 + k] : B * x->Np * x->Mp;
   st.capacity = x->cap;
   st.bytes_ctx = (int64_t)x->bytes;
   st.launches = x->launches;

@@ -265,7 +265,8 @@ template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const int* __restrict__ own_perm,
                  const float* __restrict__ str_soa, int str_np, const float* __restrict__ str_cb,
-                 const float* __restrict__ str_fb, int relabel, float2* __restrict__ out) {
+                 const float* __restrict__ str_fb, int relabel, float2* __restrict__ out,
+                 unsigned long long* __restrict__ evals) {
   constexpr int kW = kSweepThreads / 32;
   const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = own_soa + (size_t)b * 3 * own_np;
@@ -303,6 +304,7 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
 #pragma unroll
   for (int r = 0; r < R; ++r) wmax = fmaxf(wmax, gmax[r]);
 
+  unsigned nev = 0;
   const int own_base = blockIdx.x * kSweepThreads * R + w * 32 * R;
   const int t0 = min(nt - 1, (int)((long long)own_base * nt / own_np));
   for (int base = 0; base < 2 * nt; base += 32) {
@@ -320,6 +322,7 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
       }
       const unsigned fm = __ballot_sync(0xffffffffu, need);
       if (!fm) continue;
+      nev += (unsigned)__popc(fm);  // (group, sub-tile) blocks of 32 x kSub evaluations
       stage_tile_xyz(str, str_np, t, tx, ty, tz);
       __syncwarp();
       for (int q = 0; q < kSubPerTile; ++q) {
@@ -355,6 +358,7 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
       __syncwarp();
     }
   }
+  if (evals && lane == 0 && nev) atomicAdd(evals, (unsigned long long)nev * 32ull * kSub);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int idx = cull_idx<R>(blockIdx.x, r);
@@ -373,7 +377,8 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
             const int* __restrict__ gperm, int relabel, const float2* __restrict__ gre, const float* __restrict__ gcb,
             const float* __restrict__ gfb, const float* __restrict__ gce2, const float* __restrict__ gfe2,
             uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
-            unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt, unsigned* __restrict__ col_cnt) {
+            unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt, unsigned* __restrict__ col_cnt,
+            unsigned long long* __restrict__ evals) {
   constexpr int kW = kSweepThreads / 32;
   const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = pred_soa + (size_t)b * 3 * np;
@@ -426,6 +431,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
   }
   __syncwarp();
   const unsigned lt_mask = (1u << lane) - 1u;
+  unsigned nev = 0;
   for (int base = 0; base < nt; base += 32) {
     const int T = base + lane;
     bool cand = false;
@@ -445,6 +451,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
       }
       const unsigned fm = __ballot_sync(0xffffffffu, need);
       if (!fm) continue;
+      nev += (unsigned)__popc(fm);
       stage_tile_xyz(str, mp, t, tx, ty, tz);
       {
         const float4* src = reinterpret_cast<const float4*>(re + (size_t)t * kTQ);
@@ -505,6 +512,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
   }
   __syncwarp();
   if (wcnt) warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+  if (evals && lane == 0 && nev) atomicAdd(evals, (unsigned long long)nev * 32ull * kSub);
 }
 
 }  // namespace apml
