@@ -392,6 +392,21 @@ void print_phases(const char* name, const unsigned long long* d, int grid, int n
     out += buf;
   }
   fprintf(stderr, "%s\n", out.c_str());
+  if (getenv("APML_PHASES_CTA")) {  // the slowest CTAs of the slowest phase
+    int kk = 1;
+    double best = -1;
+    for (int k = 1; k < n; ++k)
+      for (int g = 0; g < grid; ++g) {
+        const double d = (double)(h[g * 16 + k] - h[g * 16 + k - 1]);
+        if (d > best) { best = d; kk = k; }
+      }
+    std::vector<std::pair<double, int>> v;
+    for (int g = 0; g < grid; ++g) v.push_back({(double)(h[g * 16 + kk] - h[g * 16 + kk - 1]), g});
+    std::sort(v.rbegin(), v.rend());
+    fprintf(stderr, "[apml phases] %s slowest phase %d:", name, kk);
+    for (int q = 0; q < 8 && q < (int)v.size(); ++q) fprintf(stderr, " cta %d %.1f us;", v[q].second, v[q].first / 1e3);
+    fprintf(stderr, "\n");
+  }
 }
 
 // One cluster of c->cl CTAs per pair.

@@ -111,7 +111,7 @@ struct Side {
 // In-place sort of the entries [beg, beg + L) of a line by ORIGINAL index of the other cloud
 // (keys are distinct on a line).  kRows: key = orig_col(j), also records the CSR position of
 // each entry in A.inv (by emit index).  G == 1: L <= kRegLine, registers; G == 32: warp, L <= 32
-// by a shuffle rank count, longer by lane 0 (insertion sort; rare).
+// by a shuffle rank count, up to 256 with 8 entries per lane in registers, longer by bitonic sort.
 template <bool kRows>
 __device__ __forceinline__ uint32_t sort_key(const SparseArgs& A, int b, uint32_t idx) {
   return kRows ? orig_col(A, b, idx & kIdxMask) : orig_row(A, b, idx & kIdxMask);
@@ -158,21 +158,67 @@ __device__ void sort_line_warp(const SparseArgs& A, int b, const Side& S, uint32
     __syncwarp();
     return;
   }
-  if (lane == 0) {
-    for (uint32_t k = 1; k < L; ++k) {
-      const uint32_t ix = S.idx[beg + k], tt = S.t[beg + k], key = sort_key<kRows>(A, b, ix);
-      uint32_t q = k;
-      while (q > 0 && sort_key<kRows>(A, b, S.idx[beg + q - 1]) > key) {
-        S.idx[beg + q] = S.idx[beg + q - 1];
-        S.t[beg + q] = S.t[beg + q - 1];
-        --q;
-      }
-      S.idx[beg + q] = ix;
-      S.t[beg + q] = tt;
+  constexpr uint32_t kSlots = 8;  // entries per lane held in registers: L <= 256
+  if (L <= 32 * kSlots) {
+    uint32_t ix[kSlots], tt[kSlots], rk[kSlots], key[kSlots];
+#pragma unroll
+    for (uint32_t u = 0; u < kSlots; ++u) {
+      const uint32_t p = lane + 32 * u;
+      ix[u] = p < L ? S.idx[beg + p] : 0u;
+      tt[u] = p < L ? S.t[beg + p] : 0u;
+      key[u] = p < L ? sort_key<kRows>(A, b, ix[u]) : 0xffffffffu;
+      rk[u] = 0u;
     }
-    if (kRows)
-      for (uint32_t k = 0; k < L; ++k) A.inv[(size_t)b * A.cap + S.t[beg + k]] = gbase + beg + k;
+    // rank = number of smaller keys on the line; the keys are broadcast 32 at a time
+#pragma unroll
+    for (uint32_t v = 0; v < kSlots; ++v) {
+      if (32 * v >= L) break;
+      for (uint32_t q = 0; q < 32 && 32 * v + q < L; ++q) {
+        const uint32_t kq = __shfl_sync(0xffffffffu, key[v], q);
+#pragma unroll
+        for (uint32_t u = 0; u < kSlots; ++u) rk[u] += (kq < key[u]) ? 1u : 0u;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (uint32_t u = 0; u < kSlots; ++u) {
+      if (lane + 32 * u < L) {
+        S.idx[beg + rk[u]] = ix[u];
+        S.t[beg + rk[u]] = tt[u];
+        if (kRows) A.inv[(size_t)b * A.cap + tt[u]] = gbase + beg + rk[u];
+      }
+    }
+    __syncwarp();
+    return;
   }
+  // > 256 entries (outlier points whose line is nearly flat; seen at C3): in-place bitonic
+  // sort over the next power of two with ascending comparators only, so the virtual +inf
+  // elements beyond L never move (O(L log^2 L), deterministic)
+  uint32_t n2 = 1;
+  while (n2 < L) n2 <<= 1;
+  for (uint32_t k = 2; k <= n2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t q = lane; q < n2 / 2; q += 32) {
+        // q-th pair of this step: i has bit j clear; partner = i ^ (k - 1) (flip) or i ^ j
+        const uint32_t i = ((q & ~(j - 1)) << 1) | (q & (j - 1));
+        const uint32_t pi = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
+        const uint32_t lo = min(i, pi), hi = max(i, pi);
+        if (hi < L) {
+          const uint32_t a = S.idx[beg + lo], c = S.idx[beg + hi];
+          if (sort_key<kRows>(A, b, a) > sort_key<kRows>(A, b, c)) {
+            const uint32_t ta = S.t[beg + lo];
+            S.idx[beg + lo] = c;
+            S.idx[beg + hi] = a;
+            S.t[beg + lo] = S.t[beg + hi];
+            S.t[beg + hi] = ta;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (kRows)
+    for (uint32_t k = lane; k < L; k += 32) A.inv[(size_t)b * A.cap + S.t[beg + k]] = gbase + beg + k;
   __syncwarp();
 }
 
