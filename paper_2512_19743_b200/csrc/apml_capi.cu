@@ -18,6 +18,7 @@
 #include "common.cuh"
 #include "k_cull.cuh"
 #include "k_fwd2.cuh"
+#include "k_bwd2.cuh"
 #include "k_dist.cuh"
 #include "k_mega.cuh"
 #include "k_rowshard.cuh"
@@ -115,6 +116,8 @@ struct apml_ctx {
   uint2* ebuf; unsigned *cursor, *aux;
   unsigned *row_cnt, *col_cnt, *row_ptr, *col_ptr;
   uint32_t *csr_t, *csc_t, *inv, *csr_jf, *csc_i, *csc_perm;
+  uint32_t* csc_if = nullptr;  // CSC-order copies (k_sparse_fwd2 -> k_sparse_bwd2)
+  float *csc_c = nullptr, *csc_pc = nullptr;
   float *d2s, *cs, *prow, *pcol, *P0, *P0c, *pbar;
   int2 *rowidx, *colidx;
   float *a_hist, *b_hist, *gvec;
@@ -288,6 +291,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_csr_jf = k.take<uint32_t>(E), o_csc_i = k.take<uint32_t>(E), o_csc_perm = k.take<uint32_t>(E);
   size_t o_d2 = k.take<float>(E), o_cs = k.take<float>(E), o_prow = k.take<float>(E), o_pcol = k.take<float>(E);
   size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
+  const int64_t E2 = c->fwd2 ? E : 0;  // CSC-order copies written by k_sparse_fwd2
+  size_t o_csc_if = k.take<uint32_t>(E2), o_csc_c = k.take<float>(E2), o_csc_pc = k.take<float>(E2);
   size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
   size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
   size_t o_gv = k.take<float>(B * 2 * (N + M));
@@ -328,6 +333,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->csr_jf = (uint32_t*)(p + o_csr_jf); c->csc_i = (uint32_t*)(p + o_csc_i); c->csc_perm = (uint32_t*)(p + o_csc_perm);
   c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
   c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
+  c->csc_if = (uint32_t*)(p + o_csc_if); c->csc_c = (float*)(p + o_csc_c); c->csc_pc = (float*)(p + o_csc_pc);
   c->rowidx = (int2*)(p + o_rowidx); c->colidx = (int2*)(p + o_colidx);
   c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh); c->gvec = (float*)(p + o_gv);
   c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
@@ -355,6 +361,7 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.ebuf = c->ebuf; a.cursor = c->cursor; a.row_cnt = c->row_cnt; a.col_cnt = c->col_cnt;
   a.row_ptr = c->row_ptr; a.col_ptr = c->col_ptr; a.csr_t = c->csr_t; a.csc_t = c->csc_t; a.inv = c->inv;
   a.csr_jf = c->csr_jf; a.csc_i = c->csc_i; a.csc_perm = c->csc_perm;
+  a.csc_if = c->csc_if; a.csc_c = c->csc_c; a.csc_pc = c->csc_pc;
   a.d2s = c->d2s; a.cs = c->cs; a.prow = c->prow; a.pcol = c->pcol; a.P0 = c->P0; a.P0c = c->P0c; a.pbar = c->pbar;
   a.rowidx = c->rowidx; a.colidx = c->colidx; a.a_hist = c->a_hist; a.b_hist = c->b_hist; a.gvec = c->gvec;
   a.rowback = c->rowback; a.colback = c->colback;
@@ -910,8 +917,11 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
     return APML_OK;
   }
   const SparseArgs a = sparse_args(x, nullptr, grad_loss, grad_pred);
-  apml_status st = x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s, "bwd", 6)
-                            : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s, "bwd", 6);
+  // full gradient after k_sparse_fwd2: k_sparse_bwd2 (its CSC-order arrays); else k_sparse_bwd
+  apml_status st = (x->fwd2 && a.full && env_long("APML_BWD2", 1) != 0)
+                       ? launch_cluster(x, k_sparse_bwd2, a, s, "bwd2", 7)
+                   : x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s, "bwd", 6)
+                              : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s, "bwd", 6);
   if (st != APML_OK) return st;
   mark(x, 8, s);
   x->launches += 1;

@@ -98,7 +98,8 @@ __device__ LongList collect_long_local(const unsigned* off, Slice s, uint32_t* l
 
 // One side (CSR rows or CSC columns) of a CTA's slice.  idx: other-cloud index | flags;
 // t: emit-buffer index (only until the CSC side has read the CSR positions), reused as c;
-// val: P0; pr: unnormalised similarity of this side's softmax, then this side's P.
+// val: P0; pr: unnormalised similarity of this side's softmax, then this side's P (CSR:
+// P_row, CSC: P_col).
 struct Side {
   unsigned* off;  // [n + 1] local offsets
   uint32_t* idx;
@@ -333,10 +334,8 @@ __device__ void line_p0(const SparseArgs& A, int b, const Side& S, int line, int
       const float poth = (ix[u] & fo) ? __fmul_rn(line_sim(c[u], lo[u]), iz_oth[o]) : 0.f;
       const float prow = kRows ? pown : poth, pcol = kRows ? poth : pown;
       S.val[p0 + u] = sym_p0(prow, pcol);
-      if (kRows) {
-        S.pr[p0 + u] = prow;
-        A.pcol[pb + gbase + p0 + u] = pcol;
-      }
+      S.pr[p0 + u] = pown;  // this side's probability (CSR: P_row, CSC: P_col)
+      if (kRows) A.pcol[pb + gbase + p0 + u] = pcol;
     }
   }
 }
@@ -604,11 +603,19 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
     }
     for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) {
       A.csc_i[pb + gc + q] = C.idx[q] & kIdxMask;
+      A.csc_if[pb + gc + q] = C.idx[q];
       A.P0c[pb + gc + q] = C.val[q];
+      A.csc_c[pb + gc + q] = C.c[q];
+      A.csc_pc[pb + gc + q] = C.pr[q];
     }
   } else {
     for (uint32_t p = threadIdx.x; p < nnzr; p += blockDim.x) A.cs[pb + gr + p] = R.c[p];
-    for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) C.idx[q] &= kIdxMask;  // = csc_i
+    for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) {
+      A.csc_if[pb + gc + q] = C.idx[q];
+      A.csc_c[pb + gc + q] = C.c[q];
+      A.csc_pc[pb + gc + q] = C.pr[q];
+      C.idx[q] &= kIdxMask;  // = csc_i
+    }
   }
   cl.sync();
   if (rank == 0 && threadIdx.x == 0) {

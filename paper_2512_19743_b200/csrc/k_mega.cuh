@@ -56,6 +56,9 @@ struct SparseArgs {
   uint32_t* csr_jf;
   uint32_t* csc_i;
   uint32_t* csc_perm;
+  uint32_t* csc_if;  // CSC order (k_sparse_fwd2): i | flags, c, P_col
+  float* csc_c;
+  float* csc_pc;
   float* d2s;
   float* cs;
   float* prow;
@@ -1000,8 +1003,9 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     APML_ASSUME_SMEM(xq.rep);
     APML_ASSUME_SMEM(ab);
     APML_ASSUME_SMEM(bb);
-    APML_ASSUME_SMEM(ahs);
-    APML_ASSUME_SMEM(bhs);
+    if (ahs) APML_ASSUME_SMEM(ahs);
+    if (bhs) APML_ASSUME_SMEM(bhs);
+    if (bls) APML_ASSUME_SMEM(bls);
   }
   const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks(), me = cl.block_rank();
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -1030,6 +1034,15 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       }
     }
     const float* bcur = bls ? bls + (l & 1) * M : bh + (size_t)l * M;  // b^l
+    // b^{l-1} of this thread's first kOwnPf columns, loaded now so that the column step does
+    // not wait on it when the history is not in shared memory
+    constexpr int kOwnPf = 2;
+    float blm_pf[kOwnPf];
+#pragma unroll
+    for (int u = 0; u < kOwnPf; ++u) {
+      const int j = sc.lo + threadIdx.x + u * blockDim.x;
+      blm_pf[u] = j < sc.hi ? bh[(size_t)(l - 1) * M + j] : 1.f;
+    }
     // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
     // P0bar_ij += Rbar^l_i b^l_j
     auto row_rev = [&](int i, int k, float abk, bool writer) -> float {
@@ -1060,24 +1073,31 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     }
     xchg_end(cl, xr, CL, me);
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
-    auto col_rev = [&](int j, int k, float t) {
+    auto col_rev = [&](int j, int k, float t, float blm) {
       const float bsum = bb[k] + t;
-      const float bl = bh[(size_t)l * M + j], blm = bh[(size_t)(l - 1) * M + j];
+      const float bl = bcur[j];
       const float r = bl / blm;
       bb[k] = bsum * A.eps * r * r;
       xchg_put(xq, CL, j, -bsum * bl * bl);
     };
-    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
-      const int k = j - sc.lo;
-      const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
-      if (p1 - p0 <= kRegLine) col_rev(j, k, seg_dot(C, p0, p1, rcur));
+    {
+      int u = 0;
+      for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x, ++u) {
+        const int k = j - sc.lo;
+        const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
+        float blm = 0.f;
+#pragma unroll
+        for (int v = 0; v < kOwnPf; ++v) blm = u == v ? blm_pf[v] : blm;
+        if (u >= kOwnPf) blm = bh[(size_t)(l - 1) * M + j];
+        if (p1 - p0 <= kRegLine) col_rev(j, k, seg_dot(C, p0, p1, rcur), blm);
+      }
     }
     for (int q = w; q < llc.count(); q += nw) {
       const int j = llc.line(q), k = j - sc.lo;
       const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
       if (p1 - p0 <= kRegLine) continue;
       const float t = warp_dot(C, p0, p1, rcur);
-      if (lane == 0) col_rev(j, k, t);
+      if (lane == 0) col_rev(j, k, t, bh[(size_t)(l - 1) * M + j]);
     }
     xchg_end(cl, xq, CL, me);
     // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (one pass)
