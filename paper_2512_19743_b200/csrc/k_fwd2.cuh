@@ -340,12 +340,14 @@ __device__ void line_p0(const SparseArgs& A, int b, const Side& S, int line, int
   }
 }
 
-template <bool kSm>
-__device__ void fwd2_sinkhorn(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc, const Side& R,
-                              const Side& C, Xchg& xa, Xchg& xb, const LongList& llr, const LongList& llc) {
-  const SliceView<uint32_t> RV{R.off, R.idx, R.val, nullptr};
-  const SliceView<uint32_t> CV{C.off, C.idx, C.val, nullptr};
-  sinkhorn_fwd<uint32_t, kSm>(cl, A, b, sr, sc, RV, CV, xa, xb, llr, llc);
+template <typename IdxT, bool kSm>
+__device__ void fwd2_sinkhorn(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
+                              const unsigned* roff, const IdxT* ridx, const float* rval, const unsigned* coff,
+                              const IdxT* cidx, const float* cval, Xchg& xa, Xchg& xb, const LongList& llr,
+                              const LongList& llc) {
+  const SliceView<IdxT> RV{roff, ridx, rval, nullptr};
+  const SliceView<IdxT> CV{coff, cidx, cval, nullptr};
+  sinkhorn_fwd<IdxT, kSm>(cl, A, b, sr, sc, RV, CV, xa, xb, llr, llc);
 }
 
 __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArgs A) {
@@ -567,11 +569,27 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
   for (int k = sr.lo + threadIdx.x; k < sr.hi; k += blockDim.x) ah[k] = 1.f;
   for (int k = sc.lo + threadIdx.x; k < sc.hi; k += blockDim.x) bh[k] = 1.f;
   __syncthreads();
+  // this side's probabilities are final: write them now and reuse their shared memory for
+  // 16-bit copies of the indices (half the shared-memory bytes per gather in Sinkhorn)
+  const bool idx16 = fit && N <= 65536 && M <= 65536;
+  if (fit) {
+    for (uint32_t p = threadIdx.x; p < nnzr; p += blockDim.x) A.prow[pb + gr + p] = R.pr[p];
+    for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) A.csc_pc[pb + gc + q] = C.pr[q];
+    __syncthreads();
+  }
+  uint16_t* r16 = reinterpret_cast<uint16_t*>(R.pr);
+  uint16_t* c16 = reinterpret_cast<uint16_t*>(C.pr);
+  if (idx16) {
+    for (uint32_t p = threadIdx.x; p < nnzr; p += blockDim.x) r16[p] = (uint16_t)(R.idx[p] & kIdxMask);
+    for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) c16[q] = (uint16_t)(C.idx[q] & kIdxMask);
+    __syncthreads();
+  }
   phase(A, 6);
 
   // ---- S6: Sinkhorn, L_iter x {Eq. (3), Eq. (4)}
-  if (fit) fwd2_sinkhorn<true>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
-  else fwd2_sinkhorn<false>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
+  if (idx16) fwd2_sinkhorn<uint16_t, true>(cl, A, b, sr, sc, roff, r16, R.val, coff, c16, C.val, xa, xb, llr, llc);
+  else if (fit) fwd2_sinkhorn<uint32_t, true>(cl, A, b, sr, sc, roff, R.idx, R.val, coff, C.idx, C.val, xa, xb, llr, llc);
+  else fwd2_sinkhorn<uint32_t, false>(cl, A, b, sr, sc, roff, R.idx, R.val, coff, C.idx, C.val, xa, xb, llr, llc);
   phase(A, 7);
 
   // ---- S7: loss_b = sum_i a_i sum_j P0_ij b_j c_ij, own rows, then cluster sum
@@ -599,14 +617,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
       A.csr_jf[pb + gr + p] = R.idx[p];
       A.P0[pb + gr + p] = R.val[p];
       A.cs[pb + gr + p] = R.c[p];
-      A.prow[pb + gr + p] = R.pr[p];
     }
     for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) {
       A.csc_i[pb + gc + q] = C.idx[q] & kIdxMask;
       A.csc_if[pb + gc + q] = C.idx[q];
       A.P0c[pb + gc + q] = C.val[q];
       A.csc_c[pb + gc + q] = C.c[q];
-      A.csc_pc[pb + gc + q] = C.pr[q];
     }
   } else {
     for (uint32_t p = threadIdx.x; p < nnzr; p += blockDim.x) A.cs[pb + gr + p] = R.c[p];
