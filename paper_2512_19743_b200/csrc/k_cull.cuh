@@ -307,56 +307,88 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
   unsigned nev = 0;
   const int own_base = blockIdx.x * kSweepThreads * R + w * 32 * R;
   const int t0 = min(nt - 1, (int)((long long)own_base * nt / own_np));
-  for (int base = 0; base < 2 * nt; base += 32) {
-    const int T = ring_tile(t0, base + lane, nt);
-    const bool cand = T >= 0 && box_dist2(wbox, cb + (size_t)T * 6) * kCullMargin <= wmax;
-    unsigned cm = __ballot_sync(0xffffffffu, cand);
-    while (cm) {
-      const int l = __ffs(cm) - 1;
-      cm &= cm - 1;
-      const int t = __shfl_sync(0xffffffffu, T, l);
-      bool need = false;
-      if (lane < kSubPerTile * R) {
-        const int r = lane / kSubPerTile, q = lane % kSubPerTile;
-        need = box_dist2(s_gbox[w][r], fb + ((size_t)t * kSubPerTile + q) * 6) * kCullMargin <= s_gmax[w][r];
-      }
-      const unsigned fm = __ballot_sync(0xffffffffu, need);
-      if (!fm) continue;
-      nev += (unsigned)__popc(fm);  // (group, sub-tile) blocks of 32 x kSub evaluations
-      stage_tile_xyz(str, str_np, t, tx, ty, tz);
-      __syncwarp();
-      for (int q = 0; q < kSubPerTile; ++q) {
-        const ulonglong2* px = reinterpret_cast<const ulonglong2*>(tx + q * kSub);
-        const ulonglong2* py = reinterpret_cast<const ulonglong2*>(ty + q * kSub);
-        const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(tz + q * kSub);
+  // Candidate tiles come from a generator (32 ring steps per ballot against the warp bound);
+  // the data of the NEXT candidate (its sub-tile box for this lane's (group, sub-tile) test
+  // and its coordinates) is loaded into registers before the current one is evaluated, so
+  // the two dependent global round trips per tile overlap the arithmetic (the walk was
+  // latency-bound: ncu 13 % occupancy, 45 % issue).  A candidate chosen with an older,
+  // larger bound is only a weaker filter: the result is unchanged.
+  int gbase = 0, gT = -1;
+  unsigned gcm = 0u;
+  auto next_cand = [&]() -> int {
+    while (!gcm) {
+      if (gbase >= 2 * nt) return -1;
+      gT = ring_tile(t0, gbase + lane, nt);
+      const bool cand = gT >= 0 && box_dist2(wbox, cb + (size_t)gT * 6) * kCullMargin <= wmax;
+      gcm = __ballot_sync(0xffffffffu, cand);
+      gbase += 32;
+    }
+    const int l = __ffs(gcm) - 1;
+    gcm &= gcm - 1;
+    return __shfl_sync(0xffffffffu, gT, l);
+  };
+  const int sl_r = lane / kSubPerTile, sl_q = lane % kSubPerTile;  // this lane's (group, sub-tile)
+  const bool sl_on = lane < kSubPerTile * R;
+  float4 nxv, nyv, nzv;
+  float nbox[6];
+  auto prefetch = [&](int t) {
+    const size_t o = (size_t)t * kTQ;
+    nxv = __ldg(reinterpret_cast<const float4*>(str + o) + lane);
+    nyv = __ldg(reinterpret_cast<const float4*>(str + str_np + o) + lane);
+    nzv = __ldg(reinterpret_cast<const float4*>(str + 2 * (size_t)str_np + o) + lane);
+    const float* fbp = fb + ((size_t)t * kSubPerTile + sl_q) * 6;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!((fm >> (r * kSubPerTile + q)) & 1u)) continue;  // warp-uniform
+    for (int d = 0; d < 6; ++d) nbox[d] = sl_on ? __ldg(fbp + d) : 0.f;
+  };
+  int tn = next_cand();
+  if (tn >= 0) prefetch(tn);
+  while (tn >= 0) {
+    const float4 cx = nxv, cy = nyv, cz = nzv;
+    float cbx[6];
 #pragma unroll
-          for (int k = 0; k < kSub / 4; ++k) {
-            const ulonglong2 qx = px[k], qy = py[k], qz = pz[k];
-            const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
-            const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
-            float d0, d1, d2, d3;
-            f2_unpack(d01, d0, d1);
-            f2_unpack(d23, d2, d3);
-            top2_pair(m[r], s[r], d0, d1);
-            top2_pair(m[r], s[r], d2, d3);
-          }
-        }
-      }
-      wmax = -1.f;
+    for (int d = 0; d < 6; ++d) cbx[d] = nbox[d];
+    tn = next_cand();
+    if (tn >= 0) prefetch(tn);
+    bool need = false;
+    if (sl_on) need = box_dist2(s_gbox[w][sl_r], cbx) * kCullMargin <= s_gmax[w][sl_r];
+    const unsigned fm = __ballot_sync(0xffffffffu, need);
+    if (!fm) continue;
+    nev += (unsigned)__popc(fm);  // (group, sub-tile) blocks of 32 x kSub evaluations
+    reinterpret_cast<float4*>(tx)[lane] = cx;
+    reinterpret_cast<float4*>(ty)[lane] = cy;
+    reinterpret_cast<float4*>(tz)[lane] = cz;
+    __syncwarp();
+    for (int q = 0; q < kSubPerTile; ++q) {
+      const ulonglong2* px = reinterpret_cast<const ulonglong2*>(tx + q * kSub);
+      const ulonglong2* py = reinterpret_cast<const ulonglong2*>(ty + q * kSub);
+      const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(tz + q * kSub);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if ((fm >> (r * kSubPerTile)) & ((1u << kSubPerTile) - 1u)) gmax[r] = warp_max(valid[r] ? s[r] : -1.f);
-        wmax = fmaxf(wmax, gmax[r]);
-      }
-      __syncwarp();  // every lane is done with the staged tile and the old bounds
+        if (!((fm >> (r * kSubPerTile + q)) & 1u)) continue;  // warp-uniform
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (lane == r) s_gmax[w][r] = gmax[r];
-      __syncwarp();
+        for (int k = 0; k < kSub / 4; ++k) {
+          const ulonglong2 qx = px[k], qy = py[k], qz = pz[k];
+          const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
+          const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
+          float d0, d1, d2, d3;
+          f2_unpack(d01, d0, d1);
+          f2_unpack(d23, d2, d3);
+          top2_pair(m[r], s[r], d0, d1);
+          top2_pair(m[r], s[r], d2, d3);
+        }
+      }
     }
+    wmax = -1.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if ((fm >> (r * kSubPerTile)) & ((1u << kSubPerTile) - 1u)) gmax[r] = warp_max(valid[r] ? s[r] : -1.f);
+      wmax = fmaxf(wmax, gmax[r]);
+    }
+    __syncwarp();  // every lane is done with the staged tile and the old bounds
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (lane == r) s_gmax[w][r] = gmax[r];
+    __syncwarp();
   }
   if (evals && lane == 0 && nev) atomicAdd(evals, (unsigned long long)nev * 32ull * kSub);
 #pragma unroll

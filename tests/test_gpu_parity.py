@@ -264,6 +264,9 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_GRID": "1"},                                          # grid-wide kernels (few, large pairs)
     {"APML_CULL": "1"},                                          # spatially culled sweeps (NEXT-2)
     {"APML_CULL": "1", "APML_GRID": "1"},
+    {"APML_FWD2": "0"},                                          # global-memory sparse forward (k_sparse_fwd)
+    {"APML_BWD2": "0"},                                          # k_sparse_fwd2 + k_sparse_bwd
+    {"APML_SMEM_LIMIT": "60000", "APML_CL": "1"},                # fwd2 / bwd2 slices in global memory
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_sparse_stage_fallback_paths(env, monkeypatch):
     """The plan the library picks depends on N, M, B and shared memory; force every variant at a
