@@ -183,6 +183,18 @@ APML_API apml_status apml_forward_rowsharded(const float* pred_local, const floa
  * d loss_b / d pred_b.  grad_loss device [B].  One backward per context (ERR_STATE after). */
 APML_API apml_status apml_backward(apml_ctx* ctx, const float* grad_loss, float* grad_pred, void* stream);
 
+/* apml_backward plus, when grad_gt != NULL, the gradient with respect to gt (SURVEY 8(f)-3,
+ * for settings where gt is itself predicted).  The loss depends on gt only through the costs
+ * c_ij, so by Eq. (5) with x and y exchanged:
+ *     grad_gt[b][j] = - sum_i w_ij (x_i - y_j),  w_ij = cbar_ij / (c_ij + eps_dist),
+ * the same per-entry adjoints cbar as grad_pred (full or plan-detached mode).
+ * grad_gt: device [B][M][3] fp32, caller-owned, overwritten (NaN rows for overflowed pairs).
+ * Row-sharded contexts: every rank passes a full [B][M][3] buffer and receives the sum over
+ * ranks (one allreduce_sum_f32 of 3 B M floats through the context's apml_comm).
+ * Errors as apml_backward. */
+APML_API apml_status apml_backward_ex(apml_ctx* ctx, const float* grad_loss, float* grad_pred, float* grad_gt,
+                                      void* stream);
+
 /* Diagnostics; SYNCHRONISES the context's stream.  nnz_per_pair: host [B] or NULL. */
 APML_API apml_status apml_ctx_stats(const apml_ctx* ctx, int64_t* nnz_per_pair, apml_stats* out);
 

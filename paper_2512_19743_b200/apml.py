@@ -110,12 +110,19 @@ class Context:
         A.check(A.lib().apml_ctx_lines(self._h, b, direction, ptr(m), ptr(c2), ptr(T), ptr(a), ptr(s)))
         return dict(m=m, c2=c2, T=T, a=a, b=s)
 
-    def backward(self, grad_loss: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def backward(self, grad_loss: torch.Tensor, out: torch.Tensor | None = None,
+                 want_gt: bool = False, gt_out: torch.Tensor | None = None):
+        """d loss / d pred [B,N,3]; with want_gt (or gt_out) also d loss / d gt [B,M,3]
+        (apml_backward_ex) and returns (grad_pred, grad_gt)."""
         gl = grad_loss.to(device=self.device, dtype=torch.float32).contiguous().reshape(self.B)
         g = out if out is not None else torch.empty(self.B, self.N, 3, device=self.device)
         s = torch.cuda.current_stream(self.device).cuda_stream
-        A.check(A.lib().apml_backward(self._h, gl.data_ptr(), g.data_ptr(), s))
-        return g
+        if not (want_gt or gt_out is not None):
+            A.check(A.lib().apml_backward(self._h, gl.data_ptr(), g.data_ptr(), s))
+            return g
+        gg = gt_out if gt_out is not None else torch.empty(self.B, self.M, 3, device=self.device)
+        A.check(A.lib().apml_backward_ex(self._h, gl.data_ptr(), g.data_ptr(), gg.data_ptr(), s))
+        return g, gg
 
     def close(self):
         if self._h:
@@ -160,9 +167,12 @@ class _APMLFunction(torch.autograd.Function):
     @staticmethod
     def backward(fctx, grad_loss):
         ctx = fctx.apml
-        g = ctx.backward(grad_loss)
+        if fctx.needs_input_grad[1]:  # gt is itself predicted: apml_backward_ex
+            g, gg = ctx.backward(grad_loss, want_gt=True)
+        else:
+            g, gg = ctx.backward(grad_loss), None
         ctx.close()
-        return g, None, None
+        return g, gg, None
 
 
 def apml_loss(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,

@@ -84,6 +84,7 @@ struct apml_ctx {
   int rep_smem = 0;       // scaling-vector replicas in shared memory
   size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
   bool fwd2 = false;      // sparse forward built in shared memory (k_fwd2.cuh)
+  float* grad_gt = nullptr;  // set by apml_backward_ex for the duration of the call
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // spatially culled sweeps (k_cull.cuh)
   bool cull = false;
@@ -358,6 +359,8 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.N = (int)c->N; a.M = (int)c->M; a.L = c->cfg.l_iter; a.full = c->cfg.grad_mode == APML_GRAD_FULL;
   a.cap = c->cap; a.eps = c->cfg.eps_stab; a.eps_dist = c->cfg.eps_dist;
   a.pred4 = c->pred4; a.gt4 = c->gt4; a.rowA = c->rowA; a.rowB = c->rowB; a.colA = c->colA; a.colB = c->colB;
+  a.grad_gt = c->grad_gt;
+  a.gw = c->grad_gt ? c->d2s : nullptr;  // d2s is forward-only scratch: free in the backward
   a.ebuf = c->ebuf; a.cursor = c->cursor; a.row_cnt = c->row_cnt; a.col_cnt = c->col_cnt;
   a.row_ptr = c->row_ptr; a.col_ptr = c->col_ptr; a.csr_t = c->csr_t; a.csc_t = c->csc_t; a.inv = c->inv;
   a.csr_jf = c->csr_jf; a.csc_i = c->csc_i; a.csc_perm = c->csc_perm;
@@ -896,7 +899,13 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
 }
 
 apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred, void* stream) {
+  return apml_backward_ex(x, grad_loss, grad_pred, nullptr, stream);
+}
+
+apml_status apml_backward_ex(apml_ctx* x, const float* grad_loss, float* grad_pred, float* grad_gt, void* stream) {
   if (!x) return fail(APML_ERR_STATE, "NULL context");
+  x->grad_gt = grad_gt;
+  struct Reset { apml_ctx* c; ~Reset() { c->grad_gt = nullptr; } } reset{x};
   if (x->backward_done) return fail(APML_ERR_STATE, "backward already ran on this context");
   if (!grad_loss || !grad_pred) return fail(APML_ERR_INVALID_ARG, "grad_loss / grad_pred must be non-NULL");
   cudaStream_t s = stream ? (cudaStream_t)stream : x->stream;
@@ -912,6 +921,13 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
   if (x->rs) {
     apml_status st = launch_backward_rs(x, grad_loss, grad_pred, s);
     if (st != APML_OK) return st;
+    if (grad_gt) {  // this rank's rows' contributions, summed over ranks (X3-style all-reduce)
+      k_grad_gt<<<dim3((unsigned)((x->M + 255) / 256), (unsigned)x->B), 256, 0, s>>>(
+          sparse_args(x, nullptr, grad_loss, grad_pred));
+      x->launches += 1;
+      CK(cudaGetLastError());
+      if (x->comm.world > 1 && (st = coll_sum(x, grad_gt, 3 * x->B * x->M)) != APML_OK) return st;
+    }
     mark(x, 8, s);
     x->backward_done = true;
     return APML_OK;
@@ -923,6 +939,10 @@ apml_status apml_backward(apml_ctx* x, const float* grad_loss, float* grad_pred,
                    : x->idx16 ? launch_cluster(x, k_sparse_bwd<uint16_t>, a, s, "bwd", 6)
                               : launch_cluster(x, k_sparse_bwd<uint32_t>, a, s, "bwd", 6);
   if (st != APML_OK) return st;
+  if (grad_gt) {
+    k_grad_gt<<<dim3((unsigned)((x->M + 255) / 256), (unsigned)x->B), 256, 0, s>>>(a);
+    x->launches += 1;
+  }
   mark(x, 8, s);
   x->launches += 1;
   CK(cudaGetLastError());

@@ -76,6 +76,8 @@ struct SparseArgs {
   float* loss;
   const float* grad_loss;
   float* grad_pred;
+  float* gw;       // optional [B][cap]: Eq. (5) weight cbar / (c + eps_dist) per CSR entry (grad_gt)
+  float* grad_gt;  // optional [B][M][3]
   size_t smem_bytes;
   int rep_smem;
   unsigned long long* dbg;  // optional phase timestamps [grid][16] (APML_PHASES=1), else NULL
@@ -1338,6 +1340,7 @@ __device__ void grad_rows(const SparseArgs& A, int b, Slice s, const LongList& l
           }
         }
         const double w = cbar / ((double)cv[u] + (double)A.eps_dist);  // Eq. (5)
+        if (A.gw) A.gw[pb + p0 + u * G + mem] = (float)w;
         gx += w * ((double)x.x - (double)y[u].x);
         gy += w * ((double)x.y - (double)y[u].y);
         gz += w * ((double)x.z - (double)y[u].z);
@@ -1551,6 +1554,35 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
   grad_rows<1, 4>(A, b, sr, llr);
   grad_rows<32, 1>(A, b, sr, llr);
   phase(A, 5);
+}
+
+// Gradient with respect to gt: the loss depends on y only through the costs
+// c_ij, so by Eq. (5) with the roles of x and y exchanged (dc/dy_j = -(x_i - y_j) / c_ij),
+//   ybar_j = - sum_i w_ij (x_i - y_j),   w_ij = cbar_ij / (c_ij + eps_dist),
+// with the per-entry weights w written by grad_rows (CSR order) and summed here over each
+// column's CSC segment in sorted order (deterministic).  Thread per column, all pairs.
+__global__ void __launch_bounds__(256) k_grad_gt(const SparseArgs A) {
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int N = A.N, M = A.M;
+  if (j >= M) return;
+  float* g = A.grad_gt + ((size_t)b * M + orig_col(A, b, (uint32_t)j)) * 3;
+  if (A.cursor[b] > A.cap) {
+    const float nan = __int_as_float(0x7fc00000);
+    g[0] = nan; g[1] = nan; g[2] = nan;
+    return;
+  }
+  const size_t pb = (size_t)b * A.cap;
+  const unsigned* cp = A.col_ptr + (size_t)b * (M + 1);
+  const float4 y = A.gt4[(size_t)b * M + j];
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  for (unsigned q = cp[j]; q < cp[j + 1]; ++q) {
+    const float4 x = A.pred4[(size_t)b * N + A.csc_i[pb + q]];
+    const double w = (double)A.gw[pb + A.csc_perm[pb + q]];
+    gx -= w * ((double)x.x - (double)y.x);
+    gy -= w * ((double)x.y - (double)y.y);
+    gz -= w * ((double)x.z - (double)y.z);
+  }
+  g[0] = (float)gx; g[1] = (float)gy; g[2] = (float)gz;
 }
 
 }  // namespace apml

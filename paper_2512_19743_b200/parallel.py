@@ -155,9 +155,13 @@ class _RowShardedFunction(torch.autograd.Function):
 
     @staticmethod
     def backward(fctx, grad_loss):
-        g = fctx.apml.backward(grad_loss)
+        gg = None
+        if fctx.needs_input_grad[1]:  # d global loss / d gt, summed over ranks (every rank)
+            g, gg = fctx.apml.backward(grad_loss, want_gt=True)
+        else:
+            g = fctx.apml.backward(grad_loss)
         fctx.apml.close()
-        return g, None, None, None, None, None
+        return g, gg, None, None, None, None
 
 
 def apml_loss_rowsharded(pred_local: torch.Tensor, gt: torch.Tensor, row_offset: int, n_global: int,

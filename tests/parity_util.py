@@ -84,3 +84,21 @@ def normwise(a, b) -> float:
     d = np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64))
     n = np.linalg.norm(np.asarray(b, np.float64))
     return d / n if n > 0 else d
+
+
+def well_conditioned_gt(x, y, plan, cfg, thresh=1e6) -> np.ndarray:
+    """Boolean mask over gt points: the gt analogue of well_conditioned (column j's own line
+    and every row whose argmin / second argmin is j)."""
+    N, M = x.shape[0], y.shape[0]
+    rows, cols = plan.lines(0), plan.lines(1)
+    s = float(np.median(rows["m"]))
+    ok = np.ones(M, bool)
+    if N > 1:
+        ok &= ~(_lam(N, cfg.p_min) * s * s / np.maximum(cols["g"], 1e-300) ** 2 >= thresh)
+    if M > 1:
+        bad_r = _lam(M, cfg.p_min) * s * s / np.maximum(rows["g"], 1e-300) ** 2 >= thresh
+        for i in np.nonzero(bad_r)[0]:
+            for j in (rows["a"][i], rows["b"][i]):
+                if j >= 0:
+                    ok[j] = False
+    return ok

@@ -14,7 +14,7 @@ import torch
 
 from oracle import OracleConfig, SparsePlan, batch as oracle_batch
 from synth import clouds
-from tests.parity_util import boundary, flags_map, normwise, support_diff, well_conditioned
+from tests.parity_util import boundary, flags_map, normwise, support_diff, well_conditioned, well_conditioned_gt
 
 pytestmark = pytest.mark.gpu
 
@@ -280,3 +280,65 @@ def test_sparse_stage_fallback_paths(env, monkeypatch):
         lg, gg, ctx = _run(x, y, cfg)
         for b in range(B):
             _check_pair(x, y, cfg, lg, gg, ctx, b)
+
+
+GT_CASES = [("uniform", 2, 300, 280, 21), ("mmfi", 2, 512, 1024, 22), ("shapenet", 2, 700, 333, 23)]
+
+
+def _check_grad_gt(x, y, cfg, gp, gg):
+    """grad w.r.t. gt (apml_backward_ex) against the oracle's ybar; translation
+    invariance sum xbar + sum ybar = 0 on the GPU values themselves."""
+    oc = _ocfg(cfg)
+    for b in range(x.shape[0]):
+        plan = SparsePlan(x[b], y[b], oc)
+        gx, gy = plan.backward(1.0)
+        if cfg.grad_mode == "full":
+            mask = well_conditioned_gt(x[b], y[b], plan, oc)
+            assert mask.mean() > 0.9
+            e = normwise(gg[b][mask], gy[mask])
+        else:
+            e = normwise(gg[b], gy)
+        assert e <= GRAD_RTOL, f"pair {b}: grad_gt normwise error {e:.3e} ({cfg.grad_mode})"
+        t = np.abs(gp[b].sum(0) + gg[b].sum(0)).max()
+        assert t <= 1e-4 * np.abs(gg[b]).sum(0).max(), f"pair {b}: translation invariance {t:.3e}"
+
+
+@pytest.mark.parametrize("case", GT_CASES, ids=lambda c: f"{c[0]}-{c[2]}x{c[3]}")
+@pytest.mark.parametrize("mode", ["full", "plan_detached"])
+def test_grad_gt_matches_oracle(case, mode):
+    Config, forward = _gpu()
+    kind, B, N, M, seed = case
+    x, y = clouds.batch(kind, B, N, M, seed)
+    cfg = Config(grad_mode=mode)
+    _, ctx = forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"), cfg)
+    gp, gg = ctx.backward(torch.ones(B, device="cuda"), want_gt=True)
+    torch.cuda.synchronize()
+    _check_grad_gt(x, y, cfg, gp.cpu().numpy().astype(np.float64), gg.cpu().numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("env", [{"APML_FWD2": "0"}, {"APML_GRID": "1"}, {"APML_CULL": "1"},
+                                 {"APML_CULL": "1", "APML_GRID": "1"}],
+                         ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
+def test_grad_gt_every_path(env, monkeypatch):
+    Config, forward = _gpu()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x, y = clouds.batch("uniform", 2, 700, 650, 24)
+    cfg = Config()
+    _, ctx = forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"), cfg)
+    gp, gg = ctx.backward(torch.ones(2, device="cuda"), want_gt=True)
+    torch.cuda.synchronize()
+    _check_grad_gt(x, y, cfg, gp.cpu().numpy().astype(np.float64), gg.cpu().numpy().astype(np.float64))
+
+
+def test_grad_gt_through_autograd():
+    """apml_loss with gt.requires_grad: torch autograd receives both gradients."""
+    _gpu()
+    from paper_2512_19743_b200 import Config, apml_loss
+    x, y = clouds.batch("shapenet", 2, 300, 300, 25)
+    pred = torch.tensor(x, device="cuda", requires_grad=True)
+    gt = torch.tensor(y, device="cuda", requires_grad=True)
+    apml_loss(pred, gt, Config(), reduction="sum").backward()
+    torch.cuda.synchronize()
+    _check_grad_gt(x, y, Config(), pred.grad.cpu().numpy().astype(np.float64),
+                   gt.grad.cpu().numpy().astype(np.float64))

@@ -14,7 +14,7 @@ import torch.multiprocessing as mp
 
 from oracle import OracleConfig, SparsePlan
 from synth import clouds
-from tests.parity_util import normwise, well_conditioned
+from tests.parity_util import normwise, well_conditioned, well_conditioned_gt
 
 pytestmark = pytest.mark.gpu
 
@@ -36,12 +36,13 @@ def _run_rank(rank, world, port, kind, B, N, M, mode, out):
     x, y = clouds.batch(kind, B, N, M, seed=41)
     a, b = shard_rows(N, rank, world)
     pred = torch.tensor(x[:, a:b], device="cuda", requires_grad=True)
-    gt = torch.tensor(y, device="cuda")
+    gt = torch.tensor(y, device="cuda", requires_grad=True)
     comm = Collectives(device="cuda")
     loss = apml_loss_rowsharded(pred, gt, a, N, Config(grad_mode=mode), comm, reduction="none")
     loss.sum().backward()
     torch.cuda.synchronize()
-    out[rank] = (loss.detach().cpu().numpy().tolist(), a, b, pred.grad.cpu().numpy().tolist(), comm.errors)
+    out[rank] = (loss.detach().cpu().numpy().tolist(), a, b, pred.grad.cpu().numpy().tolist(), comm.errors,
+                 gt.grad.cpu().numpy().tolist())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -66,13 +67,18 @@ def test_rowsharded_matches_oracle(world, mode, case, cull_env):
     oc = OracleConfig(grad_mode=0 if mode == "full" else 1)
     grad = np.zeros((B, N, 3))
     for r in range(world):
-        loss, a, b, g, errs = out[r]
+        loss, a, b, g, errs, _ = out[r]
         assert not errs
         grad[:, a:b] = np.asarray(g)
     for bb in range(B):
         plan = SparsePlan(x[bb], y[bb], oc)
         for r in range(world):
             assert abs(out[r][0][bb] - plan.loss) <= 1e-5 * plan.loss
-        gx, _ = plan.backward()
+        gx, gy = plan.backward()
         mask = well_conditioned(x[bb], y[bb], plan, oc) if mode == "full" else np.ones(N, bool)
         assert normwise(grad[bb][mask], gx[mask]) <= 1e-4
+        # grad w.r.t. gt: every rank holds the sum over ranks (apml_backward_ex all-reduce)
+        mg = well_conditioned_gt(x[bb], y[bb], plan, oc) if mode == "full" else np.ones(M, bool)
+        for r in range(world):
+            ggr = np.asarray(out[r][5])[bb]
+            assert normwise(ggr[mg], gy[mg]) <= 1e-4
