@@ -187,9 +187,16 @@ int max_smem_optin() {
 }
 
 // Column-range split of a sweep so that the grid covers the SMs several times over.
+// Test / diagnostics overrides of the sparse-stage plan (exercise the fallback paths at sizes
+// the oracle can check): APML_FORCE_IDX32=1, APML_SMEM_LIMIT=<bytes>, APML_CL=<1|2|4|8>.
+long env_long(const char* name, long dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? strtol(e, nullptr, 10) : dflt;
+}
+
 void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk) {
   const int64_t blocks = own_np / kOwnTile * B;
-  const int64_t target = 4LL * num_sms() * 4;  // ~4 waves of 4 CTAs / SM
+  const int64_t target = env_long("APML_SPLIT_TARGET", 4LL * num_sms() * 4);  // ~4 waves of 4 CTAs / SM
   int64_t s = (target + blocks - 1) / blocks;
   const int64_t tiles = str_np / kTQ;
   if (s > tiles) s = tiles;
@@ -203,13 +210,6 @@ void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk) {
 size_t slice_bytes_h(int64_t nl, int64_t cnt, size_t idx, bool acc) {
   auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
   return a16(4 * (size_t)(nl + 1)) + a16(idx * (size_t)cnt) + a16(4 * (size_t)cnt) + (acc ? a16(4 * (size_t)cnt) : 0);
-}
-
-// Test / diagnostics overrides of the sparse-stage plan (exercise the fallback paths at sizes
-// the oracle can check): APML_FORCE_IDX32=1, APML_SMEM_LIMIT=<bytes>, APML_CL=<1|2|4|8>.
-long env_long(const char* name, long dflt) {
-  const char* e = getenv(name);
-  return (e && *e) ? strtol(e, nullptr, 10) : dflt;
 }
 
 // Sparse-stage plan: cluster size, replica placement, dynamic shared memory.

@@ -65,13 +65,16 @@ k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restri
   __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ];
 
   f2_t nx[R], ny[R], nz[R];
-  float m[R], s[R];
+  // two independent running (min, second) per owned point (streamed points 0,1 / 2,3 of each
+  // group of 4), merged exactly at the end: twice the independent dependency chains
+  float m[R], s[R], m2[R], s2[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int idx = base + r * kSweepThreads;
     const float x = -__ldg(own + idx), y = -__ldg(own + own_np + idx), z = -__ldg(own + 2 * own_np + idx);
     nx[r] = f2_pack(x, x); ny[r] = f2_pack(y, y); nz[r] = f2_pack(z, z);
     m[r] = __int_as_float(0x7f800000); s[r] = m[r];
+    m2[r] = m[r]; s2[r] = m[r];
   }
   const int j0 = split * chunk, j1 = min(str_np, j0 + chunk);
   for (int jt = j0; jt < j1; jt += kTQ) {
@@ -92,13 +95,16 @@ k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restri
         f2_unpack(d01, d0, d1);
         f2_unpack(d23, d2, d3);
         top2_pair(m[r], s[r], d0, d1);
-        top2_pair(m[r], s[r], d2, d3);
+        top2_pair(m2[r], s2[r], d2, d3);
       }
     }
   }
   float2* out = part + ((size_t)split * B + b) * own_np;
 #pragma unroll
-  for (int r = 0; r < R; ++r) out[base + r * kSweepThreads] = make_float2(m[r], s[r]);
+  for (int r = 0; r < R; ++r) {
+    top2_merge(m[r], s[r], m2[r], s2[r]);
+    out[base + r * kSweepThreads] = make_float2(m[r], s[r]);
+  }
 }
 
 // S2: one thread per line.  lam = Lambda_K (fp64 on the host, rounded), rho = ln(1/tau) /
@@ -168,6 +174,42 @@ __device__ __forceinline__ void warp_flush(int b, uint2* wbuf, int n, uint32_t c
   __syncwarp();
 }
 
+// Per-lane emission queues (k_emit): every lane appends its own hits to its own slots of a
+// shared-memory queue with no cross-lane communication (the common case -- a warp with a hit
+// somewhere in a 4-column step -- used to cost 4 ballots + popcounts + a serialised compaction
+// per step); the warp flushes all queues with one shuffle scan and one returning atomic when a
+// queue is nearly full and at the end.
+constexpr int kLaneQ = 16;  // queue slots per lane
+
+__device__ __forceinline__ void lane_flush(int b, const uint2* q, int cnt, uint32_t cap, uint2* __restrict__ ebuf,
+                                           unsigned* __restrict__ cursor, unsigned* __restrict__ aux_cnt,
+                                           unsigned* __restrict__ row_cnt, int N, unsigned* __restrict__ col_cnt,
+                                           int M) {
+  const int lane = threadIdx.x & 31;
+  unsigned inc = (unsigned)cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+  if (total == 0) return;
+  unsigned base = 0;
+  if (lane == 31) base = atomicAdd(cursor + b, total);
+  base = __shfl_sync(0xffffffffu, base, 31) + inc - (unsigned)cnt;
+  unsigned aux = 0;
+  for (int k = 0; k < cnt; ++k) {
+    const uint2 e = q[k * 32];
+    const unsigned pos = base + k;
+    if (pos < cap) ebuf[(size_t)b * cap + pos] = e;
+    atomicAdd(row_cnt + (size_t)b * (N + 1) + e.x, 1u);
+    atomicAdd(col_cnt + (size_t)b * (M + 1) + (e.y & kIdxMask), 1u);
+    aux += (e.y & (kFlagRow | kFlagCol)) ? 0u : 1u;
+  }
+  aux = __reduce_add_sync(0xffffffffu, aux);
+  if (lane == 0 && aux) atomicAdd(aux_cnt + b, aux);
+}
+
 // S3 (Pass B).  Rows own pred points; gt streamed with its column radii in shared memory.
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
@@ -182,9 +224,9 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ], sR[kTQ], sE[kTQ];
-  __shared__ uint2 wbuf_all[kSweepThreads / 32][kWarpBuf];
-  uint2* wbuf = wbuf_all[w];
-  int wcnt = 0;  // warp-uniform staged count
+  __shared__ uint2 queue_all[kSweepThreads / 32][kLaneQ][32];  // [warp][slot][lane]: conflict-free
+  uint2* q = &queue_all[w][0][lane];
+  int qn = 0;  // this lane's queued entries
 
   f2_t nx[R], ny[R], nz[R];
   float rR2[R], rE2[R];
@@ -200,7 +242,6 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
       rR2[r] = -1.f; rE2[r] = -1.f;
     }
   }
-  const unsigned lt_mask = (1u << lane) - 1u;
   const int j0 = split * chunk, j1 = min(mp, j0 + chunk);
   for (int jt = j0; jt < j1; jt += kTQ) {
     __syncthreads();
@@ -219,10 +260,11 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
     const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
     const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
     const float4* pE = reinterpret_cast<const float4*>(sE);
+    const float4* pR = reinterpret_cast<const float4*>(sR);
 #pragma unroll 2
-    for (int q = 0; q < kTQ / 4; ++q) {
-      const ulonglong2 qx = px[q], qy = py[q], qz = pz[q];
-      const float4 ce = pE[q];
+    for (int qq = 0; qq < kTQ / 4; ++qq) {
+      const ulonglong2 qx = px[qq], qy = py[qq], qz = pz[qq];
+      const float4 ce = pE[qq];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
@@ -230,33 +272,34 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
         float d[4];
         f2_unpack(d01, d[0], d[1]);
         f2_unpack(d23, d[2], d[3]);
-        const bool hit = (d[0] <= fmaxf(rE2[r], ce.x)) | (d[1] <= fmaxf(rE2[r], ce.y)) |
-                         (d[2] <= fmaxf(rE2[r], ce.z)) | (d[3] <= fmaxf(rE2[r], ce.w));
-        if (__any_sync(0xffffffffu, hit)) {  // warp-uniform; ~5 kept entries per line of K
+        const bool h0 = d[0] <= fmaxf(rE2[r], ce.x), h1 = d[1] <= fmaxf(rE2[r], ce.y);
+        const bool h2 = d[2] <= fmaxf(rE2[r], ce.z), h3 = d[3] <= fmaxf(rE2[r], ce.w);
+        if (h0 | h1 | h2 | h3) {  // rare per lane (~1 %): this lane's hits only
           const uint32_t i = base + r * kSweepThreads;
+          const float4 cr = pR[qq];
+          const bool hh[4] = {h0, h1, h2, h3};
+          const float crv[4] = {cr.x, cr.y, cr.z, cr.w};
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const int t = 4 * q + c;
-            const uint32_t j = jt + t;
-            const bool h = d[c] <= fmaxf(rE2[r], sE[t]) && i < (uint32_t)N && j < (uint32_t)M;
-            const unsigned bal = __ballot_sync(0xffffffffu, h);
-            if (h) {
-              const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= sR[t] ? kFlagCol : 0u);
-              wbuf[wcnt + __popc(bal & lt_mask)] = make_uint2(i, j | fl);
+            const uint32_t j = jt + 4 * qq + c;
+            if (hh[c] && i < (uint32_t)N && j < (uint32_t)M) {
+              const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= crv[c] ? kFlagCol : 0u);
+              q[qn * 32] = make_uint2(i, j | fl);
+              ++qn;
             }
-            wcnt += __popc(bal);
           }
-          if (wcnt > kFlushAt) {
-            __syncwarp();
-            warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
-            wcnt = 0;
-          }
+        }
+        if (__any_sync(0xffffffffu, qn > kLaneQ - 4)) {  // warp-uniform; a step adds <= 4
+          __syncwarp();
+          lane_flush(b, q, qn, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+          qn = 0;
+          __syncwarp();
         }
       }
     }
   }
   __syncwarp();
-  if (wcnt) warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+  lane_flush(b, q, qn, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
 }
 
 }  // namespace apml
