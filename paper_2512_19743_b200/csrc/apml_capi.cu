@@ -44,6 +44,10 @@ apml_status fail(apml_status s, const std::string& msg) {
 #define APML_SWEEP_R 4
 #endif
 constexpr int kR = APML_SWEEP_R;             // owned points per thread in the sweeps
+#ifndef APML_CULL_R
+#define APML_CULL_R 2
+#endif
+constexpr int kRc = APML_CULL_R;  // owned 32-point groups per warp in the culled sweeps (more warps)
 constexpr int kOwnTile = kSweepThreads * kR; // owned points per CTA (512)
 
 inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
@@ -491,10 +495,10 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->pcb, c->pfb);
   k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
   mark(c, 1, s);
-  k_line_top2_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
+  k_line_top2_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
       c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r, c->clamp + 1);
   mark(c, 2, s);
-  k_line_top2_cull<kR><<<dim3(Mp / kOwnTile, B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
+  k_line_top2_cull<kRc><<<dim3(Mp / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
       c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c, c->clamp + 2);
   c->launches += 11;  // + the scan's own
   CK(cudaGetLastError());
@@ -506,7 +510,7 @@ apml_status launch_emit_cull(apml_ctx* c) {
   cudaStream_t s = c->stream;
   k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
                                                c->gfe2);
-  k_emit_cull<kR><<<dim3(Np / kOwnTile, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
+  k_emit_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
       c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor, c->aux,
       c->row_cnt, c->col_cnt, c->clamp + 3);
   c->launches += 2;
