@@ -163,6 +163,18 @@ APML_API apml_status apml_forward(const float* pred, const float* gt, int64_t B,
                          const apml_config* cfg, const apml_allocator* alloc, void* stream,
                          float* loss, apml_ctx** ctx_out);
 
+/* Ragged batches (MM-Fi clouds of varying size): pair b uses only its first
+ * n_sizes[b] pred points and m_sizes[b] gt points of the padded [B][N][3] / [B][M][3] buffers
+ * (the padding is never read), every line length K in Eq. (1) is the PAIR's (m_b for rows,
+ * n_b for columns), and the result per pair equals apml_forward on that pair alone.
+ * n_sizes, m_sizes: HOST arrays [B] with 1 <= n_b <= N, 1 <= m_b <= M (else APML_ERR_SHAPE).
+ * apml_backward writes zeros into the padding rows of grad_pred (and of grad_gt).
+ * Ragged contexts run the full (non-culled) sweeps and the per-pair cluster sparse stage.
+ * Errors as apml_forward. */
+APML_API apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
+                                         const int64_t* n_sizes, const int64_t* m_sizes, const apml_config* cfg,
+                                         const apml_allocator* alloc, void* stream, float* loss, apml_ctx** ctx_out);
+
 /* Forward with one cloud's pred rows SHARDED over the ranks of `comm` (north_star: "pred
  * rows shard and per-iteration column sums are all-reduced").  This rank holds pred rows
  * [row_offset, row_offset + N_local) of every pair (pred_local device [B][N_local][3]) and

@@ -20,7 +20,8 @@ APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE, APML_FLAG_STAGE_TIMING = 1, 2, 4
 STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "sparse_fwd", "sparse_bwd")
 
 # exported symbols declared in include/apml.h (checked by tests/test_abi.py)
-EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forward_rowsharded",
+EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forward_ragged",
+           "apml_forward_rowsharded",
            "apml_backward", "apml_backward_ex",
            "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
            "apml_ctx_destroy",
@@ -82,6 +83,9 @@ def lib() -> C.CDLL:
         L.apml_forward.restype = C.c_int
         L.apml_forward.argtypes = [vp, vp, i64, i64, i64, C.POINTER(ApmlConfig),
                                    C.POINTER(ApmlAllocator), vp, vp, C.POINTER(vp)]
+        L.apml_forward_ragged.restype = C.c_int
+        L.apml_forward_ragged.argtypes = [vp, vp, i64, i64, i64, vp, vp, C.POINTER(ApmlConfig),
+                                          C.POINTER(ApmlAllocator), vp, vp, C.POINTER(vp)]
         L.apml_forward_rowsharded.restype = C.c_int
         L.apml_forward_rowsharded.argtypes = [vp, vp, i64, i64, i64, i64, i64, C.POINTER(ApmlConfig),
                                               C.POINTER(ApmlAllocator), C.POINTER(ApmlComm), vp, vp,

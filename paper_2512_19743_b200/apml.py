@@ -137,8 +137,12 @@ class Context:
 
 
 def forward(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
-            keep_ctx: bool = True, loss_out: torch.Tensor | None = None):
-    """Per-pair losses [B] (fp32, device) and a Context for backward (or None)."""
+            keep_ctx: bool = True, loss_out: torch.Tensor | None = None,
+            n_sizes=None, m_sizes=None):
+    """Per-pair losses [B] (fp32, device) and a Context for backward (or None).
+
+    Ragged batches (apml_forward_ragged): n_sizes / m_sizes (length B, host integers) give the
+    real cloud sizes of each pair inside the padded [B, N, 3] / [B, M, 3] tensors."""
     cfg = cfg or Config()
     pred = _check_points(pred, "pred")
     gt = _check_points(gt, "gt")
@@ -150,17 +154,25 @@ def forward(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
     c = cfg.to_c()
     with torch.cuda.device(pred.device):
         s = torch.cuda.current_stream(pred.device).cuda_stream
-        A.check(A.lib().apml_forward(pred.data_ptr(), gt.data_ptr(), B, N, M, C.byref(c),
-                                     C.byref(_ALLOC), s, loss.data_ptr(),
-                                     C.byref(h) if keep_ctx else None))
+        if n_sizes is None and m_sizes is None:
+            A.check(A.lib().apml_forward(pred.data_ptr(), gt.data_ptr(), B, N, M, C.byref(c),
+                                         C.byref(_ALLOC), s, loss.data_ptr(),
+                                         C.byref(h) if keep_ctx else None))
+        else:
+            nb = (C.c_int64 * B)(*[int(v) for v in n_sizes])
+            mb = (C.c_int64 * B)(*[int(v) for v in m_sizes])
+            A.check(A.lib().apml_forward_ragged(pred.data_ptr(), gt.data_ptr(), B, N, M,
+                                                C.cast(nb, C.c_void_p), C.cast(mb, C.c_void_p), C.byref(c),
+                                                C.byref(_ALLOC), s, loss.data_ptr(),
+                                                C.byref(h) if keep_ctx else None))
     ctx = Context(h.value, B, N, M, pred.device) if keep_ctx else None
     return loss, ctx
 
 
 class _APMLFunction(torch.autograd.Function):
     @staticmethod
-    def forward(fctx, pred, gt, cfg):
-        loss, ctx = forward(pred, gt, cfg, keep_ctx=True)
+    def forward(fctx, pred, gt, cfg, n_sizes=None, m_sizes=None):
+        loss, ctx = forward(pred, gt, cfg, keep_ctx=True, n_sizes=n_sizes, m_sizes=m_sizes)
         fctx.apml = ctx
         return loss
 
@@ -172,13 +184,14 @@ class _APMLFunction(torch.autograd.Function):
         else:
             g, gg = ctx.backward(grad_loss), None
         ctx.close()
-        return g, gg, None
+        return g, gg, None, None, None
 
 
 def apml_loss(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
-              reduction: str = "sum") -> torch.Tensor:
-    """Batched sparse APML (Alg. 1) with autograd w.r.t. pred."""
-    loss = _APMLFunction.apply(pred, gt, cfg or Config())
+              reduction: str = "sum", n_sizes=None, m_sizes=None) -> torch.Tensor:
+    """Batched sparse APML (Alg. 1) with autograd w.r.t. pred (and gt when it requires
+    grad).  n_sizes / m_sizes: per-pair real sizes of a ragged batch (padded tensors)."""
+    loss = _APMLFunction.apply(pred, gt, cfg or Config(), n_sizes, m_sizes)
     if reduction == "sum":
         return loss.sum()
     if reduction == "mean":

@@ -89,6 +89,12 @@ struct apml_ctx {
   size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
   bool fwd2 = false;      // sparse forward built in shared memory (k_fwd2.cuh)
   float* grad_gt = nullptr;  // set by apml_backward_ex for the duration of the call
+  // ragged batches (apml_forward_ragged): per-pair real sizes and Eq. (1) constants
+  bool ragged = false;
+  std::vector<int> nb_h, mb_h;
+  std::vector<float> lr_h;  // [B][4] = lam_r, rho_r, lam_c, rho_c
+  int *nb_d = nullptr, *mb_d = nullptr;
+  float* lr_d = nullptr;
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // spatially culled sweeps (k_cull.cuh)
   bool cull = false;
@@ -264,7 +270,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   // exact spatial culling of the sweeps pays off once a 512-point block is a small part of
   // the cloud (override: APML_CULL=0/1)
   const long fc = env_long("APML_CULL", -1);
-  c->cull = fc >= 0 ? fc != 0 : std::min(N, M) >= 4096;
+  c->cull = !c->ragged && (fc >= 0 ? fc != 0 : std::min(N, M) >= 4096);
   c->relabel = c->cull && (!c->rs || (c->comm.world == 1 && c->row_offset == 0)) && env_long("APML_RELABEL", 1) != 0;
   if (c->cull) {
     int lg = 0;
@@ -297,6 +303,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t o_d2 = k.take<float>(E), o_cs = k.take<float>(E), o_prow = k.take<float>(E), o_pcol = k.take<float>(E);
   size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
   const int64_t E2 = c->fwd2 ? E : 0;  // CSC-order copies written by k_sparse_fwd2
+  size_t o_nb = k.take<int>(c->ragged ? B : 0), o_mb = k.take<int>(c->ragged ? B : 0);
+  size_t o_lr = k.take<float>(c->ragged ? 4 * B : 0);
   size_t o_csc_if = k.take<uint32_t>(E2), o_csc_c = k.take<float>(E2), o_csc_pc = k.take<float>(E2);
   size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
   size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
@@ -339,6 +347,12 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
   c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
   c->csc_if = (uint32_t*)(p + o_csc_if); c->csc_c = (float*)(p + o_csc_c); c->csc_pc = (float*)(p + o_csc_pc);
+  if (c->ragged) {  // pageable host vectors: the copies are staged before the calls return
+    c->nb_d = (int*)(p + o_nb); c->mb_d = (int*)(p + o_mb); c->lr_d = (float*)(p + o_lr);
+    CK(cudaMemcpyAsync(c->nb_d, c->nb_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->mb_d, c->mb_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->lr_d, c->lr_h.data(), sizeof(float) * 4 * B, cudaMemcpyHostToDevice, c->stream));
+  }
   c->rowidx = (int2*)(p + o_rowidx); c->colidx = (int2*)(p + o_colidx);
   c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh); c->gvec = (float*)(p + o_gv);
   c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
@@ -477,8 +491,8 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   cudaStream_t s = c->stream;
   const int bits = c->cell_bits;
   if (!c->relabel) {  // float4 copies at original positions (relabelled: by k_cell_scatter)
-    k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, nullptr, c->pred4);
-    k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, nullptr, c->gt4);
+    k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, nullptr, c->pred4, nullptr);
+    k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, nullptr, c->gt4, nullptr);
     c->launches += 2;
   }
   k_pair_bbox_part<<<dim3(kBoxParts, B), kBoxThreads, 0, s>>>(pred, N, gt, M, c->bbpart);
@@ -527,9 +541,9 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     if (st != APML_OK) return st;
     mark(c, 3, s);
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, 1, B, N, N, M, c->lam_r, c->rho_r,
-        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
     k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, N, c->lam_c, c->rho_c,
-        c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+        c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
     mark(c, 4, s);
     if ((st = launch_emit_cull(c)) != APML_OK) return st;
     mark(c, 5, s);
@@ -537,8 +551,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     return APML_OK;
   }
   // S0 staging
-  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
-  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
+  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4, c->nb_d);
+  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4, c->mb_d);
   mark(c, 1, s);
   // S1 Pass A: rows (own pred, stream gt) and columns (own gt, stream pred)
   k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
@@ -549,14 +563,14 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 3, s);
   // S2 line constants
   k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
-      c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+      c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
   k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, N, c->lam_c,
-      c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+      c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
   mark(c, 4, s);
   // S3 Pass B emit
   k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
       c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
-      c->aux, c->row_cnt, c->col_cnt);
+      c->aux, c->row_cnt, c->col_cnt, c->nb_d, c->mb_d);
   mark(c, 5, s);
   c->launches += 7;
   CK(cudaGetLastError());
@@ -588,6 +602,7 @@ int local_allgather(const float* send, float* recv, int64_t n, void* stream, voi
 // Also when the per-pair cluster cannot keep its scaling-vector replicas in shared memory
 // (N + M too large): measured at C4 (B = 64, N = M = 16384) the grid-wide kernels win.
 bool use_grid_path(apml_ctx* c) {
+  if (c->ragged) return false;  // ragged batches: cluster path only
   const long f = env_long("APML_GRID", -1);
   if (f >= 0) return f != 0;
   if (c->B * 8 < num_sms() && c->N + c->M >= 65536) return true;
@@ -616,8 +631,8 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
     if ((st = launch_passA_cull(c, pred, gt)) != APML_OK) return st;
     k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, c->colpart);
   } else {
-    k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4);
-    k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4);
+    k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4, nullptr);
+    k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4, nullptr);
     mark(c, 1, s);
     k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
         c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
@@ -632,19 +647,19 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 3, s);
   if (c->cull)
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, 1, B, N, N, M, c->lam_r, c->rho_r,
-        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
   else
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
-        c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp);
+        c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
   k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->gath, c->comm.world, B, M, M, (int)c->N_global,
-      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp);
+      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
   mark(c, 4, s);
   if (c->cull) {
     if ((st = launch_emit_cull(c)) != APML_OK) return st;
   } else {
     k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
         c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
-        c->aux, c->row_cnt, c->col_cnt);
+        c->aux, c->row_cnt, c->col_cnt, nullptr, nullptr);
   }
   mark(c, 5, s);
   c->launches += 5;
@@ -764,11 +779,39 @@ const char* apml_last_error(void) { return g_err.c_str(); }
 apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
                          const apml_config* cfg, const apml_allocator* alloc, void* stream,
                          float* loss, apml_ctx** ctx_out) {
+  return apml_forward_ragged(pred, gt, B, N, M, nullptr, nullptr, cfg, alloc, stream, loss, ctx_out);
+}
+
+apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, int64_t N, int64_t M,
+                                const int64_t* n_sizes, const int64_t* m_sizes, const apml_config* cfg,
+                                const apml_allocator* alloc, void* stream, float* loss, apml_ctx** ctx_out) {
   if (ctx_out) *ctx_out = nullptr;
   apml_config c;
   if (cfg) c = *cfg; else apml_config_default(&c);
   apml_status st = validate(pred, gt, B, N, M, c);
   if (st != APML_OK) return st;
+  if ((n_sizes == nullptr) != (m_sizes == nullptr))
+    return fail(APML_ERR_INVALID_ARG, "n_sizes and m_sizes must both be given or both be NULL");
+  const bool ragged = n_sizes != nullptr;
+  std::vector<int> nbv, mbv;
+  std::vector<float> lrv;
+  if (ragged) {
+    nbv.resize((size_t)B); mbv.resize((size_t)B); lrv.resize(4 * (size_t)B);
+    const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t nb = n_sizes[b], mb = m_sizes[b];
+      if (nb < 1 || nb > N || mb < 1 || mb > M)
+        return fail(APML_ERR_SHAPE, "ragged sizes must satisfy 1 <= n_b <= N and 1 <= m_b <= M");
+      for (int64_t K : {nb, mb})
+        if (K > 1 && !((double)c.p_min * (double)K > 1.0))
+          return fail(APML_ERR_INVALID_ARG, "p_min <= 1/K makes T <= 0 (dense line); outside the sparse contract");
+      nbv[(size_t)b] = (int)nb; mbv[(size_t)b] = (int)mb;
+      lrv[4 * (size_t)b + 0] = (float)lambda_K(mb, c.p_min);  // rows: K = m_b
+      lrv[4 * (size_t)b + 1] = mb > 1 ? (float)(lt / lambda_K(mb, c.p_min)) : INFINITY;
+      lrv[4 * (size_t)b + 2] = (float)lambda_K(nb, c.p_min);  // columns: K = n_b
+      lrv[4 * (size_t)b + 3] = nb > 1 ? (float)(lt / lambda_K(nb, c.p_min)) : INFINITY;
+    }
+  }
   if (!loss) return fail(APML_ERR_INVALID_ARG, "loss must be a non-NULL device pointer");
   if (alloc && (!alloc->alloc || !alloc->free)) return fail(APML_ERR_INVALID_ARG, "allocator needs alloc and free");
   cudaStream_t s = (cudaStream_t)stream;
@@ -785,6 +828,7 @@ apml_status apml_forward(const float* pred, const float* gt, int64_t B, int64_t 
   for (int attempt = 0; attempt < 2; ++attempt) {
     apml_ctx* x = new apml_ctx();
     x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = s;
+    if (ragged) { x->ragged = true; x->nb_h = nbv; x->mb_h = mbv; x->lr_h = lrv; }
     if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
     if (c.flags & APML_FLAG_STAGE_TIMING) {
       x->timing = true;

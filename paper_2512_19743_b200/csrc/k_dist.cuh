@@ -28,15 +28,19 @@ namespace apml {
 constexpr int kSweepThreads = 128;
 constexpr int kTQ = 128;  // streamed points per shared-memory tile
 
+// nb (ragged batches, else NULL): pair b has nb[b] <= n real points; the rest of its n slots
+// are staged as sentinels (never a minimum, never emitted).
 __global__ void k_stage(const float* __restrict__ pts, int n, int np, float sentinel,
-                        float* __restrict__ soa, float4* __restrict__ p4) {
+                        float* __restrict__ soa, float4* __restrict__ p4, const int* __restrict__ nb) {
   const int b = blockIdx.y;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= np) return;
   float x = sentinel, y = sentinel, z = sentinel;
   if (k < n) {
-    const float* p = pts + ((size_t)b * n + k) * 3;
-    x = p[0]; y = p[1]; z = p[2];
+    if (!nb || k < nb[b]) {
+      const float* p = pts + ((size_t)b * n + k) * 3;
+      x = p[0]; y = p[1]; z = p[2];
+    }
     p4[(size_t)b * n + k] = make_float4(x, y, z, 0.f);
   }
   if (!soa) return;  // culled mode: the SoA copy is written in Morton order by k_cell_scatter
@@ -109,13 +113,28 @@ k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restri
 
 // S2: one thread per line.  lam = Lambda_K (fp64 on the host, rounded), rho = ln(1/tau) /
 // Lambda_K (+inf for tau = 0).  K == 1 lines keep their single entry with P = 1.
+// Ragged batches (nown != NULL): pair b has nown[b] real lines of length K = kpair[b], with
+// lam / rho = lr[4 b + lr_off], lr[4 b + lr_off + 1]; the padding lines are inactive (radii
+// -1: nothing emitted; no entries downstream).
 __global__ void k_line_info(const float2* __restrict__ part, int S, int B, int own_np, int n,
                             int K, float lam, float rho, float delta, float eps_g,
                             LineA* __restrict__ A, LineB* __restrict__ Bo,
-                            unsigned long long* __restrict__ clamp_count) {
+                            unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
+                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off) {
   const int b = blockIdx.y;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
+  if (nown) {
+    if (k >= nown[b]) {
+      const float inf = __int_as_float(0x7f800000);
+      A[(size_t)b * n + k] = LineA{inf, inf, -1.f, -1.f};
+      Bo[(size_t)b * n + k] = LineB{0.f, 0.f, 0.f, 0};
+      return;
+    }
+    K = kpair[b];
+    lam = lr[4 * b + lr_off];
+    rho = lr[4 * b + lr_off + 1];
+  }
   float m2 = __int_as_float(0x7f800000), s2 = m2;
   for (int sp = 0; sp < S; ++sp) {
     const float2 p = part[((size_t)sp * B + b) * own_np + k];
@@ -217,8 +236,9 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
        const float* __restrict__ gt_soa, int mp, int M, const LineA* __restrict__ colA,
        int chunk, uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
        unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt,
-       unsigned* __restrict__ col_cnt) {
+       unsigned* __restrict__ col_cnt, const int* __restrict__ nb, const int* __restrict__ mb) {
   const int b = blockIdx.z, split = blockIdx.y;
+  const uint32_t nreal = nb ? (uint32_t)nb[b] : (uint32_t)N, mreal = mb ? (uint32_t)mb[b] : (uint32_t)M;
   const float* own = pred_soa + (size_t)b * 3 * np;
   const float* str = gt_soa + (size_t)b * 3 * mp;
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
@@ -282,7 +302,7 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint32_t j = jt + 4 * qq + c;
-            if (hh[c] && i < (uint32_t)N && j < (uint32_t)M) {
+            if (hh[c] && i < nreal && j < mreal) {
               const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= crv[c] ? kFlagCol : 0u);
               q[qn * 32] = make_uint2(i, j | fl);
               ++qn;

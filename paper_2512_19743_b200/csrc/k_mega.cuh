@@ -744,16 +744,18 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // Eq. (3): colsum_j = b_j Q_j, b_j <- b_j / (colsum_j + eps)
-  auto col_upd = [&](int j, float Q, int l) {
+  // an EMPTY line (the padding lines of a ragged pair; a real line always holds its argmin)
+  // keeps its scale: Eq. (3)/(4) would divide by eps alone and overflow
+  auto col_upd = [&](int j, float Q, int l, bool empty = false) {
     const float bj = bv[j];
-    const float nb = __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
+    const float nb = empty ? bj : __fdividef(bj, __fmaf_rn(bj, Q, A.eps));
     xchg_put(xb, CL, j, nb);
     bh[(size_t)l * M + j] = nb;
   };
   // Eq. (4): rowsum_i = a_i R_i, a_i <- a_i / (rowsum_i + eps)
-  auto row_upd = [&](int i, float Rs, int l) {
+  auto row_upd = [&](int i, float Rs, int l, bool empty = false) {
     const float ai = a[i];
-    const float na = __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
+    const float na = empty ? ai : __fdividef(ai, __fmaf_rn(ai, Rs, A.eps));
     xchg_put(xa, CL, i, na);
     ah[(size_t)l * N + i] = na;
   };
@@ -761,7 +763,7 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
       const int k = j - sc.lo;
       const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
-      if (p1 - p0 <= kRegLine) col_upd(j, seg_dot(C, p0, p1, a), l);
+      if (p1 - p0 <= kRegLine) col_upd(j, seg_dot(C, p0, p1, a), l, p1 == p0);
     }
     for (int q = w; q < llc.count(); q += nw) {
       const int j = llc.line(q), k = j - sc.lo;
@@ -774,7 +776,7 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
       const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
-      if (p1 - p0 <= kRegLine) row_upd(i, seg_dot(R, p0, p1, bv), l);
+      if (p1 - p0 <= kRegLine) row_upd(i, seg_dot(R, p0, p1, bv), l, p1 == p0);
     }
     for (int q = w; q < llr.count(); q += nw) {
       const int i = llr.line(q), k = i - sr.lo;

@@ -342,3 +342,68 @@ def test_grad_gt_through_autograd():
     torch.cuda.synchronize()
     _check_grad_gt(x, y, Config(), pred.grad.cpu().numpy().astype(np.float64),
                    gt.grad.cpu().numpy().astype(np.float64))
+
+
+def _ragged_case(seed):
+    rng = np.random.default_rng(seed)
+    B, N, M = 5, 700, 520
+    ns = [700, 1, 300, 437, 64]
+    ms = [520, 260, 1, 333, 128]
+    x, y = clouds.batch("mmfi", B, N, M, seed)
+    # the padding is garbage on purpose: it must never be read
+    for b in range(B):
+        x[b, ns[b]:] = rng.normal(size=(N - ns[b], 3)).astype(np.float32) * 1e3
+        y[b, ms[b]:] = np.nan
+    return x, y, ns, ms
+
+
+@pytest.mark.parametrize("env", [{}, {"APML_FWD2": "0"}, {"APML_CL": "1"}],
+                         ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()) or "default")
+@pytest.mark.parametrize("mode", ["full", "plan_detached"])
+def test_ragged_batch_matches_per_pair_oracle(env, mode, monkeypatch):
+    """apml_forward_ragged: every pair equals the oracle on its trimmed clouds
+    (loss, support, grad_pred and grad_gt), padding rows of the gradients are zero; includes
+    K = 1 pairs (n_b = 1, m_b = 1)."""
+    Config, forward = _gpu()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x, y, ns, ms = _ragged_case(31)
+    B = x.shape[0]
+    cfg = Config(grad_mode=mode)
+    loss, ctx = forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"), cfg,
+                        n_sizes=ns, m_sizes=ms)
+    gp, gg = ctx.backward(torch.ones(B, device="cuda"), want_gt=True)
+    torch.cuda.synchronize()
+    loss = loss.cpu().numpy().astype(np.float64)
+    gp = gp.cpu().numpy().astype(np.float64)
+    gg = gg.cpu().numpy().astype(np.float64)
+    oc = _ocfg(cfg)
+    for b in range(B):
+        xb, yb = x[b, :ns[b]], y[b, :ms[b]]
+        plan = SparsePlan(xb, yb, oc)
+        rel = abs(loss[b] - plan.loss) / abs(plan.loss)
+        assert rel <= LOSS_RTOL, f"pair {b} ({ns[b]}x{ms[b]}): loss rel {rel:.3e}"
+        gs, os_ = ctx.support(b), plan.support()
+        only_g, only_o = support_diff(gs, os_)
+        bad = [e for e in only_g | only_o if not boundary(xb, yb, plan, e[0], e[1], oc)]
+        assert not bad, f"pair {b}: support differs at {sorted(bad)[:5]}"
+        assert np.all(gp[b, ns[b]:] == 0) and np.all(gg[b, ms[b]:] == 0)
+        gx, gy = plan.backward(1.0)
+        if mode == "full":
+            mx = well_conditioned(xb, yb, plan, oc)
+            my = well_conditioned_gt(xb, yb, plan, oc)
+        else:
+            mx, my = np.ones(ns[b], bool), np.ones(ms[b], bool)
+        if ns[b] > 1 or ms[b] > 1:
+            assert normwise(gp[b, :ns[b]][mx], gx[mx]) <= GRAD_RTOL, f"pair {b}: grad_pred"
+            assert normwise(gg[b, :ms[b]][my], gy[my]) <= GRAD_RTOL, f"pair {b}: grad_gt"
+
+
+def test_ragged_rejects_bad_sizes():
+    Config, forward = _gpu()
+    x, y, ns, ms = _ragged_case(32)
+    from paper_2512_19743_b200._lib import ApmlError
+    for bad_n, bad_m in (([0] + ns[1:], ms), (ns, [9999] + ms[1:])):
+        with pytest.raises(ApmlError, match="SHAPE"):
+            forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"), Config(),
+                    n_sizes=bad_n, m_sizes=bad_m)
