@@ -30,6 +30,8 @@ CONFIGS = {
                workload="C2 ShapeNet-55-shaped: B=32, N=M=2048 (FoldingNet-style step)"),
     "C3": dict(B=512, N=1024, M=512, kind="mmfi",
                workload="C3 MM-Fi-shaped: B=512, N=1024, M=512 (N != M)"),
+    "C3R": dict(B=512, N=1024, M=1024, kind="mmfi", ragged=(256, 1024),
+                workload="C3 MM-Fi-shaped ragged: B=512, per-pair N_b, M_b ~ U[256, 1024], N_b != M_b"),
     "C4": dict(B=64, N=16384, M=16384, kind="shapenet",
                workload="C4 PCN-shaped: B=64, N=M=16384 (per-GPU batch at weak scaling)"),
     "C5": dict(B=1, N=262144, M=262144, kind="scene",
@@ -122,6 +124,42 @@ def cpu_baseline(cfg_name: str, seed: int, budget_s: float = 15.0) -> dict:
             "sample": f"{reps} x {n} pairs of {cfg_name} ({c['kind']}, N={c['N']}, M={c['M']}){note}, fwd+full bwd, fp64, {el:.1f} s"}
 
 
+def _ragged_reference(args, c) -> None:
+    """--impl reference for a ragged config: the oracle per pair (SparsePlan + backward, one
+    core) on the first pairs of the same seeded ragged batch."""
+    import numpy as np
+    from oracle import OracleConfig, SparsePlan
+    from synth import clouds
+    lo, hi = c["ragged"]
+    rng = np.random.default_rng(args.seed)
+    sizes = []
+    for _ in range(8):
+        nb, mb = int(rng.integers(lo, hi + 1)), int(rng.integers(lo, hi + 1))
+        while mb == nb:
+            mb = int(rng.integers(lo, hi + 1))
+        sizes.append((nb, mb))
+    pairs = [clouds.pair(c["kind"], nb, mb, args.seed, b) for b, (nb, mb) in enumerate(sizes)]
+    def step():
+        for xb, yb in pairs:
+            SparsePlan(xb, yb, OracleConfig()).backward()
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    val = len(pairs) * args.steps / el
+    out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "pairs/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": c["workload"], "B": c["B"], "kind": c["kind"],
+                                           "step_sample_pairs": len(pairs)},
+           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": 1, "kind": "oracle",
+                            "sample": f"{len(pairs)} ragged pairs of {args.config} per step, fwd+full bwd, fp64"},
+           "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
 def run_reference(args) -> None:
     """--impl reference: the oracle timed on the host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -130,6 +168,9 @@ def run_reference(args) -> None:
     from oracle import OracleConfig, batch as oracle_batch
     from synth import clouds
     c = CONFIGS[args.config]
+    if "ragged" in c:
+        _ragged_reference(args, c)
+        return
     cores = os.cpu_count() or 1
     n = max(1, min(c["B"], cores))
     sN, sM, scale = _oracle_sample(c)
@@ -198,7 +239,22 @@ def main():
         x = np.ascontiguousarray(x[:, r0:r1])
         comm = Collectives(device=dev)
     else:
-        x, y = clouds.batch(c["kind"], B, N, M, args.seed + 1000 * rank)
+        x, y = clouds.batch(c["kind"], B, N, M, args.seed + 1000 * rank) if "ragged" not in c else (None, None)
+    ns = ms = None
+    if "ragged" in c:  # per-pair sizes (seeded), clouds padded to N, M (apml_forward_ragged)
+        lo, hi = c["ragged"]
+        rng = np.random.default_rng(args.seed + 1000 * rank)
+        ns, ms = [], []
+        x = np.zeros((B, N, 3), np.float32)
+        y = np.zeros((B, M, 3), np.float32)
+        for b in range(B):
+            nb, mb = int(rng.integers(lo, hi + 1)), int(rng.integers(lo, hi + 1))
+            while mb == nb:
+                mb = int(rng.integers(lo, hi + 1))
+            xb, yb = clouds.pair(c["kind"], nb, mb, args.seed + 1000 * rank, b)
+            x[b, :nb], y[b, :mb] = xb, yb
+            ns.append(nb)
+            ms.append(mb)
     pred = torch.tensor(x, device=dev)
     gt = torch.tensor(y, device=dev)
     ones = torch.ones(B, device=dev)
@@ -212,7 +268,7 @@ def main():
             loss, ctx = forward_rowsharded(pred, gt, r0, N, cfg, comm, loss_out=loss_buf)
             ctx.backward(ones, out=grad_buf)
             return ctx
-        loss, ctx = forward(pred, gt, cfg, loss_out=loss_buf)
+        loss, ctx = forward(pred, gt, cfg, loss_out=loss_buf, n_sizes=ns, m_sizes=ms)
         ctx.backward(ones, out=grad_buf)
         if world > 1:
             sharded_reduce(loss)  # X1: NCCL all-reduce of the loss (batch sharding)
@@ -272,7 +328,7 @@ def main():
     # algorithmic (i, j) evaluations per sweep on this rank: B N M for the full sweeps; the
     # spatially culled sweeps (C4, C5) count on the device the 32 x 32 blocks they evaluate
     # (apml_stats.sweep_evals), capped at B N M
-    full_evals = B * pred.shape[1] * M
+    full_evals = B * pred.shape[1] * M if ns is None else int(sum(a * b for a, b in zip(ns, ms)))
     evals_by = {k: min(int(e), full_evals) for k, e in zip(dist_stages, st0["sweep_evals"])}
     culled = any(e < full_evals for e in evals_by.values())
     nnz = st0["nnz_total"]
@@ -310,7 +366,7 @@ def main():
 
     # end to end through the host entry point (pinned host buffers; copies inside the bracket)
     e2e = None
-    if not args.no_e2e and not rowshard:
+    if not args.no_e2e and not rowshard and ns is None:
         ph = torch.tensor(x).pin_memory()
         gh = torch.tensor(y).pin_memory()
         lo = torch.empty(B, pin_memory=True)
@@ -336,7 +392,7 @@ def main():
                "api": "apml_loss_grad_host (host fp32 in, host loss + grad out)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and ns is None:
         cpu = cpu_baseline(args.config, args.seed)
 
     if world > 1:
@@ -347,6 +403,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if rowshard else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": c["workload"], "B": B, "N": N, "M": M, "kind": c["kind"], "tau": cfg.tau,
+                       **({} if ns is None else {"ragged_mean_N": float(np.mean(ns)), "ragged_mean_M": float(np.mean(ms))}),
                        "l_iter": cfg.l_iter, "p_min": cfg.p_min, "grad_mode": args.grad_mode,
                        "global_batch": pairs_per_step,
                        "parallelism": (f"row-shard x{world} (NCCL all-gather + per-iteration column-sum all-reduce)"

@@ -556,10 +556,10 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 1, s);
   // S1 Pass A: rows (own pred, stream gt) and columns (own gt, stream pred)
   k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
+      c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r, c->nb_d, c->mb_d);
   mark(c, 2, s);
   k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
-      c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
+      c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c, c->mb_d, c->nb_d);
   mark(c, 3, s);
   // S2 line constants
   k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
@@ -635,10 +635,10 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
     k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4, nullptr);
     mark(c, 1, s);
     k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-        c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r);
+        c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r, c->nb_d, c->mb_d);
     mark(c, 2, s);
     k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
-        c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c);
+        c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c, c->mb_d, c->nb_d);
     k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, c->colpart);
   }
   CK(cudaGetLastError());

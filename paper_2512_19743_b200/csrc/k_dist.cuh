@@ -61,8 +61,13 @@ __device__ __forceinline__ void load_tile(const float* __restrict__ str, int str
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restrict__ str_soa,
-            int str_np, int chunk, int B, float2* __restrict__ part) {
+            int str_np, int chunk, int B, float2* __restrict__ part, const int* __restrict__ nown,
+            const int* __restrict__ nstr) {
   const int b = blockIdx.z, split = blockIdx.y;
+  // ragged batches: blocks of padding rows have no line to serve (k_line_info ignores their
+  // partials); streamed tiles past the pair's real points hold only sentinels
+  if (nown && (int)(blockIdx.x * kSweepThreads * R) >= nown[b]) return;
+  const int str_end = nstr ? min(str_np, (nstr[b] + kTQ - 1) / kTQ * kTQ) : str_np;
   const float* own = own_soa + (size_t)b * 3 * own_np;
   const float* str = str_soa + (size_t)b * 3 * str_np;
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
@@ -80,7 +85,7 @@ k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restri
     m[r] = __int_as_float(0x7f800000); s[r] = m[r];
     m2[r] = m[r]; s2[r] = m[r];
   }
-  const int j0 = split * chunk, j1 = min(str_np, j0 + chunk);
+  const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
   for (int jt = j0; jt < j1; jt += kTQ) {
     __syncthreads();
     load_tile(str, str_np, jt, sx, sy, sz);
@@ -239,6 +244,8 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
        unsigned* __restrict__ col_cnt, const int* __restrict__ nb, const int* __restrict__ mb) {
   const int b = blockIdx.z, split = blockIdx.y;
   const uint32_t nreal = nb ? (uint32_t)nb[b] : (uint32_t)N, mreal = mb ? (uint32_t)mb[b] : (uint32_t)M;
+  if ((uint32_t)(blockIdx.x * kSweepThreads * R) >= nreal) return;  // a block of padding rows
+  const int str_end = min(mp, (int)((mreal + kTQ - 1) / kTQ * kTQ));
   const float* own = pred_soa + (size_t)b * 3 * np;
   const float* str = gt_soa + (size_t)b * 3 * mp;
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
@@ -262,7 +269,7 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
       rR2[r] = -1.f; rE2[r] = -1.f;
     }
   }
-  const int j0 = split * chunk, j1 = min(mp, j0 + chunk);
+  const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
   for (int jt = j0; jt < j1; jt += kTQ) {
     __syncthreads();
     load_tile(str, mp, jt, sx, sy, sz);
