@@ -331,6 +331,9 @@ def main():
     full_evals = B * pred.shape[1] * M if ns is None else int(sum(a * b for a, b in zip(ns, ms)))
     evals_by = {k: min(int(e), full_evals) for k, e in zip(dist_stages, st0["sweep_evals"])}
     culled = any(e < full_evals for e in evals_by.values())
+    if med.get("passA_cols", 0.0) == 0.0:  # both Pass A directions in one launch (full sweeps)
+        evals_by["passA_rows"] += evals_by["passA_cols"]
+        evals_by["passA_cols"] = 0
     nnz = st0["nnz_total"]
     L = cfg.l_iter
     sparse_bytes = {  # algorithmic bytes per launch (SURVEY 8(d) per-entry totals x nnz)

@@ -84,7 +84,8 @@ typedef enum {
 enum {
     APML_STAGE_STAGING = 0,     /* S0: AoS -> padded SoA + float4 copies */
     APML_STAGE_PASSA_ROWS = 1,  /* S1: row min / second min sweep (k_line_top2, B N M pairs) */
-    APML_STAGE_PASSA_COLS = 2,  /* S1: column min / second min sweep (k_line_top2, B N M pairs) */
+    APML_STAGE_PASSA_COLS = 2,  /* S1: column min / second min sweep (k_line_top2, B N M pairs);
+                                   0 when both directions ran in one launch (counted under ROWS) */
     APML_STAGE_LINE_INFO = 3,   /* S2: line constants */
     APML_STAGE_EMIT = 4,        /* S3: emit sweep (k_emit, B N M pairs) */
     APML_STAGE_SPARSE_FWD = 5,  /* S4-S7: CSR/CSC, normalisation, Sinkhorn, loss (k_sparse_fwd) */

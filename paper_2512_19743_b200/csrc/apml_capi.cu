@@ -88,6 +88,7 @@ struct apml_ctx {
   int rep_smem = 0;       // scaling-vector replicas in shared memory
   size_t smem_bytes = 0;  // dynamic shared memory of k_sparse_fwd / k_sparse_bwd
   bool fwd2 = false;      // sparse forward built in shared memory (k_fwd2.cuh)
+  bool passA_fused = false;  // both Pass A directions in one launch (k_line_top2_both)
   float* grad_gt = nullptr;  // set by apml_backward_ex for the duration of the call
   // ragged batches (apml_forward_ragged): per-pair real sizes and Eq. (1) constants
   bool ragged = false;
@@ -555,11 +556,17 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4, c->mb_d);
   mark(c, 1, s);
   // S1 Pass A: rows (own pred, stream gt) and columns (own gt, stream pred)
-  k_line_top2<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, c->gtS, Mp, c->chunk_rows, B, c->part_r, c->nb_d, c->mb_d);
+  // (rows and columns in one launch; the stage marks 2 and 3 bracket it together)
+  {
+    const Top2Dir dr{c->predS, (int)Np, c->gtS, (int)Mp, c->chunk_rows, c->S_rows, (int)(Np / kOwnTile),
+                     c->part_r, c->nb_d, c->mb_d};
+    const Top2Dir dc{c->gtS, (int)Mp, c->predS, (int)Np, c->chunk_cols, c->S_cols, (int)(Mp / kOwnTile),
+                     c->part_c, c->mb_d, c->nb_d};
+    k_line_top2_both<kR><<<dim3(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B),
+                           kSweepThreads, 0, s>>>(dr, dc, B);
+  }
+  c->passA_fused = true;
   mark(c, 2, s);
-  k_line_top2<kR><<<dim3(Mp / kOwnTile, c->S_cols, B), kSweepThreads, 0, s>>>(
-      c->gtS, Mp, c->predS, Np, c->chunk_cols, B, c->part_c, c->mb_d, c->nb_d);
   mark(c, 3, s);
   // S2 line constants
   k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
@@ -572,7 +579,7 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
       c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
       c->aux, c->row_cnt, c->col_cnt, c->nb_d, c->mb_d);
   mark(c, 5, s);
-  c->launches += 7;
+  c->launches += 6;
   CK(cudaGetLastError());
   return APML_OK;
 }
@@ -1120,6 +1127,10 @@ apml_status apml_ctx_stage_times(const apml_ctx* x, float* ms, int32_t n) {
   for (int k = 0; k < APML_NUM_STAGES; ++k) ms[k] = 0.f;
   CK(cudaEventSynchronize(x->ev[x->bwd_timed ? 8 : 6]));
   for (int k = 0; k < 6; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k], x->ev[k + 1]));
+  if (x->passA_fused) {  // one launch for both Pass A directions: reported as the rows stage
+    CK(cudaEventElapsedTime(&ms[APML_STAGE_PASSA_ROWS], x->ev[1], x->ev[3]));
+    ms[APML_STAGE_PASSA_COLS] = 0.f;
+  }
   if (x->bwd_timed) CK(cudaEventElapsedTime(&ms[APML_STAGE_SPARSE_BWD], x->ev[7], x->ev[8]));
   return APML_OK;
 }

@@ -58,19 +58,20 @@ __device__ __forceinline__ void load_tile(const float* __restrict__ str, int str
   }
 }
 
+// One direction of Pass A (own points in registers, the other cloud streamed): block bx of
+// the own points, column split `split`, pair b.
 template <int R>
-__global__ void __launch_bounds__(kSweepThreads)
-k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restrict__ str_soa,
-            int str_np, int chunk, int B, float2* __restrict__ part, const int* __restrict__ nown,
-            const int* __restrict__ nstr) {
-  const int b = blockIdx.z, split = blockIdx.y;
+__device__ __forceinline__ void top2_block(const float* __restrict__ own_soa, int own_np,
+                                           const float* __restrict__ str_soa, int str_np, int chunk, int B,
+                                           float2* __restrict__ part, const int* __restrict__ nown,
+                                           const int* __restrict__ nstr, int bx, int split, int b) {
   // ragged batches: blocks of padding rows have no line to serve (k_line_info ignores their
   // partials); streamed tiles past the pair's real points hold only sentinels
-  if (nown && (int)(blockIdx.x * kSweepThreads * R) >= nown[b]) return;
+  if (nown && (int)(bx * kSweepThreads * R) >= nown[b]) return;
   const int str_end = nstr ? min(str_np, (nstr[b] + kTQ - 1) / kTQ * kTQ) : str_np;
   const float* own = own_soa + (size_t)b * 3 * own_np;
   const float* str = str_soa + (size_t)b * 3 * str_np;
-  const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
+  const int base = bx * kSweepThreads * R + threadIdx.x;
   __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ];
 
   f2_t nx[R], ny[R], nz[R];
@@ -114,6 +115,34 @@ k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restri
     top2_merge(m[r], s[r], m2[r], s2[r]);
     out[base + r * kSweepThreads] = make_float2(m[r], s[r]);
   }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads)
+k_line_top2(const float* __restrict__ own_soa, int own_np, const float* __restrict__ str_soa,
+            int str_np, int chunk, int B, float2* __restrict__ part, const int* __restrict__ nown,
+            const int* __restrict__ nstr) {
+  top2_block<R>(own_soa, own_np, str_soa, str_np, chunk, B, part, nown, nstr, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// Both directions of Pass A in ONE launch (grid.z = 2 B: rows, then columns): the two sweeps
+// share the waves, so neither pays a partly empty last wave (and one launch gap less).
+struct Top2Dir {
+  const float* own;
+  int own_np;
+  const float* str;
+  int str_np, chunk, S, nblk;
+  float2* part;
+  const int* nown;
+  const int* nstr;
+};
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads) k_line_top2_both(const Top2Dir d0, const Top2Dir d1, int B) {
+  const int dir = blockIdx.z >= (unsigned)B;
+  const Top2Dir& d = dir ? d1 : d0;
+  if ((int)blockIdx.x >= d.nblk || (int)blockIdx.y >= d.S) return;
+  top2_block<R>(d.own, d.own_np, d.str, d.str_np, d.chunk, B, d.part, d.nown, d.nstr, blockIdx.x, blockIdx.y,
+                blockIdx.z - dir * B);
 }
 
 // S2: one thread per line.  lam = Lambda_K (fp64 on the host, rounded), rho = ln(1/tau) /
