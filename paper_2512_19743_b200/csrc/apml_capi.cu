@@ -77,6 +77,7 @@ struct apml_ctx {
   size_t bytes = 0;
   uint32_t cap = 0;
   int S_rows = 1, S_cols = 1, chunk_rows = 0, chunk_cols = 0;
+  int S_emit = 1, chunk_emit = 0;  // column split of the emit sweep (its own wave target)
   bool backward_done = false;
   bool timing = false;
   bool bwd_timed = false;
@@ -205,9 +206,10 @@ long env_long(const char* name, long dflt) {
   return (e && *e) ? strtol(e, nullptr, 10) : dflt;
 }
 
-void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk) {
+void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk, int64_t target_div = 1) {
   const int64_t blocks = own_np / kOwnTile * B;
-  const int64_t target = env_long("APML_SPLIT_TARGET", 4LL * num_sms() * 4);  // ~4 waves of 4 CTAs / SM
+  // ~4 waves of 4 CTAs / SM (target_div = 2: the two Pass A directions share one launch)
+  const int64_t target = env_long("APML_SPLIT_TARGET", 4LL * num_sms() * 4) / target_div;
   int64_t s = (target + blocks - 1) / blocks;
   const int64_t tiles = str_np / kTQ;
   if (s > tiles) s = tiles;
@@ -278,8 +280,13 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
     while ((1LL << lg) < std::max(N, M)) ++lg;
     c->cell_bits = std::min(7, std::max(2, (lg + 2) / 3));
   }
-  plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows);
-  plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols);
+  // full sweeps: Pass A rows + columns share one launch (half the target each; fewer partials
+  // for k_line_info to merge); the emit sweep keeps the full target.  The row-sharded mode
+  // launches the Pass A directions separately.
+  const int64_t pa_div = c->rs ? 1 : 2;
+  plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows, pa_div);
+  plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols, pa_div);
+  plan_split(c->Np, c->Mp, B, &c->S_emit, &c->chunk_emit);
   plan_sparse(c);
   Carve k;
   const int64_t E = B * (int64_t)cap;
@@ -575,8 +582,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
       c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
   mark(c, 4, s);
   // S3 Pass B emit
-  k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
+  k_emit<kR><<<dim3(Np / kOwnTile, c->S_emit, B), kSweepThreads, 0, s>>>(
+      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_emit, c->cap, c->ebuf, c->cursor,
       c->aux, c->row_cnt, c->col_cnt, c->nb_d, c->mb_d);
   mark(c, 5, s);
   c->launches += 6;

@@ -170,9 +170,14 @@ __global__ void k_line_info(const float2* __restrict__ part, int S, int B, int o
     rho = lr[4 * b + lr_off + 1];
   }
   float m2 = __int_as_float(0x7f800000), s2 = m2;
-  for (int sp = 0; sp < S; ++sp) {
-    const float2 p = part[((size_t)sp * B + b) * own_np + k];
-    top2_merge(m2, s2, p.x, p.y);
+  for (int sp0 = 0; sp0 < S; sp0 += 8) {  // 8 partials in flight per step
+    float2 p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      p[u] = sp0 + u < S ? part[((size_t)(sp0 + u) * B + b) * own_np + k]
+                         : make_float2(__int_as_float(0x7f800000), __int_as_float(0x7f800000));
+#pragma unroll
+    for (int u = 0; u < 8; ++u) top2_merge(m2, s2, p[u].x, p[u].y);
   }
   LineA a;
   LineB o;
