@@ -559,8 +559,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     return APML_OK;
   }
   // S0 staging
-  k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4, c->nb_d);
-  k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4, c->mb_d);
+  k_stage_both<<<dim3((std::max(Np, Mp) + 255) / 256, 1, 2 * B), 256, 0, s>>>(
+      pred, N, Np, c->predS, c->pred4, c->nb_d, gt, M, Mp, c->gtS, c->gt4, c->mb_d, B);
   mark(c, 1, s);
   // S1 Pass A: rows (own pred, stream gt) and columns (own gt, stream pred)
   // (rows and columns in one launch; the stage marks 2 and 3 bracket it together)
@@ -575,18 +575,20 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   c->passA_fused = true;
   mark(c, 2, s);
   mark(c, 3, s);
-  // S2 line constants
-  k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
-      c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
-  k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, N, c->lam_c,
-      c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
+  // S2 line constants (rows and columns in one launch)
+  {
+    const LineInfoDir lr_{c->part_r, c->S_rows, (int)Np, N, M, c->lam_r, c->rho_r, c->rowA, c->rowB, c->nb_d, c->mb_d, 0};
+    const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2};
+    k_line_info_both<<<dim3((std::max(N, M) + 255) / 256, B, 2), 256, 0, s>>>(lr_, lc_, B, c->cfg.delta, c->cfg.eps_g,
+                                                                             c->clamp, c->lr_d);
+  }
   mark(c, 4, s);
   // S3 Pass B emit
   k_emit<kR><<<dim3(Np / kOwnTile, c->S_emit, B), kSweepThreads, 0, s>>>(
       c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_emit, c->cap, c->ebuf, c->cursor,
       c->aux, c->row_cnt, c->col_cnt, c->nb_d, c->mb_d);
   mark(c, 5, s);
-  c->launches += 6;
+  c->launches += 4;
   CK(cudaGetLastError());
   return APML_OK;
 }

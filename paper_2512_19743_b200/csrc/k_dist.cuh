@@ -30,6 +30,31 @@ constexpr int kTQ = 128;  // streamed points per shared-memory tile
 
 // nb (ragged batches, else NULL): pair b has nb[b] <= n real points; the rest of its n slots
 // are staged as sentinels (never a minimum, never emitted).
+__device__ __forceinline__ void stage_point(const float* __restrict__ pts, int n, int np, float sentinel,
+                                            float* __restrict__ soa, float4* __restrict__ p4,
+                                            const int* __restrict__ nb, int b, int k) {
+  if (k >= np) return;
+  float x = sentinel, y = sentinel, z = sentinel;
+  if (k < n) {
+    if (!nb || k < nb[b]) {
+      const float* p = pts + ((size_t)b * n + k) * 3;
+      x = p[0]; y = p[1]; z = p[2];
+    }
+    p4[(size_t)b * n + k] = make_float4(x, y, z, 0.f);
+  }
+  float* s = soa + (size_t)b * 3 * np;
+  s[k] = x; s[np + k] = y; s[2 * np + k] = z;
+}
+// pred and gt of every pair in ONE launch (grid.z = 2 B: pred, then gt)
+__global__ void k_stage_both(const float* __restrict__ pred, int N, int Np, float* __restrict__ predS,
+                             float4* __restrict__ pred4, const int* __restrict__ nb, const float* __restrict__ gt,
+                             int M, int Mp, float* __restrict__ gtS, float4* __restrict__ gt4,
+                             const int* __restrict__ mb, int B) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)blockIdx.z < B) stage_point(pred, N, Np, kPadPred, predS, pred4, nb, blockIdx.z, k);
+  else stage_point(gt, M, Mp, kPadGt, gtS, gt4, mb, blockIdx.z - B, k);
+}
+
 __global__ void k_stage(const float* __restrict__ pts, int n, int np, float sentinel,
                         float* __restrict__ soa, float4* __restrict__ p4, const int* __restrict__ nb) {
   const int b = blockIdx.y;
@@ -150,13 +175,12 @@ __global__ void __launch_bounds__(kSweepThreads) k_line_top2_both(const Top2Dir 
 // Ragged batches (nown != NULL): pair b has nown[b] real lines of length K = kpair[b], with
 // lam / rho = lr[4 b + lr_off], lr[4 b + lr_off + 1]; the padding lines are inactive (radii
 // -1: nothing emitted; no entries downstream).
-__global__ void k_line_info(const float2* __restrict__ part, int S, int B, int own_np, int n,
-                            int K, float lam, float rho, float delta, float eps_g,
-                            LineA* __restrict__ A, LineB* __restrict__ Bo,
-                            unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
-                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off) {
-  const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void line_info(const float2* __restrict__ part, int S, int B, int own_np, int n,
+                                          int K, float lam, float rho, float delta, float eps_g,
+                                          LineA* __restrict__ A, LineB* __restrict__ Bo,
+                                          unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
+                                          const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off,
+                                          int b, int k) {
   if (k >= n) return;
   if (nown) {
     if (k >= nown[b]) {
@@ -199,6 +223,33 @@ __global__ void k_line_info(const float2* __restrict__ part, int S, int B, int o
   }
   A[(size_t)b * n + k] = a;
   Bo[(size_t)b * n + k] = o;
+}
+
+__global__ void k_line_info(const float2* __restrict__ part, int S, int B, int own_np, int n,
+                            int K, float lam, float rho, float delta, float eps_g,
+                            LineA* __restrict__ A, LineB* __restrict__ Bo,
+                            unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
+                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off) {
+  line_info(part, S, B, own_np, n, K, lam, rho, delta, eps_g, A, Bo, clamp_count, nown, kpair, lr, lr_off,
+            blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
+}
+
+// Rows and columns in ONE launch (grid.z = 2: rows, columns; grid.y = pair).
+struct LineInfoDir {
+  const float2* part;
+  int S, own_np, n, K;
+  float lam, rho;
+  LineA* A;
+  LineB* Bo;
+  const int* nown;
+  const int* kpair;
+  int lr_off;
+};
+__global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int B, float delta, float eps_g,
+                                 unsigned long long* __restrict__ clamp_count, const float* __restrict__ lr) {
+  const LineInfoDir& d = blockIdx.z ? d1 : d0;
+  line_info(d.part, d.S, B, d.own_np, d.n, d.K, d.lam, d.rho, delta, eps_g, d.A, d.Bo, clamp_count, d.nown,
+            d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // Emission staging: each warp compacts its hits into a shared-memory buffer (ballot +
