@@ -203,9 +203,11 @@ def apml_loss(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
 
 def loss_grad_host(pred_host: torch.Tensor, gt_host: torch.Tensor, cfg: Config | None = None,
                    loss_out: torch.Tensor | None = None, grad_out: torch.Tensor | None = None,
-                   device: int | None = None):
+                   device: int | None = None, torch_allocator: bool = False):
     """apml_loss_grad_host: host fp32 buffers in, host loss [B] and grad [B,N,3] out (sum
-    reduction), host<->device copies included.  Pinned inputs give async copies."""
+    reduction), host<->device copies included.  Pinned inputs give async copies.  The library's
+    device workspace comes from the CUDA stream-ordered pool (no Python callbacks inside the
+    call) unless torch_allocator=True."""
     cfg = cfg or Config()
     for t, n in ((pred_host, "pred"), (gt_host, "gt")):
         if t.is_cuda or t.dtype != torch.float32 or t.dim() != 3 or not t.is_contiguous():
@@ -218,6 +220,6 @@ def loss_grad_host(pred_host: torch.Tensor, gt_host: torch.Tensor, cfg: Config |
     with torch.cuda.device(dev):
         s = torch.cuda.current_stream().cuda_stream
         A.check(A.lib().apml_loss_grad_host(pred_host.data_ptr(), gt_host.data_ptr(), B, N, M,
-                                            C.byref(c), C.byref(_ALLOC), s, loss.data_ptr(),
-                                            grad.data_ptr()))
+                                            C.byref(c), C.byref(_ALLOC) if torch_allocator else None, s,
+                                            loss.data_ptr(), grad.data_ptr()))
     return loss, grad

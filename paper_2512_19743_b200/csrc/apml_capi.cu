@@ -143,8 +143,29 @@ void mark(apml_ctx* c, int k, cudaStream_t s) {
   if (c->timing) cudaEventRecord(c->ev[k], s);
 }
 
+__global__ void k_fill(float* p, int n, float v) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) p[k] = v;
+}
+
+// Library-owned memory without a caller allocator: the device's default stream-ordered pool,
+// told once per device to keep freed blocks (release threshold = max) so that a call per
+// training step does not map and unmap its workspace every time.
+void keep_default_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 void* ctx_alloc(apml_ctx* c, size_t bytes) {
   if (c->has_alloc) return c->alloc.alloc(bytes, c->stream, c->alloc.user);
+  keep_default_pool();
   void* p = nullptr;
   if (cudaMallocAsync(&p, bytes, c->stream) != cudaSuccess) return nullptr;
   return p;
@@ -1174,10 +1195,12 @@ apml_status apml_loss_grad_host(const float* pred_host, const float* gt_host, in
   float* d_grad = d_gl + round_up(B, 64);
   apml_status st = APML_OK;
   apml_ctx* ctx = nullptr;
-  std::vector<float> ones((size_t)B, 1.f);
   cudaError_t e = cudaMemcpyAsync(d_pred, pred_host, bp, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d_gt, gt_host, bg, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d_gl, ones.data(), bl, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {  // d loss_sum / d loss_b = 1 (no pageable host copy)
+    k_fill<<<(unsigned)((B + 255) / 256), 256, 0, s>>>(d_gl, (int)B, 1.f);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess) st = fail(APML_ERR_CUDA, cudaGetErrorString(e));
   if (st == APML_OK) st = apml_forward(d_pred, d_gt, B, N, M, cfg, alloc, stream, d_loss, &ctx);
   if (st == APML_OK) st = apml_backward(ctx, d_gl, d_grad, stream);
