@@ -208,6 +208,21 @@ APML_API apml_status apml_backward(apml_ctx* ctx, const float* grad_loss, float*
 APML_API apml_status apml_backward_ex(apml_ctx* ctx, const float* grad_loss, float* grad_pred, float* grad_gt,
                                       void* stream);
 
+/* Reusable plans (CUDA-graph capturable steps).  apml_plan_create allocates, once, every
+ * device buffer of a B x N x M problem (emit capacity = cfg->capacity x (N + M) entries per
+ * pair) and returns a context; apml_plan_forward then runs the forward on new pred / gt with
+ * NO allocation, NO host synchronisation and NO host read (APML_FLAG_SYNC_CHECK and
+ * APML_FLAG_CHECK_FINITE are ignored), so a training step `apml_plan_forward +
+ * apml_backward[_ex]` can be captured into a CUDA graph and replayed.  A pair whose support
+ * exceeds the capacity gets a NaN loss / gradient (apml_ctx_stats reports it).  Each
+ * apml_plan_forward allows one backward; the introspection calls read the last forward.
+ * Destroy with apml_ctx_destroy.  Errors: as apml_forward; APML_ERR_STATE for a context that
+ * is not a plan. */
+APML_API apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config* cfg,
+                                      const apml_allocator* alloc, void* stream, apml_ctx** plan_out);
+APML_API apml_status apml_plan_forward(apml_ctx* plan, const float* pred, const float* gt, void* stream,
+                                       float* loss);
+
 /* Diagnostics; SYNCHRONISES the context's stream.  nnz_per_pair: host [B] or NULL. */
 APML_API apml_status apml_ctx_stats(const apml_ctx* ctx, int64_t* nnz_per_pair, apml_stats* out);
 

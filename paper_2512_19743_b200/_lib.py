@@ -22,7 +22,7 @@ STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "sparse_fw
 # exported symbols declared in include/apml.h (checked by tests/test_abi.py)
 EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forward_ragged",
            "apml_forward_rowsharded",
-           "apml_backward", "apml_backward_ex",
+           "apml_backward", "apml_backward_ex", "apml_plan_create", "apml_plan_forward",
            "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
            "apml_ctx_destroy",
            "apml_loss_grad_host", "apml_last_error")
@@ -92,6 +92,11 @@ def lib() -> C.CDLL:
                                               C.POINTER(vp)]
         L.apml_backward.restype = C.c_int
         L.apml_backward.argtypes = [vp, vp, vp, vp]
+        L.apml_plan_create.restype = C.c_int
+        L.apml_plan_create.argtypes = [i64, i64, i64, C.POINTER(ApmlConfig), C.POINTER(ApmlAllocator), vp,
+                                       C.POINTER(vp)]
+        L.apml_plan_forward.restype = C.c_int
+        L.apml_plan_forward.argtypes = [vp, vp, vp, vp, vp]
         L.apml_backward_ex.restype = C.c_int
         L.apml_backward_ex.argtypes = [vp, vp, vp, vp, vp]
         L.apml_ctx_stats.restype = C.c_int

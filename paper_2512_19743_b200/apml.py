@@ -169,6 +169,32 @@ def forward(pred: torch.Tensor, gt: torch.Tensor, cfg: Config | None = None,
     return loss, ctx
 
 
+class Plan(Context):
+    """A reusable forward/backward plan (apml_plan_create): all device memory allocated once,
+    every forward sync-free and allocation-free, so `plan.forward` + `plan.backward` can be
+    captured into a torch.cuda.CUDAGraph and replayed (static input / output tensors)."""
+
+    def __init__(self, B: int, N: int, M: int, cfg: Config | None = None, device=None):
+        cfg = cfg or Config()
+        device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        h = C.c_void_p()
+        c = cfg.to_c()
+        with torch.cuda.device(device):
+            s = torch.cuda.current_stream(device).cuda_stream
+            A.check(A.lib().apml_plan_create(B, N, M, C.byref(c), C.byref(_ALLOC), s, C.byref(h)))
+        super().__init__(h.value, B, N, M, device)
+
+    def forward(self, pred: torch.Tensor, gt: torch.Tensor, loss_out: torch.Tensor | None = None) -> torch.Tensor:
+        pred = _check_points(pred, "pred")
+        gt = _check_points(gt, "gt")
+        if tuple(pred.shape) != (self.B, self.N, 3) or tuple(gt.shape) != (self.B, self.M, 3):
+            raise ValueError("pred / gt shapes differ from the plan's")
+        loss = loss_out if loss_out is not None else torch.empty(self.B, device=self.device, dtype=torch.float32)
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        A.check(A.lib().apml_plan_forward(self._h, pred.data_ptr(), gt.data_ptr(), s, loss.data_ptr()))
+        return loss
+
+
 class _APMLFunction(torch.autograd.Function):
     @staticmethod
     def forward(fctx, pred, gt, cfg, n_sizes=None, m_sizes=None):

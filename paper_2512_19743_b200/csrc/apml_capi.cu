@@ -79,6 +79,9 @@ struct apml_ctx {
   int S_rows = 1, S_cols = 1, chunk_rows = 0, chunk_cols = 0;
   int S_emit = 1, chunk_emit = 0;  // column split of the emit sweep (its own wave target)
   bool backward_done = false;
+  bool plan = false;            // created by apml_plan_create: reusable, no per-call allocation
+  bool forward_done = false;    // a plan has run at least one forward
+  size_t zero_off = 0, zero_bytes = 0;  // the counters block zeroed before every forward
   bool timing = false;
   bool bwd_timed = false;
   cudaEvent_t ev[9] = {};  // 0..6 forward stage boundaries, 7 backward start, 8 backward end
@@ -139,8 +142,14 @@ struct apml_ctx {
 
 namespace {
 
+// Stage events.  Under CUDA-graph capture they become event-record nodes (External flag), so
+// every replay re-records them and apml_ctx_stage_times reads the last replay.
 void mark(apml_ctx* c, int k, cudaStream_t s) {
-  if (c->timing) cudaEventRecord(c->ev[k], s);
+  if (!c->timing) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(c->ev[k], s, cudaEventRecordExternal);
+  else cudaEventRecord(c->ev[k], s);
 }
 
 __global__ void k_fill(float* p, int n, float v) {
@@ -397,6 +406,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
   c->pstart = (uint32_t*)(p + o_pstart); c->gstart = (uint32_t*)(p + o_gstart);
   c->pperm = (int*)(p + o_pperm); c->gperm = (int*)(p + o_gperm);
+  c->zero_off = z0;
+  c->zero_bytes = z1 - z0;
   CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
   return APML_OK;
 }
@@ -992,6 +1003,7 @@ apml_status apml_backward_ex(apml_ctx* x, const float* grad_loss, float* grad_pr
   x->grad_gt = grad_gt;
   struct Reset { apml_ctx* c; ~Reset() { c->grad_gt = nullptr; } } reset{x};
   if (x->backward_done) return fail(APML_ERR_STATE, "backward already ran on this context");
+  if (x->plan && !x->forward_done) return fail(APML_ERR_STATE, "plan: apml_plan_forward has not run");
   if (!grad_loss || !grad_pred) return fail(APML_ERR_INVALID_ARG, "grad_loss / grad_pred must be non-NULL");
   cudaStream_t s = stream ? (cudaStream_t)stream : x->stream;
   if (s != x->stream) {  // order after the forward's stream
@@ -1169,6 +1181,63 @@ void apml_ctx_destroy(apml_ctx* x) {
   if (!x) return;
   ctx_free(x);
   delete x;
+}
+
+apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config* cfg,
+                             const apml_allocator* alloc, void* stream, apml_ctx** plan_out) {
+  if (!plan_out) return fail(APML_ERR_INVALID_ARG, "plan_out must be non-NULL");
+  *plan_out = nullptr;
+  apml_config c;
+  if (cfg) c = *cfg; else apml_config_default(&c);
+  static const float kDummy[1] = {0.f};  // validate() wants non-NULL inputs; none are read here
+  apml_status st = validate(kDummy, kDummy, B, N, M, c);
+  if (st != APML_OK) return st;
+  if (alloc && (!alloc->alloc || !alloc->free)) return fail(APML_ERR_INVALID_ARG, "allocator needs alloc and free");
+  const int64_t per = c.capacity > 0 ? c.capacity : 6;
+  int64_t cap64 = per * (N + M);
+  if (cap64 > N * M) cap64 = N * M;
+  if (cap64 < 1) cap64 = 1;
+  if (cap64 * B > (int64_t)1 << 40 || cap64 >= ((int64_t)1 << 32))
+    return fail(APML_ERR_SHAPE, "emit capacity exceeds 32-bit per-pair positions");
+  apml_ctx* x = new apml_ctx();
+  x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = (cudaStream_t)stream;
+  x->plan = true;
+  if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
+  if (c.flags & APML_FLAG_STAGE_TIMING) {
+    x->timing = true;
+    for (auto& e : x->ev)
+      if (cudaEventCreate(&e) != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, "cudaEventCreate"); }
+  }
+  const double p = c.p_min;
+  x->lam_r = (float)lambda_K(M, p);
+  x->lam_c = (float)lambda_K(N, p);
+  const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;
+  x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
+  x->rho_c = N > 1 ? (float)(lt / lambda_K(N, p)) : INFINITY;
+  if (use_grid_path(x)) {
+    x->rs = true;
+    x->comm = apml_comm{0, 1, local_allreduce, local_allgather, nullptr};
+    x->row_offset = 0;
+    x->N_global = N;
+  }
+  if ((st = build_ctx(x, (uint32_t)cap64)) != APML_OK) { apml_ctx_destroy(x); return st; }
+  *plan_out = x;
+  return APML_OK;
+}
+
+apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, void* stream, float* loss) {
+  if (!x || !x->plan) return fail(APML_ERR_STATE, "not a plan (apml_plan_create)");
+  if (!pred || !gt || !loss) return fail(APML_ERR_INVALID_ARG, "pred / gt / loss must be non-NULL device pointers");
+  if (stream) x->stream = (cudaStream_t)stream;
+  // per-call state: counters zeroed on the stream (capturable), one backward allowed again
+  CK(cudaMemsetAsync(static_cast<char*>(x->base) + x->zero_off, 0, x->zero_bytes, x->stream));
+  x->backward_done = false;
+  x->bwd_timed = false;
+  x->grad_gt = nullptr;
+  apml_status st = x->rs ? launch_forward_rs(x, pred, gt) : launch_forward(x, pred, gt);
+  if (st == APML_OK) st = x->rs ? launch_sparse_fwd_rs(x, loss) : launch_sparse_fwd(x, loss);
+  if (st == APML_OK) x->forward_done = true;
+  return st;
 }
 
 apml_status apml_loss_grad_host(const float* pred_host, const float* gt_host, int64_t B,

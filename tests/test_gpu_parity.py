@@ -407,3 +407,61 @@ def test_ragged_rejects_bad_sizes():
         with pytest.raises(ApmlError, match="SHAPE"):
             forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"), Config(),
                     n_sizes=bad_n, m_sizes=bad_m)
+
+
+def test_plan_matches_forward_and_replays_in_a_cuda_graph():
+    """apml_plan_create / apml_plan_forward: allocation- and sync-free steps give the same bits
+    as apml_forward, run repeatedly on new inputs, and replay correctly from a CUDA graph."""
+    Config, forward = _gpu()
+    from paper_2512_19743_b200 import Plan
+    B, N, M = 4, 700, 650
+    cfg = Config(sync_check=False)
+    inputs = [clouds.batch(kind, B, N, M, 40 + k) for k, kind in enumerate(("shapenet", "uniform", "mmfi"))]
+
+    def ref(x, y):
+        loss, ctx = forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"), cfg)
+        g = ctx.backward(torch.ones(B, device="cuda"))
+        return loss, g
+
+    plan = Plan(B, N, M, cfg)
+    for x, y in inputs[:2]:  # eager, twice: counters re-zeroed per forward
+        lp = plan.forward(torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda"))
+        gp = plan.backward(torch.ones(B, device="cuda"))
+        lr, gr = ref(x, y)
+        assert torch.equal(lp, lr) and torch.equal(gp, gr)
+    # CUDA graph: static buffers, capture one step, replay on other inputs
+    ps = torch.zeros(B, N, 3, device="cuda")
+    gs = torch.zeros(B, M, 3, device="cuda")
+    ls = torch.zeros(B, device="cuda")
+    gout = torch.zeros(B, N, 3, device="cuda")
+    ones = torch.ones(B, device="cuda")
+    ps.copy_(torch.tensor(inputs[0][0])); gs.copy_(torch.tensor(inputs[0][1]))
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):  # warm the plan on the capture stream
+        plan.forward(ps, gs, ls)
+        plan.backward(ones, out=gout)
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        plan.forward(ps, gs, ls)
+        plan.backward(ones, out=gout)
+    for x, y in inputs:
+        ps.copy_(torch.tensor(x)); gs.copy_(torch.tensor(y))
+        graph.replay()
+        torch.cuda.synchronize()
+        lr, gr = ref(x, y)
+        assert torch.equal(ls, lr) and torch.equal(gout, gr)
+    plan.close()
+
+
+def test_plan_state_errors():
+    Config, _ = _gpu()
+    from paper_2512_19743_b200 import Plan
+    from paper_2512_19743_b200._lib import ApmlError
+    plan = Plan(2, 64, 64, Config())
+    with pytest.raises(ApmlError, match="STATE"):
+        plan.backward(torch.ones(2, device="cuda"))
+    with pytest.raises(ValueError):
+        plan.forward(torch.zeros(2, 65, 3, device="cuda"), torch.zeros(2, 64, 3, device="cuda"))
+    plan.close()
