@@ -415,9 +415,45 @@ def main():
                  "culled": culled, "dense_equivalent_evals": 3 * full_evals}
     roof_dist["frac"] = roof_dist["achieved"] / alu_peak
 
-    # end to end through the host entry point (pinned host buffers; copies inside the bracket)
+    # end to end (pinned host inputs copied in, the step, the loss read back; all inside the
+    # bracket).  Graph mode: the public Plan API as a training loop uses it (inputs copied into
+    # the plan's static tensors, graph replay, loss to the host; the gradient stays on the
+    # device for the network's backward).  Eager mode: apml_loss_grad_host (loss AND gradient
+    # back to the host).
     e2e = None
-    if not args.no_e2e and not rowshard and ns is None:
+    if not args.no_e2e and use_graph:
+        ph = torch.tensor(x).pin_memory()
+        gh = torch.tensor(y).pin_memory()
+        lo = torch.empty(B, pin_memory=True)
+
+        def e2e_step():
+            pred.copy_(ph, non_blocking=True)
+            gt.copy_(gh, non_blocking=True)
+            graph.replay()
+            if world > 1:
+                sharded_reduce(loss_buf)
+            lo.copy_(loss_buf, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+        for _ in range(2):
+            e2e_step()
+        ke = max(3, min(args.steps, 20))
+        acc = 0.0
+        for _ in range(ke):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            acc += (time.perf_counter() - t0) * 1e3
+        e2e_ms = acc / ke
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": pairs_per_step / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": 4 * B * 3 * (N + M), "d2h_bytes_per_step": 4 * B,
+               "api": "Plan (apml_plan_forward + apml_backward) in a CUDA graph: pinned H2D inputs, "
+                      "graph replay, D2H loss"}
+    elif not args.no_e2e and not rowshard and ns is None:
         ph = torch.tensor(x).pin_memory()
         gh = torch.tensor(y).pin_memory()
         lo = torch.empty(B, pin_memory=True)
