@@ -736,12 +736,18 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
   k_rs_astep<<<gr256, 256, 0, s>>>(a, 0);
   c->launches += 6;  // + the scan's own
   for (int l = 1; l <= L; ++l) {  // Eq. (3) column sums all-reduced (X3), Eq. (4) local
-    k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
-    CK(cudaGetLastError());
-    if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
-    k_rs_bstep<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
+    if (c->comm.world == 1) {  // nothing to all-reduce: column sum + column step fused
+      k_rs_colsum_bstep<<<gc256, 256, 0, s>>>(a, l);
+      c->launches += 1;
+    } else {
+      k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
+      CK(cudaGetLastError());
+      if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
+      k_rs_bstep<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
+      c->launches += 2;
+    }
     k_rs_astep<<<gr256, 256, 0, s>>>(a, l);
-    c->launches += 3;
+    c->launches += 1;
   }
   {
     const int nblk = (N + kLossThreads - 1) / kLossThreads;
@@ -770,12 +776,18 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
     c->launches += 3;
     for (int l = L; l >= 1; --l) {
       k_rs_bwd_rowrev<<<gr256, 256, 0, s>>>(a, l);
-      k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec + N + M, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
-      CK(cudaGetLastError());
-      if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
-      k_rs_bwd_colrev<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
+      if (c->comm.world == 1) {
+        k_rs_colsum_colrev<<<gc256, 256, 0, s>>>(a, l);
+        c->launches += 1;
+      } else {
+        k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec + N + M, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
+        CK(cudaGetLastError());
+        if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
+        k_rs_bwd_colrev<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
+        c->launches += 2;
+      }
       k_rs_bwd_rowrev2<<<gr256, 256, 0, s>>>(a, l);
-      c->launches += 4;
+      c->launches += 2;
     }
     k_rs_row_soft<<<gr, kRsThreads, 0, s>>>(a);
     k_rs_col_soft_part<<<gc256, 256, 0, s>>>(a, 0, c->comm.rank);

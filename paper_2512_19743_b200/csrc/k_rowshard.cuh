@@ -466,6 +466,17 @@ __global__ void __launch_bounds__(256) k_rs_colsum(const SparseArgs A, const flo
   if (j < A.M) out[(size_t)b * out_stride + j] = t;
 }
 
+// Single GPU (world 1: nothing to all-reduce between them): the column sum and the column step
+// of Eq. (3) in one launch (the column step needs only its own column's sum).
+__global__ void __launch_bounds__(256) k_rs_colsum_bstep(const SparseArgs A, int l) {
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || j - lane >= A.M) return;  // warp-uniform
+  const float t = grp_colsum(A, b, j, A.gvec + (size_t)b * 2 * (A.N + A.M), S.x[wid], S.y[wid]);
+  grp_bstep(A, b, j, l, t);
+}
+
 // Column step of Eq. (3) on the all-reduced Q (every rank).
 __global__ void k_rs_bstep(const SparseArgs A, int l, const float* __restrict__ Q) {
   const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -573,6 +584,16 @@ __global__ void __launch_bounds__(256) k_rs_bwd_rowrev(const SparseArgs A, int l
   const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
   if (A.cursor[b] > A.cap || i - lane >= A.N) return;  // warp-uniform
   grp_rowrev(A, b, i, l, S.v[wid], S.own[wid]);
+}
+
+// Single GPU: P0^T Rbar^l and the column step reverse in one launch.
+__global__ void __launch_bounds__(256) k_rs_colsum_colrev(const SparseArgs A, int l) {
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || j - lane >= A.M) return;  // warp-uniform
+  const float t = grp_colsum(A, b, j, A.gvec + (size_t)b * 2 * (A.N + A.M) + A.N + A.M, S.x[wid], S.y[wid]);
+  grp_colrev(A, b, j, l, t);
 }
 
 __global__ void k_rs_bwd_colrev(const SparseArgs A, int l, const float* __restrict__ t) {
