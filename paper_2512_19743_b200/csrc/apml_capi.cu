@@ -774,8 +774,11 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
     if ((st = coll_sum(c, c->qbuf, (int64_t)B * M)) != APML_OK) return st;
     k_rs_bwd_set_bbar<<<gc256, 256, 0, s>>>(a, c->qbuf);
     c->launches += 3;
-    for (int l = L; l >= 1; --l) {
-      k_rs_bwd_rowrev<<<gr256, 256, 0, s>>>(a, l);
+    if (L >= 1) {
+      k_rs_bwd_rowrev<<<gr256, 256, 0, s>>>(a, L);
+      c->launches += 1;
+    }
+    for (int l = L; l >= 1; --l) {  // row step reverse of l - 1 runs inside rowrev2 of l
       if (c->comm.world == 1) {
         k_rs_colsum_colrev<<<gc256, 256, 0, s>>>(a, l);
         c->launches += 1;
@@ -786,8 +789,8 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
         k_rs_bwd_colrev<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
         c->launches += 2;
       }
-      k_rs_bwd_rowrev2<<<gr256, 256, 0, s>>>(a, l);
-      c->launches += 2;
+      k_rs_bwd_rowrev2_rowrev<<<gr256, 256, 0, s>>>(a, l);
+      c->launches += 1;
     }
     k_rs_row_soft<<<gr, kRsThreads, 0, s>>>(a);
     k_rs_col_soft_part<<<gc256, 256, 0, s>>>(a, 0, c->comm.rank);

@@ -609,6 +609,20 @@ __global__ void __launch_bounds__(256) k_rs_bwd_rowrev2(const SparseArgs A, int 
   grp_rowrev2(A, b, i, l, S.x[wid], S.y[wid], S.v[wid], S.own[wid]);
 }
 
+// Row step 2 of reverse iteration l fused with the row step of iteration l - 1 (both touch
+// only the warp's own rows; no collective between them): one launch per iteration fewer.
+__global__ void __launch_bounds__(256) k_rs_bwd_rowrev2_rowrev(const SparseArgs A, int l) {
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] > A.cap || i - lane >= A.N) return;  // warp-uniform
+  grp_rowrev2(A, b, i, l, S.x[wid], S.y[wid], S.v[wid], S.own[wid]);
+  if (l > 1) {
+    __syncwarp();  // P0bar entries and the warp's scratch are shared by the lanes of both walks
+    grp_rowrev(A, b, i, l - 1, S.v[wid], S.own[wid]);
+  }
+}
+
 // Row softmax reverse (local rows).
 __global__ void __launch_bounds__(kRsThreads) k_rs_row_soft(const SparseArgs A) {
   __shared__ uint32_t s_long[kLongCap];
