@@ -407,7 +407,10 @@ def main():
         ach = byt / (med[dom] / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": ach / peaks.get("hbm_gbs", 6544.7), "traffic": traffic,
-                "note": "algorithmic bytes = SURVEY 8(d) per-entry figure x nnz"}
+                "note": "algorithmic bytes = SURVEY 8(d) per-entry figure x nnz; the per-pair working set "
+                        "is shared-memory / L2 resident (see traffic), the stage is bound by dependent "
+                        "gathers and 2 L_iter DSMEM exchange rounds (~0.6 us each, "
+                        "scripts/micro/xchg_bench.cu), not by HBM bandwidth"}
     dist_ms = sum(med[k] for k in dist_stages)
     tot_evals = sum(evals_by.values())
     roof_dist = {"bound": "alu", "achieved": LANE_OPS_PER_EVAL * tot_evals / (dist_ms / 1e3) / 1e12,
