@@ -641,7 +641,7 @@ __device__ __forceinline__ void xchg_arm(const Xchg& x) {
 // Write element k of the vector into the replica of every CTA of the cluster (st.async, DSMEM),
 // each store signalling the destination's mbarrier.
 __device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) {
-  if (!x.smem) { x.rep[k] = v; return; }
+  if (!x.smem || CL == 1) { x.rep[k] = v; return; }  // one CTA: its replica is the vector
   const uint32_t a = smem_addr(x.rep + k);
   for (int r = 0; r < CL; ++r)
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
@@ -649,8 +649,9 @@ __device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) 
 }
 // Wait until the whole vector has arrived, then re-arm for its next use.
 __device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x, int CL, int me) {
-  (void)CL; (void)me;
+  (void)me;
   if (!x.smem) { cl.sync(); return; }
+  if (CL == 1) { __syncthreads(); return; }  // no peers: a CTA barrier publishes the stores
   uint32_t done = 0;
   while (!done)
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
