@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
     const int j = llc.line(q);
     if (coff[j - sc.lo + 1] - coff[j - sc.lo] > kRegLine) col_init(j, 32);
   }
-  cl.sync();  // every CTA is done with its a^L copy before Rbar^L arrives in it
+  csync(cl);  // every CTA is done with its a^L copy before Rbar^L arrives in it
   phase(A, 2);
 
   // ---- reverse Sinkhorn (P0bar accumulated per CSR entry)
@@ -270,12 +270,12 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
   // ---- row softmax reverse (own rows; global CSR arrays, contiguous per row)
   row_soft_rev<1, 8>(A, b, sr, llr);
   row_soft_rev<32, 1>(A, b, sr, llr);
-  cl.sync();  // P0bar of every row visible to the column owners
+  csync(cl);  // P0bar of every row visible to the column owners
   phase(A, 4);
   // ---- column softmax reverse (own columns; CSC-order inputs + P0bar through csc_perm)
   col_soft_rev2<1>(A, b, sc, coff, ccs, gc, llc);
   col_soft_rev2<32>(A, b, sc, coff, ccs, gc, llc);
-  cl.sync();  // column adjoints visible to the row owners
+  csync(cl);  // column adjoints visible to the row owners
   phase(A, 5);
   // ---- cbar per entry and the Eq. (5) scatter into grad_pred
   grad_rows<1, 4>(A, b, sr, llr);

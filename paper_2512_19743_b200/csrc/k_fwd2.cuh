@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
     cl.map_shared_rank(&s_tot[0][0], (int)threadIdx.x)[rank] = nnzr;
     cl.map_shared_rank(&s_tot[1][0], (int)threadIdx.x)[rank] = nnzc;
   }
-  cl.sync();
+  csync(cl);
   unsigned gr = 0, gc = 0;  // global CSR / CSC offsets of this CTA's slices
   for (int r = 0; r < rank; ++r) { gr += s_tot[0][r]; gc += s_tot[1][r]; }
   for (int k = threadIdx.x; k < nr; k += blockDim.x) rp[sr.lo + k] = gr + roff[k];
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
       if (Ln > kRegLine) sort_line_warp<false>(A, b, C, beg, Ln, gc);
     }
   }
-  cl.sync();  // A.inv complete for the whole pair
+  csync(cl);  // A.inv complete for the whole pair
   phase(A, 3);
   // CSR position of every CSC entry (the backward's column passes); frees C.t for c
   for (uint32_t q0 = threadIdx.x; q0 < nnzc; q0 += 4 * blockDim.x) {
@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
       C.idx[q] &= kIdxMask;  // = csc_i
     }
   }
-  cl.sync();
+  csync(cl);
   if (rank == 0 && threadIdx.x == 0) {
     double t = 0.0;
     for (int r = 0; r < CL; ++r) t += s_part[r];

@@ -111,6 +111,13 @@ __device__ __forceinline__ void phase(const SparseArgs& A, int k) {
   }
 }
 
+// Cluster barrier, or a CTA barrier when the cluster is a single CTA (barrier.cluster also
+// invalidates L1, which a single CTA does not need: its own global writes are coherent to it).
+__device__ __forceinline__ void csync(cg::cluster_group& cl) {
+  if (cl.num_blocks() == 1) __syncthreads();
+  else cl.sync();
+}
+
 struct Slice {
   int lo, hi;
 };
@@ -159,7 +166,7 @@ __device__ void cluster_scan(cg::cluster_group& cl, unsigned* cnt, unsigned* ptr
     unsigned* remote = cl.map_shared_rank(s_tot, (int)threadIdx.x);
     remote[rank] = slice_total;
   }
-  cl.sync();
+  csync(cl);
   unsigned off = 0;
   for (int r = 0; r < rank; ++r) off += s_tot[r];
   unsigned run = off + inc - sum + (w ? s_warp[w - 1] : 0u);
@@ -650,7 +657,7 @@ __device__ __forceinline__ void xchg_put(const Xchg& x, int CL, int k, float v) 
 // Wait until the whole vector has arrived, then re-arm for its next use.
 __device__ __forceinline__ void xchg_end(cg::cluster_group& cl, Xchg& x, int CL, int me) {
   (void)me;
-  if (!x.smem) { cl.sync(); return; }
+  if (!x.smem) { csync(cl); return; }
   if (CL == 1) { __syncthreads(); return; }  // no peers: a CTA barrier publishes the stores
   uint32_t done = 0;
   while (!done)
@@ -819,7 +826,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   // S4: counts -> offsets ("exclusive prefix sum"), then bucket the entries
   cluster_scan(cl, rc, rp, N, sr, s_tot_r, s_warp);
   cluster_scan(cl, cc, cp, M, sc, s_tot_c, s_warp);
-  cl.sync();
+  csync(cl);
   phase(A, 1);
   {
     // kSc entries per thread per step: loads, then all atomics, then the stores, so a step
@@ -852,7 +859,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
       }
     }
   }
-  cl.sync();
+  csync(cl);
   phase(A, 2);
   // rows: sort by j (registers for short rows, warp rank sort for long ones) and the row
   // softmax (S5) on the kept support
@@ -866,7 +873,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   __syncthreads();
   phase(A, 5);
   row_norm(A, b, sr, llr);
-  cl.sync();
+  csync(cl);
   phase(A, 6);
   // columns: sort by i, column softmax, symmetrisation P0 = (P_row + P_col)/2
   col_sort_norm_regs(A, b, sc);
@@ -876,7 +883,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   __syncthreads();
   phase(A, 8);
   col_norm(A, b, sc, llc);
-  cl.sync();
+  csync(cl);
   phase(A, 9);
   // S6: Sinkhorn.  Replicas of a and b (full length) + own CSR / CSC slices in shared memory.
   uint8_t* sm = shm;
@@ -912,14 +919,14 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
   if (fit) {
     const SliceView<IdxT> R = stage_slice<IdxT>(sm, rp, sr, A.csr_jf + pb, A.P0 + pb, false);
     const SliceView<IdxT> C = stage_slice<IdxT>(sm, cp, sc, A.csc_i + pb, A.P0c + pb, false);
-    cl.sync();
+    csync(cl);
     phase(A, 10);
     if (A.rep_smem) sinkhorn_fwd<IdxT, true>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
     else sinkhorn_fwd<IdxT, false>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
   } else {
     const SliceView<uint32_t> R{rp + sr.lo, A.csr_jf + pb, A.P0 + pb, nullptr};
     const SliceView<uint32_t> C{cp + sc.lo, A.csc_i + pb, A.P0c + pb, nullptr};
-    cl.sync();
+    csync(cl);
     phase(A, 10);
     sinkhorn_fwd<uint32_t, false>(cl, A, b, sr, sc, R, C, xa, xb, llr, llc);
   }
@@ -942,7 +949,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
     cl.map_shared_rank(s_part, 0)[rank] = t;
   }
-  cl.sync();
+  csync(cl);
   if (rank == 0 && threadIdx.x == 0) {
     double t = 0.0;
     for (int r = 0; r < CL; ++r) t += s_part[r];
@@ -1138,7 +1145,7 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       __syncthreads();
     }
   }
-  cl.sync();
+  csync(cl);
 }
 
 // ---- per-line loops of the backward, run by groups of G lanes: G = 1 (thread per line,
@@ -1526,7 +1533,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
         g2s_async(bhs, bhg, (size_t)(L + 1) * M);
         cp_async_wait_all();
       }
-      cl.sync();
+      csync(cl);
       phase(A, 1);
       const bool all_sm = A.rep_smem && ahs && bhs && ab_sm;
       if (all_sm) sinkhorn_bwd<IdxT, true>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, ahs, bhs, llr, llc);
@@ -1539,7 +1546,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
       for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x)
         for (uint32_t p = rp[i]; p < rp[i + 1]; ++p)
           A.pbar[pb + p] = gl * aL[i] * bL[A.csr_jf[pb + p] & kIdxMask] * A.cs[pb + p];
-      cl.sync();
+      csync(cl);
       phase(A, 1);
       sinkhorn_bwd<uint32_t, false>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bls, nullptr, nullptr, llr, llc);
     }
@@ -1547,11 +1554,11 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs
     phase(A, 2);
     row_soft_rev<1, 8>(A, b, sr, llr);
     row_soft_rev<32, 1>(A, b, sr, llr);
-    cl.sync();
+    csync(cl);
     phase(A, 3);
     col_soft_rev<1, 8>(A, b, sc, llc);
     col_soft_rev<32, 1>(A, b, sc, llc);
-    cl.sync();
+    csync(cl);
     phase(A, 4);
   }
   grad_rows<1, 4>(A, b, sr, llr);
