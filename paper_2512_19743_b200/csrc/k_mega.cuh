@@ -999,6 +999,51 @@ __device__ __forceinline__ float seg_dot_axpy(const SliceView<IdxT>& V, uint32_t
   return (t[0] + t[1]) + (t[2] + t[3]);
 }
 
+// Row step 2 of reverse iteration l fused with the row step of iteration l - 1 for one short
+// row (<= kRegLine entries, one batched gather each):
+//   t = sum_j P0_ij Qbar^l_j;  abar_i += t;
+//   (l > 1) Rbar^{l-1}_i = -abar_i (a^{l-1}_i)^2, abar_i <- abar_i eps (a^{l-1}_i / a^{l-2}_i)^2;
+//   P0bar_ij += Qbar^l_j a^{l-1}_i  (+ Rbar^{l-1}_i b^{l-1}_j)
+// Returns Rbar^{l-1}_i (0 when l == 1); the caller pushes it.
+template <typename IdxT>
+__device__ __forceinline__ float seg_rev_fused(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* q,
+                                               const float* bprev, float alm, float almm, float& abk, float eps) {
+  const uint32_t n = p1 - p0;
+  uint32_t ix[kRegLine];
+  float g[kRegLine];
+  float t[4] = {0.f, 0.f, 0.f, 0.f};
+  {
+    float v[kRegLine];
+#pragma unroll
+    for (uint32_t u = 0; u < kRegLine; ++u) {
+      ix[u] = u < n ? V.col(p0 + u) : 0u;
+      v[u] = u < n ? V.val[p0 + u] : 0.f;
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < kRegLine; ++u) g[u] = u < n ? q[ix[u]] : 0.f;
+#pragma unroll
+    for (uint32_t u = 0; u < kRegLine; ++u)
+      if (u < n) t[u & 3] = __fmaf_rn(g[u], v[u], t[u & 3]);
+  }
+  abk += (t[0] + t[1]) + (t[2] + t[3]);
+  float Rb = 0.f;
+  if (bprev) {
+    const float r = alm / almm;
+    Rb = -abk * alm * alm;
+    abk = abk * eps * r * r;
+  }
+  float bp[kRegLine], c[kRegLine];
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u) {
+    bp[u] = (u < n && bprev) ? bprev[ix[u]] : 0.f;
+    c[u] = u < n ? V.acc[p0 + u] : 0.f;
+  }
+#pragma unroll
+  for (uint32_t u = 0; u < kRegLine; ++u)
+    if (u < n) V.acc[p0 + u] = (c[u] + g[u] * alm) + Rb * bp[u];
+  return Rb;
+}
+
 // Reverse Sinkhorn in scaling form; P0bar accumulated per CSR entry of the own
 // rows in shared memory (R.acc).  Short lines by a thread, long lines by a warp (as forward).
 template <typename IdxT, bool kSm>
@@ -1036,6 +1081,38 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     for (int k = threadIdx.x; k < M; k += blockDim.x) bls[(L & 1) * M + k] = bh[(size_t)L * M + k];
     __syncthreads();
   }
+  // row step reverse of iteration l: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
+  // P0bar_ij += Rbar^l_i b^l_j.  Iteration L's runs here; iteration l-1's runs fused with
+  // row step 2 of iteration l (seg_rev_fused / the warp loop below): one row pass fewer.
+  {
+    const float* bL = bls ? bls + (L & 1) * M : bh + (size_t)L * M;
+    auto row_rev = [&](int i, int k, float abk, bool writer) -> float {
+      const float al = ah[(size_t)L * ald + i], alm = ah[(size_t)(L - 1) * ald + i];
+      const float r = al / alm;
+      const float Rb = -abk * al * al;
+      if (writer) {
+        ab[k] = abk * A.eps * r * r;
+        xchg_put(xr, CL, i, Rb);
+      }
+      return Rb;
+    };
+    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+      const int k = i - sr.lo;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 > kRegLine) continue;
+      seg_axpy(R, p0, p1, row_rev(i, k, ab[k], true), bL);
+    }
+    for (int q = w; q < llr.count(); q += nw) {
+      const int i = llr.line(q), k = i - sr.lo;
+      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+      if (p1 - p0 <= kRegLine) continue;
+      const float abk = ab[k];
+      __syncwarp();
+      const float Rb = row_rev(i, k, abk, lane == 0);
+      for (uint32_t p = p0 + lane; p < p1; p += 32) R.acc[p] += Rb * bL[R.col(p)];
+      __syncwarp();
+    }
+  }
   for (int l = L; l >= 1; --l) {
     float pf[kPf];
     if (bls && l > 1) {
@@ -1054,34 +1131,6 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     for (int u = 0; u < kOwnPf; ++u) {
       const int j = sc.lo + threadIdx.x + u * blockDim.x;
       blm_pf[u] = j < sc.hi ? bh[(size_t)(l - 1) * M + j] : 1.f;
-    }
-    // row step reverse: Rbar^l = -abar (a^l)^2, abar <- abar eps (a^l/a^{l-1})^2,
-    // P0bar_ij += Rbar^l_i b^l_j
-    auto row_rev = [&](int i, int k, float abk, bool writer) -> float {
-      const float al = ah[(size_t)l * ald + i], alm = ah[(size_t)(l - 1) * ald + i];
-      const float r = al / alm;
-      const float Rb = -abk * al * al;
-      if (writer) {
-        ab[k] = abk * A.eps * r * r;
-        xchg_put(xr, CL, i, Rb);
-      }
-      return Rb;
-    };
-    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
-      const int k = i - sr.lo;
-      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
-      if (p1 - p0 > kRegLine) continue;
-      seg_axpy(R, p0, p1, row_rev(i, k, ab[k], true), bcur);
-    }
-    for (int q = w; q < llr.count(); q += nw) {
-      const int i = llr.line(q), k = i - sr.lo;
-      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
-      if (p1 - p0 <= kRegLine) continue;
-      const float abk = ab[k];
-      __syncwarp();
-      const float Rb = row_rev(i, k, abk, lane == 0);
-      for (uint32_t p = p0 + lane; p < p1; p += 32) R.acc[p] += Rb * bcur[R.col(p)];
-      __syncwarp();
     }
     xchg_end(cl, xr, CL, me);
     // column step reverse: bbar += P0^T Rbar^l; Qbar^l = -bbar (b^l)^2; bbar <- bbar eps (..)^2
@@ -1111,13 +1160,29 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       const float t = warp_dot(C, p0, p1, rcur);
       if (lane == 0) col_rev(j, k, t, bh[(size_t)(l - 1) * M + j]);
     }
+    // b^{l-1} into the other staging buffer (it held b^{l+1}, last read by the column step of
+    // iteration l+1); published by the barrier inside xchg_end below
+    if (bls && l > 1) {
+#pragma unroll
+      for (int u = 0; u < kPf; ++u) {
+        const int k = threadIdx.x + u * blockDim.x;
+        if (k < M) bls[((l - 1) & 1) * M + k] = pf[u];
+      }
+    }
     xchg_end(cl, xq, CL, me);
-    // abar += P0 Qbar^l; P0bar_ij += Qbar^l_j a^{l-1}_i (one pass)
+    // row step 2 of l: abar += P0 Qbar^l, P0bar_ij += Qbar^l_j a^{l-1}_i -- fused with the
+    // row step of l-1 (Rbar^{l-1} pushed for the next column step)
+    const float* bprev = l > 1 ? (bls ? bls + ((l - 1) & 1) * M : bh + (size_t)(l - 1) * M) : nullptr;
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
       const int k = i - sr.lo;
       const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
       if (p1 - p0 > kRegLine) continue;
-      ab[k] += seg_dot_axpy(R, p0, p1, qcur, ah[(size_t)(l - 1) * ald + i]);
+      const float alm = ah[(size_t)(l - 1) * ald + i];
+      const float almm = l > 1 ? ah[(size_t)(l - 2) * ald + i] : 1.f;
+      float abk = ab[k];
+      const float Rb = seg_rev_fused(R, p0, p1, qcur, bprev, alm, almm, abk, A.eps);
+      ab[k] = abk;
+      if (l > 1) xchg_put(xr, CL, i, Rb);
     }
     for (int q = w; q < llr.count(); q += nw) {
       const int i = llr.line(q), k = i - sr.lo;
@@ -1125,24 +1190,26 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       if (p1 - p0 <= kRegLine) continue;
       const float alm = ah[(size_t)(l - 1) * ald + i];
       float t = 0.f;
-      for (uint32_t p = p0 + lane; p < p1; p += 32) {
-        const float qv = qcur[R.col(p)];
-        t = __fmaf_rn(qv, R.val[p], t);
-        R.acc[p] += qv * alm;
-      }
+      for (uint32_t p = p0 + lane; p < p1; p += 32) t = __fmaf_rn(qcur[R.col(p)], R.val[p], t);
       t = gsum<32>(t);
-      if (lane == 0) ab[k] += t;
-      __syncwarp();
-    }
-    // the next row step touches only the rows this thread (warp) owns; only the staged
-    // b^{l-1} needs a CTA barrier
-    if (bls && l > 1) {
-#pragma unroll
-      for (int u = 0; u < kPf; ++u) {
-        const int k = threadIdx.x + u * blockDim.x;
-        if (k < M) bls[((l - 1) & 1) * M + k] = pf[u];
+      float abk = ab[k] + t;
+      float Rb = 0.f;
+      if (l > 1) {
+        const float almm = ah[(size_t)(l - 2) * ald + i];
+        const float r = alm / almm;
+        Rb = -abk * alm * alm;
+        abk = abk * A.eps * r * r;
       }
-      __syncthreads();
+      for (uint32_t p = p0 + lane; p < p1; p += 32) {
+        const uint32_t j = R.col(p);
+        R.acc[p] = (R.acc[p] + qcur[j] * alm) + (l > 1 ? Rb * bprev[j] : 0.f);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ab[k] = abk;
+        if (l > 1) xchg_put(xr, CL, i, Rb);
+      }
+      __syncwarp();
     }
   }
   csync(cl);
