@@ -92,6 +92,78 @@ __device__ void col_soft_rev2(const SparseArgs& A, int b, Slice s, const unsigne
   }
 }
 
+// cbar per entry and the Eq. (5) scatter (as grad_rows<1, U>) for the rows of <= kRegLine
+// entries, reading the CTA's shared-memory CSR slice (16-bit j, c, P0, P0bar) instead of the
+// global copies; flags / P_row / P_col stay global (contiguous per row).
+template <int U>
+__device__ void grad_rows_sm(const SparseArgs& A, int b, Slice s, const unsigned* off, const uint16_t* j16,
+                             const float* cs, const float* p0s, const float* pbs, uint32_t gr) {
+  const int N = A.N, M = A.M, L = A.L;
+  const size_t pb = (size_t)b * A.cap;
+  const float gl = A.grad_loss[b];
+  const float* aL = A.a_hist + ((size_t)b * (L + 1) + L) * N;
+  const float* bL = A.b_hist + ((size_t)b * (L + 1) + L) * M;
+  for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
+    const int k = i - s.lo;
+    const uint32_t beg = off[k], end = off[k + 1];
+    if (end - beg > kRegLine) continue;
+    const float4 x = A.pred4[(size_t)b * N + i];
+    const LineBack rbk = A.rowback[(size_t)b * N + i];
+    const int2 ri = A.rowidx[(size_t)b * N + i];
+    const double ai = (double)aL[i];
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    for (uint32_t p0 = beg; p0 < end; p0 += U) {
+      uint32_t jf[U], j[U];
+      float cv[U], p0v[U], pbv[U], prv[U], pcv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t p = p0 + u;
+        const bool v = p < end;
+        j[u] = v ? (uint32_t)j16[p] : 0u;
+        cv[u] = v ? cs[p] : 1.f;
+        p0v[u] = v ? p0s[p] : 0.f;
+        pbv[u] = v ? pbs[p] : 0.f;
+        jf[u] = v ? A.csr_jf[pb + gr + p] : 0u;
+        prv[u] = v ? A.prow[pb + gr + p] : 0.f;
+        pcv[u] = v ? A.pcol[pb + gr + p] : 0.f;
+      }
+      float4 y[U];
+      float bLv[U];
+      int2 ci[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool v = p0 + u < end;
+        y[u] = v ? A.gt4[(size_t)b * M + j[u]] : x;
+        bLv[u] = v ? bL[j[u]] : 0.f;
+        ci[u] = v ? A.colidx[(size_t)b * M + j[u]] : make_int2(-1, -1);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (p0 + u >= end) continue;
+        double cbar = (double)gl * ai * (double)p0v[u] * (double)bLv[u];  // d loss / d c = v
+        const double hp = 0.5 * (double)pbv[u];
+        if (jf[u] & kFlagRow) cbar -= (double)rbk.T * (double)prv[u] * (hp - (double)rbk.S);
+        if ((int)j[u] == ri.x) cbar += rbk.ca;
+        if ((int)j[u] == ri.y) cbar += rbk.cb;
+        const bool cf = (jf[u] & kFlagCol) != 0;
+        if (cf || ci[u].x == i || ci[u].y == i) {
+          const LineBack cbk = A.colback[(size_t)b * M + j[u]];
+          if (cf) cbar -= (double)cbk.T * (double)pcv[u] * (hp - (double)cbk.S);
+          if (ci[u].x == i) cbar += cbk.ca;
+          if (ci[u].y == i) cbar += cbk.cb;
+        }
+        const double w = cbar / ((double)cv[u] + (double)A.eps_dist);  // Eq. (5)
+        if (A.gw) A.gw[pb + gr + p0 + u] = (float)w;
+        gx += w * ((double)x.x - (double)y[u].x);
+        gy += w * ((double)x.y - (double)y[u].y);
+        gz += w * ((double)x.z - (double)y[u].z);
+      }
+    }
+    float* g = A.grad_pred + ((size_t)b * N + orig_row(A, b, (uint32_t)i)) * 3;
+    g[0] = (float)gx; g[1] = (float)gy; g[2] = (float)gz;
+  }
+}
+
 __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArgs A) {
   extern __shared__ __align__(16) uint8_t shm[];
   __shared__ uint32_t s_long_r[kLongCap], s_long_c[kLongCap];
@@ -278,7 +350,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
   csync(cl);  // column adjoints visible to the row owners
   phase(A, 5);
   // ---- cbar per entry and the Eq. (5) scatter into grad_pred
-  grad_rows<1, 4>(A, b, sr, llr);
+  if (fit16) grad_rows_sm<4>(A, b, sr, roff, r16, rc, rP0, racc, gr);
+  else grad_rows<1, 4>(A, b, sr, llr);
   grad_rows<32, 1>(A, b, sr, llr);
   phase(A, 6);
 }
