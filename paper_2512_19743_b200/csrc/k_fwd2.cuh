@@ -301,41 +301,46 @@ __device__ float line_softmax(const SparseArgs& A, int b, const Side& S, int lin
 // P0 of the entries of one line (chunks of 8, gathers before stores).  kRows: CSR entries of
 // row i -- own P_row = s * iz_i, P_col re-evaluated from colB[j] and 1/Z'_j; writes P_row and
 // P_col (CSR order, global, for the backward) and P0.  Else CSC entries of column j.
-template <bool kRows>
+// G == 1: one thread per line; G == 32: one warp per (long) line, lane-strided entries.
+template <bool kRows, int G = 1>
 __device__ void line_p0(const SparseArgs& A, int b, const Side& S, int line, int k, const float* iz_own,
                         const float* iz_oth, uint32_t gbase) {
   const int N = A.N, M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const uint32_t beg = S.off[k], end = S.off[k + 1];
+  const uint32_t mem = G == 1 ? 0u : (threadIdx.x & 31);
   const float izl = iz_own[line];
   const uint32_t fo = kRows ? kFlagCol : kFlagRow;  // the OTHER side's flag
-  for (uint32_t p0 = beg; p0 < end; p0 += 8) {
+  for (uint32_t p0 = beg; p0 < end; p0 += 8 * G) {
     uint32_t ix[8];
     float c[8], s[8];
     LineB lo[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      const bool v = p0 + u < end;
-      ix[u] = v ? S.idx[p0 + u] : 0u;
-      c[u] = v ? S.c[p0 + u] : 0.f;
-      s[u] = v ? S.pr[p0 + u] : 0.f;
+      const uint32_t p = p0 + u * G + mem;
+      const bool v = p < end;
+      ix[u] = v ? S.idx[p] : 0u;
+      c[u] = v ? S.c[p] : 0.f;
+      s[u] = v ? S.pr[p] : 0.f;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const uint32_t o = ix[u] & kIdxMask;
-      lo[u] = (p0 + u < end && (ix[u] & fo)) ? (kRows ? A.colB[(size_t)b * M + o] : A.rowB[(size_t)b * N + o])
-                                             : LineB{0.f, 0.f, 0.f, 0};
+      lo[u] = (p0 + u * G + mem < end && (ix[u] & fo))
+                  ? (kRows ? A.colB[(size_t)b * M + o] : A.rowB[(size_t)b * N + o])
+                  : LineB{0.f, 0.f, 0.f, 0};
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      if (p0 + u >= end) continue;
+      const uint32_t p = p0 + u * G + mem;
+      if (p >= end) continue;
       const uint32_t o = ix[u] & kIdxMask;
       const float pown = __fmul_rn(s[u], izl);
       const float poth = (ix[u] & fo) ? __fmul_rn(line_sim(c[u], lo[u]), iz_oth[o]) : 0.f;
       const float prow = kRows ? pown : poth, pcol = kRows ? poth : pown;
-      S.val[p0 + u] = sym_p0(prow, pcol);
-      S.pr[p0 + u] = pown;  // this side's probability (CSR: P_row, CSC: P_col)
-      if (kRows) A.pcol[pb + gbase + p0 + u] = pcol;
+      S.val[p] = sym_p0(prow, pcol);
+      S.pr[p] = pown;  // this side's probability (CSR: P_row, CSC: P_col)
+      if (kRows) A.pcol[pb + gbase + p] = pcol;
     }
   }
 }
@@ -561,8 +566,21 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
   xchg_end(cl, xzc, CL, rank);
   phase(A, 5);
   // P0 = (P_row + P_col) / 2 on both sides (bitwise-equal copies)
-  for (int k = threadIdx.x; k < nr; k += blockDim.x) line_p0<true>(A, b, R, sr.lo + k, k, viz, vizc, gr);
-  for (int k = threadIdx.x; k < nc; k += blockDim.x) line_p0<false>(A, b, C, sc.lo + k, k, vizc, viz, gc);
+  for (int k = threadIdx.x; k < nr; k += blockDim.x)
+    if (roff[k + 1] - roff[k] <= kRegLine) line_p0<true>(A, b, R, sr.lo + k, k, viz, vizc, gr);
+  for (int k = threadIdx.x; k < nc; k += blockDim.x)
+    if (coff[k + 1] - coff[k] <= kRegLine) line_p0<false>(A, b, C, sc.lo + k, k, vizc, viz, gc);
+  {
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int q = w; q < llr.count(); q += nw) {
+      const int k = llr.line(q) - sr.lo;
+      if (roff[k + 1] - roff[k] > kRegLine) line_p0<true, 32>(A, b, R, sr.lo + k, k, viz, vizc, gr);
+    }
+    for (int q = w; q < llc.count(); q += nw) {
+      const int k = llc.line(q) - sc.lo;
+      if (coff[k + 1] - coff[k] > kRegLine) line_p0<false, 32>(A, b, C, sc.lo + k, k, vizc, viz, gc);
+    }
+  }
   // Sinkhorn history at l = 0
   float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   float* bh = A.b_hist + (size_t)b * (L + 1) * M;
