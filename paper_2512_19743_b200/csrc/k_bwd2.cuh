@@ -206,6 +206,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
   float* bls = reinterpret_cast<float*>(carve(sm, 8 * (size_t)M));
   unsigned* roff = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)(nr + 1)));
   unsigned* coff = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)(nc + 1)));
+  // line orders by length for the reverse Sinkhorn (single-CTA clusters, as the forward)
+  uint16_t* rperm = (CL == 1 && nr <= 65536 && nc <= 65536) ? reinterpret_cast<uint16_t*>(carve(sm, 2 * (size_t)nr)) : nullptr;
+  uint16_t* cperm = rperm ? reinterpret_cast<uint16_t*>(carve(sm, 2 * (size_t)nc)) : nullptr;
+  __shared__ unsigned s_hist[kRegLine + 2];
   auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
   const size_t ent = 4 * a16(4 * (size_t)nnzr) + 3 * a16(4 * (size_t)nnzc);
   const bool fit = (size_t)(sm - shm) + ent <= A.smem_bytes;  // (u16 indices need less)
@@ -320,6 +324,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
     const int j = llc.line(q);
     if (coff[j - sc.lo + 1] - coff[j - sc.lo] > kRegLine) col_init(j, 32);
   }
+  if (rperm) {
+    line_perm(roff, nr, rperm, s_hist);
+    line_perm(coff, nc, cperm, s_hist);
+  }
   csync(cl);  // every CTA is done with its a^L copy before Rbar^L arrives in it
   phase(A, 2);
 
@@ -328,7 +336,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
     if (fit16) {
       const SliceView<uint16_t> R{roff, r16, rP0, racc};
       const SliceView<uint16_t> C{coff, c16, cP0, nullptr};
-      sinkhorn_bwd<uint16_t, true>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bhs ? nullptr : bls, ahs, bhs, llr, llc);
+      sinkhorn_bwd<uint16_t, true>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bhs ? nullptr : bls, ahs, bhs, llr, llc,
+                                    rperm, cperm);
     } else {
       const SliceView<uint32_t> R{roff, rjf, rP0, racc};
       const SliceView<uint32_t> C{coff, cif, cP0, nullptr};

@@ -349,10 +349,10 @@ template <typename IdxT, bool kSm>
 __device__ void fwd2_sinkhorn(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                               const unsigned* roff, const IdxT* ridx, const float* rval, const unsigned* coff,
                               const IdxT* cidx, const float* cval, Xchg& xa, Xchg& xb, const LongList& llr,
-                              const LongList& llc) {
+                              const LongList& llc, const uint16_t* rperm, const uint16_t* cperm) {
   const SliceView<IdxT> RV{roff, ridx, rval, nullptr};
   const SliceView<IdxT> CV{coff, cidx, cval, nullptr};
-  sinkhorn_fwd<IdxT, kSm>(cl, A, b, sr, sc, RV, CV, xa, xb, llr, llc);
+  sinkhorn_fwd<IdxT, kSm>(cl, A, b, sr, sc, RV, CV, xa, xb, llr, llc, rperm, cperm);
 }
 
 __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArgs A) {
@@ -390,6 +390,10 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
   unsigned* coff = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)(nc + 1)));
   unsigned* rcur = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)nr));
   unsigned* ccur = reinterpret_cast<unsigned*>(carve(sm, 4 * (size_t)nc));
+  // line orders by length for Sinkhorn (slices of <= 65536 lines)
+  uint16_t* rperm = (nr <= 65536 && nc <= 65536) ? reinterpret_cast<uint16_t*>(carve(sm, 2 * (size_t)nr)) : nullptr;
+  uint16_t* cperm = rperm ? reinterpret_cast<uint16_t*>(carve(sm, 2 * (size_t)nc)) : nullptr;
+  __shared__ unsigned s_hist[kRegLine + 2];
   for (int k = threadIdx.x; k < N; k += blockDim.x) va[k] = 1.f;
   for (int k = threadIdx.x; k < M; k += blockDim.x) vb[k] = 1.f;
   for (int k = threadIdx.x; k < nr; k += blockDim.x) rcur[k] = 0u;
@@ -602,12 +606,19 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
     for (uint32_t q = threadIdx.x; q < nnzc; q += blockDim.x) c16[q] = (uint16_t)(C.idx[q] & kIdxMask);
     __syncthreads();
   }
+  // (single-CTA clusters only: with DSMEM peers the pushes of a warp must stay on consecutive
+  // addresses -- scattered st.async made the exchange slower than the saved loads, measured)
+  if (CL > 1) rperm = cperm = nullptr;
+  if (rperm) {
+    line_perm(roff, nr, rperm, s_hist);
+    line_perm(coff, nc, cperm, s_hist);
+  }
   phase(A, 6);
 
   // ---- S6: Sinkhorn, L_iter x {Eq. (3), Eq. (4)}
-  if (idx16) fwd2_sinkhorn<uint16_t, true>(cl, A, b, sr, sc, roff, r16, R.val, coff, c16, C.val, xa, xb, llr, llc);
-  else if (fit) fwd2_sinkhorn<uint32_t, true>(cl, A, b, sr, sc, roff, R.idx, R.val, coff, C.idx, C.val, xa, xb, llr, llc);
-  else fwd2_sinkhorn<uint32_t, false>(cl, A, b, sr, sc, roff, R.idx, R.val, coff, C.idx, C.val, xa, xb, llr, llc);
+  if (idx16) fwd2_sinkhorn<uint16_t, true>(cl, A, b, sr, sc, roff, r16, R.val, coff, c16, C.val, xa, xb, llr, llc, rperm, cperm);
+  else if (fit) fwd2_sinkhorn<uint32_t, true>(cl, A, b, sr, sc, roff, R.idx, R.val, coff, C.idx, C.val, xa, xb, llr, llc, rperm, cperm);
+  else fwd2_sinkhorn<uint32_t, false>(cl, A, b, sr, sc, roff, R.idx, R.val, coff, C.idx, C.val, xa, xb, llr, llc, rperm, cperm);
   phase(A, 7);
 
   // ---- S7: loss_b = sum_i a_i sum_j P0_ij b_j c_ij, own rows, then cluster sum

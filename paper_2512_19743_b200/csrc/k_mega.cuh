@@ -708,6 +708,57 @@ __device__ __forceinline__ float seg_dot(const SliceView<IdxT>& V, uint32_t p0, 
   return (s0 + s1) + (s2 + s3);
 }
 
+// seg_dot with a compile-time batch of KB predicated loads (lines of <= KB entries; same
+// accumulator assignment as seg_dot, hence the same bits), and the choice of KB from the
+// warp's longest line: with lines ordered by length (line_perm) most warps issue 4 or 8
+// loads per array instead of 16.
+template <int KB, typename IdxT>
+__device__ __forceinline__ float seg_dot_n(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* vec) {
+  const uint32_t L = p1 - p0;
+  float g[KB], v[KB];
+#pragma unroll
+  for (uint32_t u = 0; u < KB; ++u) {
+    g[u] = u < L ? vec[V.col(p0 + u)] : 0.f;
+    v[u] = u < L ? V.val[p0 + u] : 0.f;
+  }
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (uint32_t u = 0; u < KB; ++u)
+    if (u < L) s[u & 3] = __fmaf_rn(g[u], v[u], s[u & 3]);
+  return (s[0] + s[1]) + (s[2] + s[3]);
+}
+template <typename IdxT>
+__device__ __forceinline__ float seg_dot_adapt(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* vec,
+                                               uint32_t wmax) {
+  if (wmax <= 4) return seg_dot_n<4>(V, p0, p1, vec);
+  if (wmax <= 8) return seg_dot_n<8>(V, p0, p1, vec);
+  return seg_dot_n<16>(V, p0, p1, vec);
+}
+
+// Lines of a slice ordered by length (counting sort: 0..kRegLine, then longer), so that the
+// 32 lines of a warp have similar lengths (seg_dot_adapt).  The order inside a length class
+// is arbitrary: every line's result is independent of the thread that computes it.
+__device__ void line_perm(const unsigned* off, int n, uint16_t* perm, unsigned* hist /*[kRegLine + 2]*/) {
+  constexpr int kB = kRegLine + 2;
+  if (threadIdx.x < kB) hist[threadIdx.x] = 0u;
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const uint32_t L = off[k + 1] - off[k];
+    atomicAdd(hist + (L <= kRegLine ? L : kRegLine + 1), 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int q = 0; q < kB; ++q) { const unsigned v = hist[q]; hist[q] = run; run += v; }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const uint32_t L = off[k + 1] - off[k];
+    perm[atomicAdd(hist + (L <= kRegLine ? L : kRegLine + 1), 1u)] = (uint16_t)k;
+  }
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- forward Sinkhorn + loss
 //
 // A half-step costs one replica exchange (~0.6 us, scripts/micro/xchg_bench.cu) plus the
@@ -738,7 +789,8 @@ __device__ __forceinline__ void assume_smem(const SliceView<IdxT>& V) {
 template <typename IdxT, bool kSm>
 __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, Xchg& xa, Xchg& xb,
-                             const LongList& llr, const LongList& llc) {
+                             const LongList& llr, const LongList& llc, const uint16_t* rperm = nullptr,
+                             const uint16_t* cperm = nullptr) {
   const int N = A.N, M = A.M, L = A.L, CL = cl.num_blocks(), me = cl.block_rank();
   float* ah = A.a_hist + (size_t)b * (L + 1) * N;
   float* bh = A.b_hist + (size_t)b * (L + 1) * M;
@@ -767,11 +819,21 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     xchg_put(xa, CL, i, na);
     ah[(size_t)l * N + i] = na;
   };
+  const int nr = sr.hi - sr.lo, nc = sc.hi - sc.lo;
   for (int l = 1; l <= L; ++l) {
-    for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
-      const int k = j - sc.lo;
-      const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
-      if (p1 - p0 <= kRegLine) col_upd(j, seg_dot(C, p0, p1, a), l, p1 == p0);
+    if (cperm) {  // lines ordered by length: the warp's longest line sets the batch
+      for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+        const int k = cperm[t], j = sc.lo + k;
+        const uint32_t p0 = C.off[k], p1 = C.off[k + 1], Ln = p1 - p0;
+        const uint32_t wmax = __reduce_max_sync(__activemask(), Ln <= kRegLine ? Ln : 0u);
+        if (Ln <= kRegLine) col_upd(j, seg_dot_adapt(C, p0, p1, a, wmax), l, Ln == 0);
+      }
+    } else {
+      for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x) {
+        const int k = j - sc.lo;
+        const uint32_t p0 = C.off[k], p1 = C.off[k + 1];
+        if (p1 - p0 <= kRegLine) col_upd(j, seg_dot(C, p0, p1, a), l, p1 == p0);
+      }
     }
     for (int q = w; q < llc.count(); q += nw) {
       const int j = llc.line(q), k = j - sc.lo;
@@ -781,10 +843,19 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       if (lane == 0) col_upd(j, Q, l);
     }
     xchg_end(cl, xb, CL, me);
-    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
-      const int k = i - sr.lo;
-      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
-      if (p1 - p0 <= kRegLine) row_upd(i, seg_dot(R, p0, p1, bv), l, p1 == p0);
+    if (rperm) {
+      for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+        const int k = rperm[t], i = sr.lo + k;
+        const uint32_t p0 = R.off[k], p1 = R.off[k + 1], Ln = p1 - p0;
+        const uint32_t wmax = __reduce_max_sync(__activemask(), Ln <= kRegLine ? Ln : 0u);
+        if (Ln <= kRegLine) row_upd(i, seg_dot_adapt(R, p0, p1, bv, wmax), l, Ln == 0);
+      }
+    } else {
+      for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+        const int k = i - sr.lo;
+        const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+        if (p1 - p0 <= kRegLine) row_upd(i, seg_dot(R, p0, p1, bv), l, p1 == p0);
+      }
     }
     for (int q = w; q < llr.count(); q += nw) {
       const int i = llr.line(q), k = i - sr.lo;
@@ -1005,24 +1076,24 @@ __device__ __forceinline__ float seg_dot_axpy(const SliceView<IdxT>& V, uint32_t
 //   (l > 1) Rbar^{l-1}_i = -abar_i (a^{l-1}_i)^2, abar_i <- abar_i eps (a^{l-1}_i / a^{l-2}_i)^2;
 //   P0bar_ij += Qbar^l_j a^{l-1}_i  (+ Rbar^{l-1}_i b^{l-1}_j)
 // Returns Rbar^{l-1}_i (0 when l == 1); the caller pushes it.
-template <typename IdxT>
-__device__ __forceinline__ float seg_rev_fused(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* q,
-                                               const float* bprev, float alm, float almm, float& abk, float eps) {
+template <int KB, typename IdxT>
+__device__ __forceinline__ float seg_rev_fused_n(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* q,
+                                                 const float* bprev, float alm, float almm, float& abk, float eps) {
   const uint32_t n = p1 - p0;
-  uint32_t ix[kRegLine];
-  float g[kRegLine];
+  uint32_t ix[KB];
+  float g[KB];
   float t[4] = {0.f, 0.f, 0.f, 0.f};
   {
-    float v[kRegLine];
+    float v[KB];
 #pragma unroll
-    for (uint32_t u = 0; u < kRegLine; ++u) {
+    for (uint32_t u = 0; u < KB; ++u) {
       ix[u] = u < n ? V.col(p0 + u) : 0u;
       v[u] = u < n ? V.val[p0 + u] : 0.f;
     }
 #pragma unroll
-    for (uint32_t u = 0; u < kRegLine; ++u) g[u] = u < n ? q[ix[u]] : 0.f;
+    for (uint32_t u = 0; u < KB; ++u) g[u] = u < n ? q[ix[u]] : 0.f;
 #pragma unroll
-    for (uint32_t u = 0; u < kRegLine; ++u)
+    for (uint32_t u = 0; u < KB; ++u)
       if (u < n) t[u & 3] = __fmaf_rn(g[u], v[u], t[u & 3]);
   }
   abk += (t[0] + t[1]) + (t[2] + t[3]);
@@ -1032,16 +1103,24 @@ __device__ __forceinline__ float seg_rev_fused(const SliceView<IdxT>& V, uint32_
     Rb = -abk * alm * alm;
     abk = abk * eps * r * r;
   }
-  float bp[kRegLine], c[kRegLine];
+  float bp[KB], c[KB];
 #pragma unroll
-  for (uint32_t u = 0; u < kRegLine; ++u) {
+  for (uint32_t u = 0; u < KB; ++u) {
     bp[u] = (u < n && bprev) ? bprev[ix[u]] : 0.f;
     c[u] = u < n ? V.acc[p0 + u] : 0.f;
   }
 #pragma unroll
-  for (uint32_t u = 0; u < kRegLine; ++u)
+  for (uint32_t u = 0; u < KB; ++u)
     if (u < n) V.acc[p0 + u] = (c[u] + g[u] * alm) + Rb * bp[u];
   return Rb;
+}
+template <typename IdxT>
+__device__ __forceinline__ float seg_rev_fused(const SliceView<IdxT>& V, uint32_t p0, uint32_t p1, const float* q,
+                                               const float* bprev, float alm, float almm, float& abk, float eps,
+                                               uint32_t wmax = kRegLine) {
+  if (wmax <= 4) return seg_rev_fused_n<4>(V, p0, p1, q, bprev, alm, almm, abk, eps);
+  if (wmax <= 8) return seg_rev_fused_n<8>(V, p0, p1, q, bprev, alm, almm, abk, eps);
+  return seg_rev_fused_n<kRegLine>(V, p0, p1, q, bprev, alm, almm, abk, eps);
 }
 
 // Reverse Sinkhorn in scaling form; P0bar accumulated per CSR entry of the own
@@ -1050,7 +1129,8 @@ template <typename IdxT, bool kSm>
 __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, Slice sr, Slice sc,
                              const SliceView<IdxT>& R, const SliceView<IdxT>& C, float* ab, float* bb,
                              Xchg& xr, Xchg& xq, float* bls, const float* ahs, const float* bhs,
-                             const LongList& llr, const LongList& llc) {
+                             const LongList& llr, const LongList& llc, const uint16_t* rperm = nullptr,
+                             const uint16_t* cperm = nullptr) {
   // kSm: slices (+ acc), replicas, abar / bbar and the staged history all in shared memory
   if (kSm) {
     assume_smem(R);
@@ -1141,7 +1221,14 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
       bb[k] = bsum * A.eps * r * r;
       xchg_put(xq, CL, j, -bsum * bl * bl);
     };
-    {
+    if (cperm) {  // lines ordered by length (single-CTA clusters): adaptive batch
+      for (int t = threadIdx.x; t < sc.hi - sc.lo; t += blockDim.x) {
+        const int k = cperm[t], j = sc.lo + k;
+        const uint32_t p0 = C.off[k], p1 = C.off[k + 1], Ln = p1 - p0;
+        const uint32_t wmax = __reduce_max_sync(__activemask(), Ln <= kRegLine ? Ln : 0u);
+        if (Ln <= kRegLine) col_rev(j, k, seg_dot_adapt(C, p0, p1, rcur, wmax), bh[(size_t)(l - 1) * M + j]);
+      }
+    } else {
       int u = 0;
       for (int j = sc.lo + threadIdx.x; j < sc.hi; j += blockDim.x, ++u) {
         const int k = j - sc.lo;
@@ -1173,16 +1260,31 @@ __device__ void sinkhorn_bwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
     // row step 2 of l: abar += P0 Qbar^l, P0bar_ij += Qbar^l_j a^{l-1}_i -- fused with the
     // row step of l-1 (Rbar^{l-1} pushed for the next column step)
     const float* bprev = l > 1 ? (bls ? bls + ((l - 1) & 1) * M : bh + (size_t)(l - 1) * M) : nullptr;
-    for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
-      const int k = i - sr.lo;
-      const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
-      if (p1 - p0 > kRegLine) continue;
-      const float alm = ah[(size_t)(l - 1) * ald + i];
-      const float almm = l > 1 ? ah[(size_t)(l - 2) * ald + i] : 1.f;
-      float abk = ab[k];
-      const float Rb = seg_rev_fused(R, p0, p1, qcur, bprev, alm, almm, abk, A.eps);
-      ab[k] = abk;
-      if (l > 1) xchg_put(xr, CL, i, Rb);
+    if (rperm) {
+      for (int t = threadIdx.x; t < sr.hi - sr.lo; t += blockDim.x) {
+        const int k = rperm[t], i = sr.lo + k;
+        const uint32_t p0 = R.off[k], p1 = R.off[k + 1], Ln = p1 - p0;
+        const uint32_t wmax = __reduce_max_sync(__activemask(), Ln <= kRegLine ? Ln : 0u);
+        if (Ln > kRegLine) continue;
+        const float alm = ah[(size_t)(l - 1) * ald + i];
+        const float almm = l > 1 ? ah[(size_t)(l - 2) * ald + i] : 1.f;
+        float abk = ab[k];
+        const float Rb = seg_rev_fused(R, p0, p1, qcur, bprev, alm, almm, abk, A.eps, wmax);
+        ab[k] = abk;
+        if (l > 1) xchg_put(xr, CL, i, Rb);
+      }
+    } else {
+      for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {
+        const int k = i - sr.lo;
+        const uint32_t p0 = R.off[k], p1 = R.off[k + 1];
+        if (p1 - p0 > kRegLine) continue;
+        const float alm = ah[(size_t)(l - 1) * ald + i];
+        const float almm = l > 1 ? ah[(size_t)(l - 2) * ald + i] : 1.f;
+        float abk = ab[k];
+        const float Rb = seg_rev_fused_n<kRegLine>(R, p0, p1, qcur, bprev, alm, almm, abk, A.eps);
+        ab[k] = abk;
+        if (l > 1) xchg_put(xr, CL, i, Rb);
+      }
     }
     for (int q = w; q < llr.count(); q += nw) {
       const int i = llr.line(q), k = i - sr.lo;
