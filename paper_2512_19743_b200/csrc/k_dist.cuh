@@ -373,39 +373,63 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
     const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
     const float4* pE = reinterpret_cast<const float4*>(sE);
     const float4* pR = reinterpret_cast<const float4*>(sR);
+    // Blocks of 32 columns: the hit test only sets bits of a per-(lane, owned point) mask
+    // (no branch, no vote per 4 columns); after the block, the lanes with hits recompute
+    // those few d2 (same operation sequence, same bits) and queue them, warp-synchronously so
+    // that a nearly full queue can be flushed collectively.
+    for (int blk = 0; blk < kTQ / 32; ++blk) {
+      uint32_t mask[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) mask[r] = 0u;
 #pragma unroll 2
-    for (int qq = 0; qq < kTQ / 4; ++qq) {
-      const ulonglong2 qx = px[qq], qy = py[qq], qz = pz[qq];
-      const float4 ce = pE[qq];
+      for (int qq = 8 * blk; qq < 8 * blk + 8; ++qq) {
+        const ulonglong2 qx = px[qq], qy = py[qq], qz = pz[qq];
+        const float4 ce = pE[qq];
+        const int sh = 4 * (qq - 8 * blk);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
+          const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
+          float d[4];
+          f2_unpack(d01, d[0], d[1]);
+          f2_unpack(d23, d[2], d[3]);
+          const uint32_t h = (d[0] <= fmaxf(rE2[r], ce.x) ? 1u : 0u) | (d[1] <= fmaxf(rE2[r], ce.y) ? 2u : 0u) |
+                             (d[2] <= fmaxf(rE2[r], ce.z) ? 4u : 0u) | (d[3] <= fmaxf(rE2[r], ce.w) ? 8u : 0u);
+          mask[r] |= h << sh;
+        }
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const f2_t d01 = f2_dist2(qx.x, qy.x, qz.x, nx[r], ny[r], nz[r]);
-        const f2_t d23 = f2_dist2(qx.y, qy.y, qz.y, nx[r], ny[r], nz[r]);
-        float d[4];
-        f2_unpack(d01, d[0], d[1]);
-        f2_unpack(d23, d[2], d[3]);
-        const bool h0 = d[0] <= fmaxf(rE2[r], ce.x), h1 = d[1] <= fmaxf(rE2[r], ce.y);
-        const bool h2 = d[2] <= fmaxf(rE2[r], ce.z), h3 = d[3] <= fmaxf(rE2[r], ce.w);
-        if (h0 | h1 | h2 | h3) {  // rare per lane (~1 %): this lane's hits only
-          const uint32_t i = base + r * kSweepThreads;
-          const float4 cr = pR[qq];
-          const bool hh[4] = {h0, h1, h2, h3};
-          const float crv[4] = {cr.x, cr.y, cr.z, cr.w};
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t j = jt + 4 * qq + c;
-            if (hh[c] && i < nreal && j < mreal) {
-              const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= crv[c] ? kFlagCol : 0u);
+        const uint32_t i = base + r * kSweepThreads;
+        uint32_t m = i < nreal ? mask[r] : 0u;
+        float xr, yr, zr;  // -x of the owned point (exactly the packed operand)
+        {
+          float t;
+          f2_unpack(nx[r], xr, t);
+          f2_unpack(ny[r], yr, t);
+          f2_unpack(nz[r], zr, t);
+        }
+        while (__any_sync(0xffffffffu, m)) {
+          if (__any_sync(0xffffffffu, qn == kLaneQ)) {
+            __syncwarp();
+            lane_flush(b, q, qn, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+            qn = 0;
+            __syncwarp();
+          }
+          if (m) {
+            const int c = 32 * blk + __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t j = jt + c;
+            if (j < mreal) {
+              const float dx = __fadd_rn(sx[c], xr), dy = __fadd_rn(sy[c], yr), dz = __fadd_rn(sz[c], zr);
+              float d2 = __fmul_rn(dx, dx);
+              d2 = __fmaf_rn(dy, dy, d2);
+              d2 = __fmaf_rn(dz, dz, d2);
+              const uint32_t fl = (d2 <= rR2[r] ? kFlagRow : 0u) | (d2 <= sR[c] ? kFlagCol : 0u);
               q[qn * 32] = make_uint2(i, j | fl);
               ++qn;
             }
           }
-        }
-        if (__any_sync(0xffffffffu, qn > kLaneQ - 4)) {  // warp-uniform; a step adds <= 4
-          __syncwarp();
-          lane_flush(b, q, qn, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
-          qn = 0;
-          __syncwarp();
         }
       }
     }
