@@ -424,7 +424,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
   const int* jp = gperm + (size_t)b * mp;
   __shared__ __align__(16) float s_t[kW][5][kTQ];
   __shared__ __align__(16) int s_j[kW][kTQ];
-  __shared__ uint2 wbuf_all[kW][kWarpBuf];
+  __shared__ uint2 queue_all[kW][kLaneQ][32];  // per-lane emission queues (as k_emit)
   __shared__ float s_gbox[kW][R][6], s_ge[kW][R];
   float* tx = s_t[w][0];
   float* ty = s_t[w][1];
@@ -432,8 +432,8 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
   float* sR = s_t[w][3];
   float* sE = s_t[w][4];
   int* sJ = s_j[w];
-  uint2* wbuf = wbuf_all[w];
-  int wcnt = 0;
+  uint2* qp = &queue_all[w][0][lane];
+  int qn = 0;
 
   f2_t nx[R], ny[R], nz[R];
   float rR2[R], rE2[R];
@@ -462,7 +462,6 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
     if (lane == 0) s_ge[w][r] = ge;
   }
   __syncwarp();
-  const unsigned lt_mask = (1u << lane) - 1u;
   unsigned nev = 0;
   for (int base = 0; base < nt; base += 32) {
     const int T = base + lane;
@@ -506,6 +505,9 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!((fm >> (r * kSubPerTile + q)) & 1u)) continue;  // warp-uniform
+          // hit mask over the 32 points of the sub-tile (no branch / vote per 4 points), then
+          // the lanes' hits recomputed (same bits) and queued warp-synchronously (as k_emit)
+          uint32_t mask = 0u;
 #pragma unroll 2
           for (int k = 0; k < kSub / 4; ++k) {
             const ulonglong2 qx = px[k], qy = py[k], qz = pz[k];
@@ -515,25 +517,35 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
             float d[4];
             f2_unpack(d01, d[0], d[1]);
             f2_unpack(d23, d[2], d[3]);
-            const bool hit = (d[0] <= fmaxf(rE2[r], ce.x)) | (d[1] <= fmaxf(rE2[r], ce.y)) |
-                             (d[2] <= fmaxf(rE2[r], ce.z)) | (d[3] <= fmaxf(rE2[r], ce.w));
-            if (__any_sync(0xffffffffu, hit)) {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const int qq = q * kSub + 4 * k + c;
-                const int j = sJ[qq];
-                const bool h = d[c] <= fmaxf(rE2[r], sE[qq]) && oi[r] >= 0 && j >= 0;
-                const unsigned bal = __ballot_sync(0xffffffffu, h);
-                if (h) {
-                  const uint32_t fl = (d[c] <= rR2[r] ? kFlagRow : 0u) | (d[c] <= sR[qq] ? kFlagCol : 0u);
-                  wbuf[wcnt + __popc(bal & lt_mask)] = make_uint2((uint32_t)oi[r], (uint32_t)j | fl);
-                }
-                wcnt += __popc(bal);
-              }
-              if (wcnt > kFlushAt) {
-                __syncwarp();
-                warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
-                wcnt = 0;
+            const uint32_t h = (d[0] <= fmaxf(rE2[r], ce.x) ? 1u : 0u) | (d[1] <= fmaxf(rE2[r], ce.y) ? 2u : 0u) |
+                               (d[2] <= fmaxf(rE2[r], ce.z) ? 4u : 0u) | (d[3] <= fmaxf(rE2[r], ce.w) ? 8u : 0u);
+            mask |= h << (4 * k);
+          }
+          uint32_t m = oi[r] >= 0 ? mask : 0u;
+          if (!__any_sync(0xffffffffu, m)) continue;
+          float xr, yr, zr, tmp;
+          f2_unpack(nx[r], xr, tmp);
+          f2_unpack(ny[r], yr, tmp);
+          f2_unpack(nz[r], zr, tmp);
+          while (__any_sync(0xffffffffu, m)) {
+            if (__any_sync(0xffffffffu, qn == kLaneQ)) {
+              __syncwarp();
+              lane_flush(b, qp, qn, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+              qn = 0;
+              __syncwarp();
+            }
+            if (m) {
+              const int qq = q * kSub + __ffs(m) - 1;
+              m &= m - 1;
+              const int j = sJ[qq];
+              if (j >= 0) {
+                const float dx = __fadd_rn(tx[qq], xr), dy = __fadd_rn(ty[qq], yr), dz = __fadd_rn(tz[qq], zr);
+                float d2 = __fmul_rn(dx, dx);
+                d2 = __fmaf_rn(dy, dy, d2);
+                d2 = __fmaf_rn(dz, dz, d2);
+                const uint32_t fl = (d2 <= rR2[r] ? kFlagRow : 0u) | (d2 <= sR[qq] ? kFlagCol : 0u);
+                qp[qn * 32] = make_uint2((uint32_t)oi[r], (uint32_t)j | fl);
+                ++qn;
               }
             }
           }
@@ -543,7 +555,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
     }
   }
   __syncwarp();
-  if (wcnt) warp_flush(b, wbuf, wcnt, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
+  lane_flush(b, qp, qn, cap, ebuf, cursor, aux_cnt, row_cnt, N, col_cnt, M);
   if (evals && lane == 0 && nev) atomicAdd(evals, (unsigned long long)nev * 32ull * kSub);
 }
 

@@ -252,38 +252,9 @@ __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int
             d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
 }
 
-// Emission staging: each warp compacts its hits into a shared-memory buffer (ballot +
-// popc, no atomics) and flushes it to the pair's segment with ONE returning global atomic
-// per flush; the per-line counts are non-returning reductions (RED).  Counts keep running
-// past the capacity so the host can size a retry; overflowed pairs are skipped downstream.
-constexpr int kWarpBuf = 512;                  // staged entries per warp
-constexpr int kFlushAt = kWarpBuf - 32 * 4;    // worst case of one (row, 4 columns) step
-
-__device__ __forceinline__ void warp_flush(int b, uint2* wbuf, int n, uint32_t cap,
-                                           uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
-                                           unsigned* __restrict__ aux_cnt,
-                                           unsigned* __restrict__ row_cnt, int N,
-                                           unsigned* __restrict__ col_cnt, int M) {
-  const int lane = threadIdx.x & 31;
-  unsigned base = 0;
-  if (lane == 0) base = atomicAdd(cursor + b, (unsigned)n);
-  base = __shfl_sync(0xffffffffu, base, 0);
-  unsigned aux = 0;
-  for (int k = lane; k < n; k += 32) {
-    const uint2 e = wbuf[k];
-    const unsigned pos = base + k;
-    if (pos < cap) ebuf[(size_t)b * cap + pos] = e;
-    const uint32_t j = e.y & kIdxMask;
-    atomicAdd(row_cnt + (size_t)b * (N + 1) + e.x, 1u);
-    atomicAdd(col_cnt + (size_t)b * (M + 1) + j, 1u);
-    aux += (e.y & (kFlagRow | kFlagCol)) ? 0u : 1u;
-  }
-  aux = __reduce_add_sync(0xffffffffu, aux);
-  if (lane == 0 && aux) atomicAdd(aux_cnt + b, aux);
-  __syncwarp();
-}
-
-// Per-lane emission queues (k_emit): every lane appends its own hits to its own slots of a
+// Emission (S3).  Counts keep running past the capacity so the host can size a retry;
+// overflowed pairs are skipped downstream; the per-line counts are non-returning reductions.
+// Per-lane emission queues (k_emit, k_emit_cull): every lane appends its own hits to its own slots of a
 // shared-memory queue with no cross-lane communication (the common case -- a warp with a hit
 // somewhere in a 4-column step -- used to cost 4 ballots + popcounts + a serialised compaction
 // per step); the warp flushes all queues with one shuffle scan and one returning atomic when a
