@@ -245,28 +245,34 @@ __device__ float line_softmax(const SparseArgs& A, int b, const Side& S, int lin
     return dist2(x.x, x.y, x.z, own.x, own.y, own.z);  // same operand order as the rows
   };
   if (G == 1) {
-    uint32_t ix[kRegLine];
-    float d2[kRegLine];
-#pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) ix[r] = r < L ? S.idx[beg + r] : 0u;
-#pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) d2[r] = r < L ? d2_of(ix[r]) : 0.f;
+    // chunks of 8 entries in sorted order (one batched gather each; most lines need one):
+    // half the unrolled code of a 16-wide batch -- this phase runs once per launch, so its
+    // instruction fetch (ncu: no_instruction stalls) matters more than a second round trip
+    constexpr uint32_t kC = 8;
     int ia = -1, ib = -1;
     float Z = 0.f;
+    for (uint32_t r0 = 0; r0 < L; r0 += kC) {
+      uint32_t ix[kC];
+      float d2[kC];
 #pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) {
-      if (r < L) {
-        const int o = (int)(ix[r] & kIdxMask);
-        if (ia < 0 && d2[r] == la.m2) ia = o;
-        else if (ib < 0 && d2[r] == la.s2) ib = o;
-        const float c = __fsqrt_rn(d2[r]);
-        float s = 0.f;
-        if (ix[r] & fl) {
-          s = line_sim(c, lb);
-          Z += s;
+      for (uint32_t r = 0; r < kC; ++r) ix[r] = r0 + r < L ? S.idx[beg + r0 + r] : 0u;
+#pragma unroll
+      for (uint32_t r = 0; r < kC; ++r) d2[r] = r0 + r < L ? d2_of(ix[r]) : 0.f;
+#pragma unroll
+      for (uint32_t r = 0; r < kC; ++r) {
+        if (r0 + r < L) {
+          const int o = (int)(ix[r] & kIdxMask);
+          if (ia < 0 && d2[r] == la.m2) ia = o;
+          else if (ib < 0 && d2[r] == la.s2) ib = o;
+          const float c = __fsqrt_rn(d2[r]);
+          float s = 0.f;
+          if (ix[r] & fl) {
+            s = line_sim(c, lb);
+            Z += s;
+          }
+          S.c[beg + r0 + r] = c;
+          S.pr[beg + r0 + r] = s;
         }
-        S.c[beg + r] = c;
-        S.pr[beg + r] = s;
       }
     }
     *argidx = make_int2(ia, ib);
