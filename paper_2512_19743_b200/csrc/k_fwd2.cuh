@@ -83,11 +83,12 @@ __device__ unsigned block_scan(const unsigned* cnt, int n, unsigned* off, unsign
 }
 
 // Lines of a slice longer than kRegLine (local offsets), as collect_long.
-__device__ LongList collect_long_local(const unsigned* off, Slice s, uint32_t* list, int* cnt) {
+__device__ LongList collect_long_local(const unsigned* off, Slice s, uint32_t* list, int* cnt,
+                                       uint32_t thresh = kRegLine) {
   if (threadIdx.x == 0) *cnt = 0;
   __syncthreads();
   for (int k = threadIdx.x; k < s.hi - s.lo; k += blockDim.x)
-    if (off[k + 1] - off[k] > kRegLine) {
+    if (off[k + 1] - off[k] > thresh) {
       const int q = atomicAdd(cnt, 1);
       if (q < kLongCap) list[q] = (uint32_t)(s.lo + k);
     }
@@ -118,21 +119,21 @@ __device__ __forceinline__ uint32_t sort_key(const SparseArgs& A, int b, uint32_
   return kRows ? orig_col(A, b, idx & kIdxMask) : orig_row(A, b, idx & kIdxMask);
 }
 
-template <bool kRows>
+template <bool kRows, uint32_t KR = kRegLine>
 __device__ void sort_line_regs(const SparseArgs& A, int b, const Side& S, uint32_t beg, uint32_t L, uint32_t gbase) {
-  uint32_t ix[kRegLine], tt[kRegLine], ok[kRegLine];
+  uint32_t ix[KR], tt[KR], ok[KR];
 #pragma unroll
-  for (uint32_t k = 0; k < kRegLine; ++k) {
+  for (uint32_t k = 0; k < KR; ++k) {
     ix[k] = k < L ? S.idx[beg + k] : 0u;
     tt[k] = k < L ? S.t[beg + k] : 0u;
   }
 #pragma unroll
-  for (uint32_t k = 0; k < kRegLine; ++k) ok[k] = k < L ? sort_key<kRows>(A, b, ix[k]) : 0xffffffffu;
+  for (uint32_t k = 0; k < KR; ++k) ok[k] = k < L ? sort_key<kRows>(A, b, ix[k]) : 0xffffffffu;
 #pragma unroll
-  for (uint32_t k = 0; k < kRegLine; ++k) {
+  for (uint32_t k = 0; k < KR; ++k) {
     uint32_t r = 0;
 #pragma unroll
-    for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
+    for (uint32_t f = 0; f < KR; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
     if (k < L) {
       S.idx[beg + r] = ix[k];
       S.t[beg + r] = tt[k];
@@ -492,31 +493,44 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
   __syncthreads();
   phase(A, 2);
 
-  // ---- S4c: order every line by original index of the other cloud (CSR: also A.inv)
-  const LongList llr = collect_long_local(roff, sr, s_long_r, &s_nlong[0]);
-  const LongList llc = collect_long_local(coff, sc, s_long_c, &s_nlong[1]);
-  for (int k = threadIdx.x; k < nr; k += blockDim.x) {
-    const uint32_t beg = roff[k], Ln = roff[k + 1] - beg;
-    if (Ln <= kRegLine) sort_line_regs<true>(A, b, R, beg, Ln, gr);
-  }
-  for (int k = threadIdx.x; k < nc; k += blockDim.x) {
-    const uint32_t beg = coff[k], Ln = coff[k + 1] - beg;
-    if (Ln <= kRegLine) sort_line_regs<false>(A, b, C, beg, Ln, gc);
-  }
+  // ---- S4c: order every line by original index of the other cloud (CSR: also A.inv).
+  // Lines of <= 8 entries (most) by one thread in registers (8 x 8 rank counts: a quarter of
+  // the once-per-launch code of 16 x 16), longer ones by a warp.
+  // (mean line length > 6 entries, e.g. the MM-Fi columns of C3: the 16-wide register path,
+  // so that the warp path stays rare)
   {
-    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int q = w; q < llr.count(); q += nw) {
-      const int k = llr.line(q) - sr.lo;
+    const bool narrow = (uint64_t)(nnzr + nnzc) <= 6ull * (uint64_t)(nr + nc);
+    const uint32_t kSortReg = narrow ? 8u : kRegLine;
+    const LongList slr = collect_long_local(roff, sr, s_long_r, &s_nlong[0], kSortReg);
+    const LongList slc = collect_long_local(coff, sc, s_long_c, &s_nlong[1], kSortReg);
+    for (int k = threadIdx.x; k < nr; k += blockDim.x) {
       const uint32_t beg = roff[k], Ln = roff[k + 1] - beg;
-      if (Ln > kRegLine) sort_line_warp<true>(A, b, R, beg, Ln, gr);
+      if (Ln > kSortReg) continue;
+      if (narrow) sort_line_regs<true, 8>(A, b, R, beg, Ln, gr);
+      else sort_line_regs<true>(A, b, R, beg, Ln, gr);
     }
-    for (int q = w; q < llc.count(); q += nw) {
-      const int k = llc.line(q) - sc.lo;
+    for (int k = threadIdx.x; k < nc; k += blockDim.x) {
       const uint32_t beg = coff[k], Ln = coff[k + 1] - beg;
-      if (Ln > kRegLine) sort_line_warp<false>(A, b, C, beg, Ln, gc);
+      if (Ln > kSortReg) continue;
+      if (narrow) sort_line_regs<false, 8>(A, b, C, beg, Ln, gc);
+      else sort_line_regs<false>(A, b, C, beg, Ln, gc);
+    }
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int q = w; q < slr.count(); q += nw) {
+      const int k = slr.line(q) - sr.lo;
+      const uint32_t beg = roff[k], Ln = roff[k + 1] - beg;
+      if (Ln > kSortReg) sort_line_warp<true>(A, b, R, beg, Ln, gr);
+    }
+    for (int q = w; q < slc.count(); q += nw) {
+      const int k = slc.line(q) - sc.lo;
+      const uint32_t beg = coff[k], Ln = coff[k + 1] - beg;
+      if (Ln > kSortReg) sort_line_warp<false>(A, b, C, beg, Ln, gc);
     }
   }
   csync(cl);  // A.inv complete for the whole pair
+  // the long-line lists of the later phases (lines of more than kRegLine entries)
+  const LongList llr = collect_long_local(roff, sr, s_long_r, &s_nlong[0]);
+  const LongList llc = collect_long_local(coff, sc, s_long_c, &s_nlong[1]);
   phase(A, 3);
   // CSR position of every CSC entry (the backward's column passes); frees C.t for c
   for (uint32_t q0 = threadIdx.x; q0 < nnzc; q0 += 4 * blockDim.x) {
