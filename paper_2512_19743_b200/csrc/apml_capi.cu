@@ -428,6 +428,7 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.rowback = c->rowback; a.colback = c->colback;
   a.loss = loss; a.grad_loss = grad_loss; a.grad_pred = grad_pred;
   a.smem_bytes = c->smem_bytes; a.rep_smem = c->rep_smem;
+  a.bhs_stage = (int)env_long("APML_BHS", 1);
   a.dbg = nullptr;
   a.row_offset = (int)c->row_offset; a.colred = c->colred; a.cand = c->cand;
   a.pperm = c->relabel ? c->pperm : nullptr;

@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
     ahs = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(L + 1) * nr));
     const float* ahg = A.a_hist + (size_t)b * (L + 1) * N;
     for (int l = 0; l <= L; ++l) g2s_async(ahs + (size_t)l * nr, ahg + (size_t)l * N + sr.lo, nr);
-    if ((size_t)(sm - shm) + 4 * (size_t)(L + 1) * M + 16 <= A.smem_bytes) {
+    if (A.bhs_stage && (size_t)(sm - shm) + 4 * (size_t)(L + 1) * M + 16 <= A.smem_bytes) {
       bhs = reinterpret_cast<float*>(carve(sm, 4 * (size_t)(L + 1) * M));
       g2s_async(bhs, A.b_hist + (size_t)b * (L + 1) * M, (size_t)(L + 1) * M);
     }

@@ -80,6 +80,7 @@ struct SparseArgs {
   float* grad_gt;  // optional [B][M][3]
   size_t smem_bytes;
   int rep_smem;
+  int bhs_stage;  // k_sparse_bwd2: stage the whole b history in shared memory (APML_BHS, default 1)
   unsigned long long* dbg;  // optional phase timestamps [grid][16] (APML_PHASES=1), else NULL
   // row-sharded mode (k_rowshard.cuh): global index of local row 0, column partial sums /
   // argmin candidates exchanged through the caller's collectives
