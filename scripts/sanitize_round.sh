@@ -1,0 +1,32 @@
+#!/bin/bash
+# compute-sanitizer memcheck (and racecheck on shared memory) over the current default paths:
+# fwd2/bwd2 cluster kernels (C2-like, CL = 4), single-CTA clusters (C3-like), ragged, culled
+# sweeps + grid sparse stage, the plan + grad w.r.t. gt.  Small sizes (sanitizer is slow).
+mkdir -p gpurun_out
+cat > /tmp/san2.py <<'PY'
+import os, sys; sys.path.insert(0, os.environ['REPO'])
+import torch
+from paper_2512_19743_b200 import Config, forward, Plan
+from synth import clouds
+kind, B, N, M = os.environ["KIND"], int(os.environ["B"]), int(os.environ["NN"]), int(os.environ["MM"])
+x, y = clouds.batch(kind, B, N, M, 5)
+p, g = torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda")
+ns = ms = None
+if os.environ.get("RAGGED"):
+    ns = [N - 37 * b for b in range(B)]; ms = [M - 11 * b for b in range(B)]
+loss, ctx = forward(p, g, Config(), n_sizes=ns, m_sizes=ms)
+gp, gg = ctx.backward(torch.ones(B, device="cuda"), want_gt=True)
+if os.environ.get("PLAN"):
+    pl = Plan(B, N, M, Config(sync_check=False))
+    pl.forward(p, g); pl.backward(torch.ones(B, device="cuda"))
+torch.cuda.synchronize()
+print("ok", float(loss.sum()), float(gp.abs().sum()), float(gg.abs().sum()))
+PY
+run() { echo "== $*"; env REPO=$PWD "$@" compute-sanitizer --tool memcheck --show-backtrace no --print-limit 5 python /tmp/san2.py 2>&1 | tail -4; }
+run KIND=shapenet B=4 NN=1024 MM=1024 PLAN=1
+run KIND=mmfi B=2 NN=1024 MM=512 APML_CL=1
+run KIND=mmfi B=3 NN=700 MM=520 RAGGED=1
+run KIND=uniform B=2 NN=4500 MM=4200 APML_CULL=1
+run KIND=uniform B=2 NN=700 MM=650 APML_FWD2=0
+echo "== racecheck (shared memory), fwd2/bwd2 CL=1"
+env REPO=$PWD KIND=mmfi B=1 NN=512 MM=256 APML_CL=1 compute-sanitizer --tool racecheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -6
