@@ -550,11 +550,25 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->pcb, c->pfb);
   k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
   mark(c, 1, s);
-  k_line_top2_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
-      c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r, c->clamp + 1);
-  mark(c, 2, s);
-  k_line_top2_cull<kRc><<<dim3(Mp / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
-      c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c, c->clamp + 2);
+  // both directions in one launch (the stage marks 2 and 3 bracket it together)
+  if (env_long("APML_CULL_BOTH", 1)) {
+    const CullDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gcb, c->gfb, c->part_r, c->clamp + 1,
+                     (int)(Np / (kSweepThreads * kRc))};
+    const CullDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pcb, c->pfb, c->part_c, c->clamp + 2,
+                     (int)(Mp / (kSweepThreads * kRc))};
+    k_line_top2_cull_both<kRc><<<dim3(std::max(dr.nblk, dc.nblk), B, 2), kSweepThreads, 0, s>>>(dr, dc,
+                                                                                             (int)c->relabel);
+    c->passA_fused = true;
+    mark(c, 2, s);
+    c->launches -= 1;
+  } else {
+    k_line_top2_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
+        c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r, c->clamp + 1);
+    mark(c, 2, s);
+    k_line_top2_cull<kRc><<<dim3(Mp / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
+        c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c, c->clamp + 2);
+    c->passA_fused = false;
+  }
   c->launches += 11;  // + the scan's own
   CK(cudaGetLastError());
   return APML_OK;

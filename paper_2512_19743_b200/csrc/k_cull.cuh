@@ -262,13 +262,14 @@ __device__ __forceinline__ void stage_tile_xyz(const float* __restrict__ str, in
 // Tiles are visited in a ring around the warp's own position in Morton order so the bounds
 // (largest current second minimum of each group) tighten after the first few tiles.
 template <int R>
-__global__ void __launch_bounds__(kSweepThreads)
-k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const int* __restrict__ own_perm,
-                 const float* __restrict__ str_soa, int str_np, const float* __restrict__ str_cb,
-                 const float* __restrict__ str_fb, int relabel, float2* __restrict__ out,
-                 unsigned long long* __restrict__ evals) {
+__device__ __forceinline__ void top2_cull_block(const float* __restrict__ own_soa, int own_np, int own_n,
+                                                const int* __restrict__ own_perm, const float* __restrict__ str_soa,
+                                                int str_np, const float* __restrict__ str_cb,
+                                                const float* __restrict__ str_fb, int relabel,
+                                                float2* __restrict__ out, unsigned long long* __restrict__ evals,
+                                                const int blk, const int b) {
   constexpr int kW = kSweepThreads / 32;
-  const int b = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = own_soa + (size_t)b * 3 * own_np;
   const float* str = str_soa + (size_t)b * 3 * str_np;
   const int nt = str_np / kTQ;
@@ -286,7 +287,7 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
   float wbox[6] = {3e38f, 3e38f, 3e38f, -3e38f, -3e38f, -3e38f};
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int idx = cull_idx<R>(blockIdx.x, r);
+    const int idx = cull_idx<R>(blk, r);
     valid[r] = idx < own_n;
     const float x = __ldg(own + idx), y = __ldg(own + own_np + idx), z = __ldg(own + 2 * own_np + idx);
     nx[r] = f2_pack(-x, -x); ny[r] = f2_pack(-y, -y); nz[r] = f2_pack(-z, -z);
@@ -305,7 +306,7 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
   for (int r = 0; r < R; ++r) wmax = fmaxf(wmax, gmax[r]);
 
   unsigned nev = 0;
-  const int own_base = blockIdx.x * kSweepThreads * R + w * 32 * R;
+  const int own_base = blk * kSweepThreads * R + w * 32 * R;
   const int t0 = min(nt - 1, (int)((long long)own_base * nt / own_np));
   // Candidate tiles come from a generator (32 ring steps per ballot against the warp bound);
   // the data of the NEXT candidate (its sub-tile box for this lane's (group, sub-tile) test
@@ -393,10 +394,45 @@ k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const
   if (evals && lane == 0 && nev) atomicAdd(evals, (unsigned long long)nev * 32ull * kSub);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int idx = cull_idx<R>(blockIdx.x, r);
+    const int idx = cull_idx<R>(blk, r);
     if (valid[r])
       out[(size_t)b * own_n + (relabel ? idx : own_perm[(size_t)b * own_np + idx])] = make_float2(m[r], s[r]);
   }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads)
+k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const int* __restrict__ own_perm,
+                 const float* __restrict__ str_soa, int str_np, const float* __restrict__ str_cb,
+                 const float* __restrict__ str_fb, int relabel, float2* __restrict__ out,
+                 unsigned long long* __restrict__ evals) {
+  top2_cull_block<R>(own_soa, own_np, own_n, own_perm, str_soa, str_np, str_cb, str_fb, relabel, out, evals,
+                     blockIdx.x, blockIdx.y);
+}
+
+// Both culled Pass A directions in ONE launch (grid.z = 2: rows, then columns).  At B = 1
+// (C5) one direction alone fills under half of the GPU's warp slots, and the walk is
+// latency-bound: the second direction's warps hide the first's latency instead of waiting
+// for their own launch.
+struct CullDir {
+  const float* own;
+  int own_np, own_n;
+  const int* own_perm;
+  const float* str;
+  int str_np;
+  const float* str_cb;
+  const float* str_fb;
+  float2* out;
+  unsigned long long* evals;
+  int nblk;
+};
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads) k_line_top2_cull_both(const CullDir d0, const CullDir d1,
+                                                                       int relabel) {
+  const CullDir& d = blockIdx.z ? d1 : d0;
+  if ((int)blockIdx.x >= d.nblk) return;
+  top2_cull_block<R>(d.own, d.own_np, d.own_n, d.own_perm, d.str, d.str_np, d.str_cb, d.str_fb, relabel, d.out,
+                     d.evals, blockIdx.x, blockIdx.y);
 }
 
 // Culled Pass B: as k_emit over the sorted clouds, evaluating only the (group, sub-tile)
