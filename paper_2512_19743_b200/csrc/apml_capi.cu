@@ -552,12 +552,21 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 1, s);
   // both directions in one launch (the stage marks 2 and 3 bracket it together)
   if (env_long("APML_CULL_BOTH", 1)) {
+    // one 32-point group per warp (finer work units, looser boxes) when the kRc-group grid
+    // would be under ~4 waves (7 resident CTAs per SM at 72 registers): C5 yes, C4 no
+    // (measured: C5 Pass A 0.61 -> 0.58 ms; C4 0.89 -> 0.96 ms with R = 1)
+    const long few = (long)B * (Np + Mp) / (kSweepThreads * kRc) < 28L * num_sms();
+    const int rc = env_long("APML_CULL_RA", few ? 1 : kRc) == 1 ? 1 : kRc;
     const CullDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gcb, c->gfb, c->part_r, c->clamp + 1,
-                     (int)(Np / (kSweepThreads * kRc))};
+                     (int)(Np / (kSweepThreads * rc))};
     const CullDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pcb, c->pfb, c->part_c, c->clamp + 2,
-                     (int)(Mp / (kSweepThreads * kRc))};
-    k_line_top2_cull_both<kRc><<<dim3(std::max(dr.nblk, dc.nblk), B, 2), kSweepThreads, 0, s>>>(dr, dc,
+                     (int)(Mp / (kSweepThreads * rc))};
+    if (rc == 1)
+      k_line_top2_cull_both<1><<<dim3(std::max(dr.nblk, dc.nblk), B, 2), kSweepThreads, 0, s>>>(dr, dc,
                                                                                              (int)c->relabel);
+    else
+      k_line_top2_cull_both<kRc><<<dim3(std::max(dr.nblk, dc.nblk), B, 2), kSweepThreads, 0, s>>>(dr, dc,
+                                                                                               (int)c->relabel);
     c->passA_fused = true;
     mark(c, 2, s);
     c->launches -= 1;
@@ -580,8 +589,8 @@ apml_status launch_emit_cull(apml_ctx* c) {
   k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
                                                c->gfe2);
   k_emit_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
-      c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor, c->aux,
-      c->row_cnt, c->col_cnt, c->clamp + 3);
+      c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor,
+      c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
   c->launches += 2;
   CK(cudaGetLastError());
   return APML_OK;

@@ -264,6 +264,8 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_GRID": "1"},                                          # grid-wide kernels (few, large pairs)
     {"APML_CULL": "1"},                                          # spatially culled sweeps (NEXT-2)
     {"APML_CULL": "1", "APML_GRID": "1"},
+    {"APML_CULL": "1", "APML_CULL_RA": "2"},                     # culled Pass A with 2 groups per warp
+    {"APML_CULL": "1", "APML_CULL_BOTH": "0"},                   # culled Pass A, one launch per direction
     {"APML_FWD2": "0"},                                          # global-memory sparse forward (k_sparse_fwd)
     {"APML_BWD2": "0"},                                          # k_sparse_fwd2 + k_sparse_bwd
     {"APML_SMEM_LIMIT": "60000", "APML_CL": "1"},                # fwd2 / bwd2 slices in global memory
