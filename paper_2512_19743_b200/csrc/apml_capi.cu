@@ -588,9 +588,16 @@ apml_status launch_emit_cull(apml_ctx* c) {
   cudaStream_t s = c->stream;
   k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
                                                c->gfe2);
-  k_emit_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
-      c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf, c->cursor,
-      c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
+  // kRc groups per warp; APML_EMIT_R=1 (one group per warp, as Pass A at C5) measured slower
+  // here: C5 emit 0.532 -> 0.546 ms, C4 0.601 -> 0.648 ms
+  if (env_long("APML_EMIT_R", kRc) == 1)
+    k_emit_cull<1><<<dim3(Np / kSweepThreads, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
+        c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf,
+        c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
+  else
+    k_emit_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
+        c->rowA, c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf,
+        c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
   c->launches += 2;
   CK(cudaGetLastError());
   return APML_OK;

@@ -264,7 +264,7 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_GRID": "1"},                                          # grid-wide kernels (few, large pairs)
     {"APML_CULL": "1"},                                          # spatially culled sweeps (NEXT-2)
     {"APML_CULL": "1", "APML_GRID": "1"},
-    {"APML_CULL": "1", "APML_CULL_RA": "2"},                     # culled Pass A with 2 groups per warp
+    {"APML_CULL": "1", "APML_CULL_RA": "2", "APML_EMIT_R": "1"},  # Pass A 2 groups per warp, emit 1
     {"APML_CULL": "1", "APML_CULL_BOTH": "0"},                   # culled Pass A, one launch per direction
     {"APML_FWD2": "0"},                                          # global-memory sparse forward (k_sparse_fwd)
     {"APML_BWD2": "0"},                                          # k_sparse_fwd2 + k_sparse_bwd
