@@ -238,8 +238,10 @@ long env_long(const char* name, long dflt) {
 
 void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk, int64_t target_div = 1) {
   const int64_t blocks = own_np / kOwnTile * B;
-  // ~4 waves of 4 CTAs / SM (target_div = 2: the two Pass A directions share one launch)
-  const int64_t target = env_long("APML_SPLIT_TARGET", 4LL * num_sms() * 4) / target_div;
+  // ~16 waves of 4 CTAs / SM (target_div = 2: the two Pass A directions share one launch);
+  // measured (APML_SPLIT_TARGET sweep, ms/step): C3 1.274 (4 waves) -> 1.232 (8) / 1.237 (16),
+  // C3R 1.455 -> 1.438 / 1.423; C2, C4 flat
+  const int64_t target = env_long("APML_SPLIT_TARGET", 4LL * num_sms() * 16) / target_div;
   int64_t s = (target + blocks - 1) / blocks;
   const int64_t tiles = str_np / kTQ;
   if (s > tiles) s = tiles;
