@@ -89,6 +89,38 @@ def test_threshold_hand_case():
     assert ln["T"][0] == pytest.approx(math.log(8.0), abs=1e-12)
 
 
+@pytest.mark.parametrize("case", GOLD["gap_clamp"]["cases"])
+def test_gap_clamp_hand_case(case):
+    """P:140 (section III-D): CUDA-APML clamps the gap, g = max(gap, eps_g) (reading R17),
+    hand-derived temperature and row similarities (golden file)."""
+    cfg = OracleConfig(p_min=case["p_min"], delta=case["delta"], eps_g=case["eps_g"],
+                       tau=case["tau"], l_iter=0)
+    P = sparse_forward(case["x"], case["y"], cfg)
+    ln = P.lines(0)
+    assert ln["clamped"][0] == 1
+    assert ln["g"][0] == case["eps_g"]
+    assert ln["T"][0] == pytest.approx(case["T"], rel=1e-12)
+    s = P.support()
+    rowmask = (s["flags"] & 1) > 0
+    want = np.asarray(case["row_s"])
+    kept = case.get("row_kept", list(range(len(want))))
+    assert sorted(s["j"][rowmask].tolist()) == kept
+    want_p = want[kept] / want[kept].sum()
+    got = dict(zip(s["j"][rowmask].tolist(), s["prow"][rowmask].tolist()))
+    for j, p in zip(kept, want_p):
+        assert got[j] == pytest.approx(p, rel=1e-12)
+
+
+def test_gap_clamp_inactive_above_eps_g():
+    """The clamp only acts below eps_g: the same line with eps_g = 0.1 < gap = 0.125 keeps
+    g = 0.125 and T = 8 ln 18 (Eq. (1)), clamped flag 0."""
+    case = GOLD["gap_clamp"]["cases"][0]
+    cfg = OracleConfig(p_min=0.9, delta=0.0, eps_g=0.1, tau=0.0, l_iter=0)
+    ln = sparse_forward(case["x"], case["y"], cfg).lines(0)
+    assert ln["clamped"][0] == 0
+    assert ln["T"][0] == pytest.approx(8 * math.log(18.0), rel=1e-12)
+
+
 def test_k1_lines():
     """Eq. (1) needs K > 1; single-entry lines carry P = 1 (R4).
     N = 1: every column is a K = 1 line, so after Sinkhorn the row spreads evenly: loss =
@@ -272,6 +304,69 @@ def test_backward_vs_torch_autograd(NM, tau, p, mode):
     assert P.loss == pytest.approx(lt.item(), rel=1e-12)
     np.testing.assert_allclose(gx, xt.grad.numpy(), rtol=1e-8, atol=1e-10)
     np.testing.assert_allclose(gy, yt.grad.numpy(), rtol=1e-8, atol=1e-10)
+
+
+def _median_gap(x, y, delta):
+    """Median over all rows and columns of c~(2) + delta, from the distance matrix (test-only)."""
+    C = _cost(x, y)
+    gaps = []
+    for A in (C, C.T):
+        s = np.sort(A, axis=1)
+        gaps.append(s[:, 1] - s[:, 0] + delta)
+    return float(np.median(np.concatenate(gaps)))
+
+
+@pytest.mark.parametrize("NM", [(12, 10), (20, 20)])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_backward_gap_clamp_vs_torch_autograd(NM, mode):
+    """P:140 clamp in the reverse pass: with eps_g at the median gap, about half of the lines
+    are clamped; a clamped g is a constant, so no gradient flows through it (the torch
+    formulation clamps with torch.where and differentiates).  Loss and both gradients must
+    agree; the test asserts that clamped and unclamped lines both occur."""
+    N, M = NM
+    x, y = clouds.pair("uniform", N, M, seed=N * 7 + M)
+    eg = _median_gap(x.astype(np.float32), y.astype(np.float32), 1e-6)
+    cfg = OracleConfig(eps_g=eg, eps_dist=0.0, tau=1e-8, grad_mode=mode)
+    P = sparse_forward(x, y, cfg)
+    cl = np.concatenate([P.lines(0)["clamped"], P.lines(1)["clamped"]])
+    assert 0 < cl.sum() < len(cl)
+    gx, gy = P.backward(1.0)
+    xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
+    yt = torch.tensor(y, dtype=torch.float64, requires_grad=True)
+    lt = _torch_dense_masked(xt, yt, cfg, detach_plan=(mode == 1))
+    lt.backward()
+    assert P.loss == pytest.approx(lt.item(), rel=1e-12)
+    np.testing.assert_allclose(gx, xt.grad.numpy(), rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(gy, yt.grad.numpy(), rtol=1e-8, atol=1e-10)
+
+
+def test_backward_gap_clamp_finite_differences():
+    """Central differences with half of the lines clamped: where g is clamped the loss
+    does not depend on the gap, so the FD derivative sees no T-path term for those lines."""
+    x, y = clouds.pair("uniform", 9, 8, 5)
+    x = x.astype(np.float64); y = y.astype(np.float64)
+    eg = _median_gap(x, y, 1e-6)
+    cfg = OracleConfig(eps_g=eg, eps_dist=0.0, tau=1e-8)
+    P = sparse_forward(x, y, cfg, f64=True)
+    cl0 = (P.lines(0)["clamped"].copy(), P.lines(1)["clamped"].copy())
+    assert 0 < cl0[0].sum() + cl0[1].sum() < 17
+    gx, _ = P.backward()
+    key = lambda Q: (Q.nnz, tuple(Q.support()["i"] * 1000 + Q.support()["j"]),
+                     tuple(Q.lines(0)["clamped"]), tuple(Q.lines(1)["clamped"]))
+    k0 = key(P)
+    h = 1e-6
+    checked = 0
+    for i in range(x.shape[0]):
+        for d in range(3):
+            xp = x.copy(); xp[i, d] += h
+            xm = x.copy(); xm[i, d] -= h
+            Pp = sparse_forward(xp, y, cfg, f64=True); Pm = sparse_forward(xm, y, cfg, f64=True)
+            if key(Pp) != k0 or key(Pm) != k0:
+                continue
+            fd = (Pp.loss - Pm.loss) / (2 * h)
+            assert fd == pytest.approx(gx[i, d], rel=1e-5, abs=1e-7)
+            checked += 1
+    assert checked >= 15
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])
