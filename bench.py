@@ -33,7 +33,7 @@ CONFIGS = {
     "C3R": dict(B=512, N=1024, M=1024, kind="mmfi", ragged=(256, 1024),
                 workload="C3 MM-Fi-shaped ragged: B=512, per-pair N_b, M_b ~ U[256, 1024], N_b != M_b"),
     "C4": dict(B=64, N=16384, M=16384, kind="shapenet",
-               workload="C4 PCN-shaped: B=64, N=M=16384 (per-GPU batch at weak scaling)"),
+               workload="C4 PCN-shaped: B=64, N=M=16384 (global batch; split over the ranks at N > 1)"),
     "C5": dict(B=1, N=262144, M=262144, kind="scene",
                workload="C5 scene: B=1, N=M=262144 (single GPU, unsharded)"),
 }
@@ -49,44 +49,119 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML thread polling
+    every ~1 ms (the C2 timed region is only ~10 ms, too short for nvidia-smi's 200 ms
+    period), falling back to `nvidia-smi -lms 20`."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index: int):
-        self.index = index
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        self.p = None
+    def __init__(self, index: int, pci_bus_id: str | None = None):
+        self.index, self.pci = index, pci_bus_id
+        self.rows, self.mode, self.p, self.th = [], None, None, None
+        self.stop_flag = False
+
+    def _nvml_loop(self, nv, h):
+        names = [("hw_slowdown", nv.nvmlClocksEventReasonHwSlowdown),
+                 ("hw_thermal_slowdown", nv.nvmlClocksEventReasonHwThermalSlowdown),
+                 ("sw_thermal_slowdown", nv.nvmlClocksEventReasonSwThermalSlowdown),
+                 ("sw_power_cap", nv.nvmlClocksEventReasonSwPowerCap)]
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while True:
+            done = self.stop_flag
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3 if (done or not self.rows) else 0.0
+                self.rows.append((float(sm), float(smax), pw, [n for n, bit in names if rs & bit]))
+            except Exception:
+                pass
+            if done:
+                return
+            time.sleep(0.0002)
 
     def start(self):
+        # the timed region can be ~10 ms: let the sampler thread take the GIL every 0.1 ms
+        self.switch = sys.getswitchinterval()
+        sys.setswitchinterval(1e-4)
         try:
+            import threading
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            if self.pci:
+                try:
+                    h = nv.nvmlDeviceGetHandleByPciBusId(self.pci)
+                except Exception:
+                    h = None
+            if h is None:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.mode = "nvml"
+            self.th = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.th.start()
+            return
+        except Exception:
+            self.mode = None
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "20"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
+            self.mode = "nvidia-smi"
         except Exception:
             self.p = None
 
     def stop(self) -> dict:
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) >= 8:
-                rows.append(parts)
-        os.unlink(self.f.name)
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
-        sm = sorted(float(r[0]) for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[4:8]) if v.lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2] not in ("", "[N/A]"))}
+        sys.setswitchinterval(getattr(self, "switch", 0.005))
+        if self.mode == "nvml":
+            self.stop_flag = True
+            self.th.join()
+        elif self.mode == "nvidia-smi" and self.p is not None:
+            time.sleep(0.05)
+            self.p.terminate()
+            self.p.wait()
+            self.f.flush()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in open(self.f.name):
+                r = [x.strip() for x in line.split(",")]
+                if len(r) >= 8:
+                    pw = float(r[2]) if r[2] not in ("", "[N/A]") else 0.0
+                    self.rows.append((float(r[0]), float(r[1]), pw,
+                                      [n for n, v in zip(names, r[4:8]) if v.lower() == "active"]))
+            os.unlink(self.f.name)
+        else:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock sampler available"]}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "source": self.mode}
+        sm = sorted(r[0] for r in self.rows)
+        reasons = sorted({n for r in self.rows for n in r[3]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.rows[0][1], "reasons": reasons,
+                "samples": len(self.rows), "sm_mhz_min": sm[0], "power_w_max": max(r[2] for r in self.rows),
+                "source": self.mode}
+
+
+def _pci_bus_id(dev) -> str | None:
+    try:
+        p = __import__("torch").cuda.get_device_properties(dev)
+        return f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+    except Exception:
+        return None
+
+
+def _host_cpu() -> dict:
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        avail = len(os.sched_getaffinity(0))
+    except Exception:
+        avail = os.cpu_count() or 1
+    return {"cpu_model": model, "nproc": avail, "cpu_count": os.cpu_count()}
 
 
 # Largest pair the oracle is timed on directly; bigger pairs (C5) are timed at this size and
@@ -120,7 +195,7 @@ def cpu_baseline(cfg_name: str, seed: int, budget_s: float = 15.0) -> dict:
         reps += 1
     el = time.perf_counter() - t0
     note = "" if scale == 1.0 else f" at N=M={sN}, scaled by the O(NM) cost x{scale:.3g}"
-    return {"value": done / el * scale, "unit": "pairs/s", "cores": used, "kind": "oracle",
+    return {"value": done / el * scale, "unit": "pairs/s", "cores": used, "kind": "oracle", **_host_cpu(),
             "sample": f"{reps} x {n} pairs of {cfg_name} ({c['kind']}, N={c['N']}, M={c['M']}){note}, fwd+full bwd, fp64, {el:.1f} s"}
 
 
@@ -154,7 +229,7 @@ def _ragged_reference(args, c) -> None:
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": c["workload"], "B": c["B"], "kind": c["kind"],
                                            "step_sample_pairs": len(pairs)},
-           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": 1, "kind": "oracle",
+           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": 1, "kind": "oracle", **_host_cpu(),
                             "sample": f"{len(pairs)} ragged pairs of {args.config} per step, fwd+full bwd, fp64"},
            "e2e": {"value": val, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -188,7 +263,7 @@ def run_reference(args) -> None:
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": {"workload": c["workload"], "B": c["B"], "N": c["N"], "M": c["M"],
                                            "kind": c["kind"], "step_sample_pairs": n},
-           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": used, "kind": "oracle",
+           "cpu_baseline": {"value": val, "unit": "pairs/s", "cores": used, "kind": "oracle", **_host_cpu(),
                             "sample": f"{n} pairs of {args.config} per step (bounded sample)"
                             + ("" if scale == 1.0 else f" at N=M={sN}, scaled by the O(NM) cost x{scale:.3g}")
                             + ", fwd+full bwd, fp64"},
@@ -207,6 +282,10 @@ def main():
     ap.add_argument("--grad-mode", default="full", choices=["full", "plan_detached"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="N > 1 batch sharding: weak = B pairs per rank; strong = the config's B split "
+                         "over the ranks (auto: strong for C3/C3R/C4, whose BASELINE configs fix the "
+                         "global batch; weak for C2)")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager calls instead of a CUDA-graph replay of a reusable plan")
     args = ap.parse_args()
@@ -232,6 +311,12 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.config]
     B, N, M = c["B"], c["N"], c["M"]
+    scaling = args.scaling if args.scaling != "auto" else ("strong" if args.config in ("C3", "C3R", "C4") else "weak")
+    B_global = B
+    if world > 1 and scaling == "strong" and args.config != "C5":
+        if B % world:
+            raise SystemExit(f"strong scaling needs B={B} divisible by the {world} ranks")
+        B = B // world  # this rank's share of the fixed global batch
     # C5 on several GPUs: one cloud, pred rows sharded (X2 all-gather + X3 column-sum
     # all-reduces inside the call); every other config: batch sharding (weak scaling)
     rowshard = args.config == "C5" and world > 1
@@ -330,7 +415,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.reset_peak_memory_stats(dev)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local, _pci_bus_id(dev))
     sampler.start()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -362,7 +447,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
     ms_per_step = tot_ms / args.steps
-    pairs_per_step = B if rowshard else B * world
+    pairs_per_step = B if rowshard else B * world  # = B_global under strong scaling
     value = pairs_per_step / (ms_per_step / 1e3)
 
     # per-stage medians and the roofline of the dominant kernel
@@ -395,13 +480,30 @@ def main():
         traffic = tr.get(args.config, {}).get(dom)
     except Exception:
         pass
+    # the method's distance work is 2 sweeps (Pass A, emit) x B N M evaluations x 6
+    # lane-ops.  This implementation's Pass A visits every (i, j) once per direction (rows and
+    # columns), so its executed evaluations are counted once for the algorithmic figure; the
+    # executed figure is reported beside it.  Culled sweeps: evaluations counted on the device.
+    alg_by = dict(evals_by)
+    alg_by["passA_rows"] = (evals_by["passA_rows"] + evals_by["passA_cols"]) // 2
+    alg_by["passA_cols"] = 0
+    fp32_meas = None
+    try:
+        fp32_meas = json.load(open(os.path.join(ROOT, "profiles", "fp32_peak.json")))
+    except Exception:
+        pass
+    meas_note = ("" if not fp32_meas else
+                 f"; measured (scripts/micro/fp32_peak.cu): FFMA2 {fp32_meas.get('ffma2_lane_tops', 0):.1f}, "
+                 f"FFMA {fp32_meas.get('ffma_lane_tops', 0):.1f} T lane-op/s")
     if dom in dist_stages:
-        ach = LANE_OPS_PER_EVAL * evals_by[dom] / (med[dom] / 1e3) / 1e12
+        ach = LANE_OPS_PER_EVAL * alg_by[dom] / (med[dom] / 1e3) / 1e12
         kname = ("k_line_top2_cull/k_emit_cull" if culled else "k_line_top2/k_emit") + f" ({dom})"
         roof = {"bound": "alu", "kernel": kname, "achieved": ach, "peak": alu_peak,
-                "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": traffic, "evals": evals_by[dom],
-                "note": "FP32 lane-op roofline (FMA counted once): 148 SM x 128 lanes x sm_max clock; "
-                        + ("evaluations counted by the culled kernels" if culled else "B N M evaluations")}
+                "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": traffic, "evals": alg_by[dom],
+                "executed_evals": evals_by[dom],
+                "note": "FP32 lane-op roofline (FMA counted once): 148 SM x 128 lanes x sm_max clock"
+                        + meas_note + "; " + ("evaluations counted by the culled kernels" if culled
+                                              else "B N M evaluations per sweep")}
     else:
         byt = sparse_bytes.get(dom, 0)
         ach = byt / (med[dom] / 1e3) / 1e9
@@ -412,74 +514,81 @@ def main():
                         "gathers and 2 L_iter DSMEM exchange rounds (~0.6 us each, "
                         "scripts/micro/xchg_bench.cu), not by HBM bandwidth"}
     dist_ms = sum(med[k] for k in dist_stages)
-    tot_evals = sum(evals_by.values())
-    roof_dist = {"bound": "alu", "achieved": LANE_OPS_PER_EVAL * tot_evals / (dist_ms / 1e3) / 1e12,
-                 "peak": alu_peak, "unit": "TFLOP/s", "sweeps": 3, "ms": dist_ms, "evals": tot_evals,
-                 "culled": culled, "dense_equivalent_evals": 3 * full_evals}
+    alg_evals, exe_evals = sum(alg_by.values()), sum(evals_by.values())
+    roof_dist = {"bound": "alu", "achieved": LANE_OPS_PER_EVAL * alg_evals / (dist_ms / 1e3) / 1e12,
+                 "peak": alu_peak, "unit": "TFLOP/s", "sweeps": 2, "ms": dist_ms, "evals": alg_evals,
+                 "executed_evals": exe_evals,
+                 "executed_achieved": LANE_OPS_PER_EVAL * exe_evals / (dist_ms / 1e3) / 1e12,
+                 "culled": culled, "dense_equivalent_evals": 2 * full_evals,
+                 "definition": "SURVEY 8(d): 6 lane-ops x 2 sweeps x evaluations / t(Pass A + emit)"}
     roof_dist["frac"] = roof_dist["achieved"] / alu_peak
+    roof_dist["executed_frac"] = roof_dist["executed_achieved"] / alu_peak
+    sm_load = (clocks or {}).get("sm_mhz")
+    if sm_load:  # the same fractions against the peak at the clock measured under load
+        roof_dist["frac_at_measured_clock"] = roof_dist["frac"] * f_max / (sm_load * 1e6)
+        if roof["bound"] == "alu":
+            roof["frac_at_measured_clock"] = roof["frac"] * f_max / (sm_load * 1e6)
 
-    # end to end (pinned host inputs copied in, the step, the loss read back; all inside the
-    # bracket).  Graph mode: the public Plan API as a training loop uses it (inputs copied into
-    # the plan's static tensors, graph replay, loss to the host; the gradient stays on the
-    # device for the network's backward).  Eager mode: apml_loss_grad_host (loss AND gradient
-    # back to the host).
+    # end to end through the C ABI on HOST buffers: pinned host pred / gt in, host loss AND
+    # gradient out, every copy inside the timed call.  Plans: apml_plan_step_host (H2D, a graph
+    # replay of forward + backward owned by the plan, D2H, sync).  Ragged / row-sharded: the
+    # public forward + backward with the same copies around them.
     e2e = None
-    if not args.no_e2e and use_graph:
+    if not args.no_e2e:
         ph = torch.tensor(x).pin_memory()
         gh = torch.tensor(y).pin_memory()
         lo = torch.empty(B, pin_memory=True)
+        go = torch.empty(B, pred.shape[1], 3, pin_memory=True)
+        lred = torch.empty(B, device=dev)
+        hplan = None
+        if use_graph:
+            hplan = Plan(B, pred.shape[1], M, Config(grad_mode=args.grad_mode, sync_check=False), device=dev)
 
         def e2e_step():
-            pred.copy_(ph, non_blocking=True)
-            gt.copy_(gh, non_blocking=True)
-            graph.replay()
-            if world > 1:
-                sharded_reduce(loss_buf)
-            lo.copy_(loss_buf, non_blocking=True)
-            torch.cuda.current_stream(dev).synchronize()
-        for _ in range(2):
+            if hplan is not None:
+                hplan.step_host(ph, gh, lo, go)  # synchronises before returning
+            else:
+                pred.copy_(ph, non_blocking=True)
+                gt.copy_(gh, non_blocking=True)
+                if rowshard:
+                    _, ctx = forward_rowsharded(pred, gt, r0, N, cfg, comm, loss_out=loss_buf)
+                else:
+                    _, ctx = forward(pred, gt, cfg, loss_out=loss_buf, n_sizes=ns, m_sizes=ms)
+                ctx.backward(ones, out=grad_buf)
+                lo.copy_(loss_buf, non_blocking=True)
+                go.copy_(grad_buf, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                ctx.close()
+            if world > 1 and not rowshard:  # X1 on the step's result
+                lred.copy_(lo, non_blocking=True)
+                sharded_reduce(lred)
+                lo.copy_(lred)
+        for _ in range(3):
             e2e_step()
-        ke = max(3, min(args.steps, 20))
-        acc = 0.0
+        ke = max(5, min(args.steps, 20))
+        e2e_list = []
         for _ in range(ke):
             flush.fill_(1)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             e2e_step()
-            acc += (time.perf_counter() - t0) * 1e3
-        e2e_ms = acc / ke
+            e2e_list.append((time.perf_counter() - t0) * 1e3)
+        e2e_ms = float(np.mean(e2e_list))
         if world > 1:
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": pairs_per_step / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 4 * B * 3 * (N + M), "d2h_bytes_per_step": 4 * B,
-               "api": "Plan (apml_plan_forward + apml_backward) in a CUDA graph: pinned H2D inputs, "
-                      "graph replay, D2H loss"}
-    elif not args.no_e2e and not rowshard and ns is None:
-        ph = torch.tensor(x).pin_memory()
-        gh = torch.tensor(y).pin_memory()
-        lo = torch.empty(B, pin_memory=True)
-        go = torch.empty(B, N, 3, pin_memory=True)
-        hcfg = Config(grad_mode=args.grad_mode, sync_check=False)
-        for _ in range(2):
-            loss_grad_host(ph, gh, hcfg, lo, go, device=local)
-        ke = max(3, min(args.steps, 20))
-        acc = 0.0
-        for _ in range(ke):
-            flush.fill_(1)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            loss_grad_host(ph, gh, hcfg, lo, go, device=local)  # synchronises before returning
-            acc += (time.perf_counter() - t0) * 1e3
-        e2e_ms = acc / ke
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": pairs_per_step / (e2e_ms / 1e3), "unit": "pairs/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": 4 * B * 3 * (N + M), "d2h_bytes_per_step": 4 * B + 4 * B * N * 3,
-               "api": "apml_loss_grad_host (host fp32 in, host loss + grad out)"}
+               "ms_p10": float(np.percentile(e2e_list, 10)), "ms_p50": float(np.median(e2e_list)),
+               "ms_p90": float(np.percentile(e2e_list, 90)), "steps": ke,
+               "h2d_bytes_per_step": ph.numel() * 4 + gh.numel() * 4,
+               "d2h_bytes_per_step": lo.numel() * 4 + go.numel() * 4,
+               "api": ("apml_plan_step_host (C ABI, host fp32 in, host loss + grad out; graph replay "
+                       "of forward + backward inside the call)" if hplan is not None else
+                       "forward + backward (C ABI) with pinned H2D inputs and D2H loss + grad in the bracket"),
+               "clock": "host wall clock around the synchronous call (max over ranks)"}
+        if hplan is not None:
+            hplan.close()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and ns is None:
@@ -490,12 +599,12 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if rowshard else "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if (rowshard or (world > 1 and scaling == "strong")) else "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": c["workload"], "B": B, "N": N, "M": M, "kind": c["kind"], "tau": cfg.tau,
+            "config": {"workload": c["workload"], "B": B_global, "N": N, "M": M, "kind": c["kind"], "tau": cfg.tau,
                        **({} if ns is None else {"ragged_mean_N": float(np.mean(ns)), "ragged_mean_M": float(np.mean(ms))}),
                        "l_iter": cfg.l_iter, "p_min": cfg.p_min, "grad_mode": args.grad_mode,
-                       "global_batch": pairs_per_step,
+                       "global_batch": pairs_per_step, "pairs_per_rank": B,
                        "parallelism": (f"row-shard x{world} (NCCL all-gather + per-iteration column-sum all-reduce)"
                                        if rowshard else f"batch-shard dp{world}" +
                                        (" + NCCL loss all-reduce" if world > 1 else "")),
@@ -506,6 +615,8 @@ def main():
             "dense_lower_bound_gb": 8 * B * N * M / 1e9,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
             "wall_s_timed": t_wall, "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),
+            "step_ms_p10": float(np.percentile(step_ms, 10)), "step_ms_p50": float(np.median(step_ms)),
+            "step_ms_p90": float(np.percentile(step_ms, 90)),
         }
         print(json.dumps(out), flush=True)
     if world > 1:

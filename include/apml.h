@@ -55,9 +55,10 @@ extern "C" {
 typedef enum {
     APML_OK = 0,
     APML_ERR_INVALID_ARG = 1, /* hyper-parameter outside its domain, NULL pointer */
-    APML_ERR_SHAPE = 2,       /* B, N or M < 1, or N, M >= 2^30 */
+    APML_ERR_SHAPE = 2,       /* B, N or M < 1, B > 32767, N, M >= 2^30, capacity >= 2^31 */
     APML_ERR_NONFINITE = 3,   /* non-finite coordinate (only with APML_FLAG_CHECK_FINITE) */
-    APML_ERR_CAPACITY = 4,    /* support exceeded the emit capacity and could not be retried */
+    APML_ERR_CAPACITY = 4,    /* support exceeded the emit capacity and could not be retried,
+                                 or a pair's support reached 2^31 entries (the saturated count) */
     APML_ERR_CUDA = 5,        /* a CUDA runtime call failed */
     APML_ERR_OOM = 6,         /* the allocator returned NULL */
     APML_ERR_STATE = 7        /* backward on a context without saved state, or called twice */
@@ -222,6 +223,19 @@ APML_API apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apm
                                       const apml_allocator* alloc, void* stream, apml_ctx** plan_out);
 APML_API apml_status apml_plan_forward(apml_ctx* plan, const float* pred, const float* gt, void* stream,
                                        float* loss);
+
+/* One training step of a plan on HOST buffers -- the end-to-end call: copies pred_host
+ * [B][N][3] and gt_host [B][M][3] (fp32, host; pinned memory gives async copies) into
+ * plan-owned device buffers, runs the forward and the backward with grad_loss = 1 for every
+ * pair (sum reduction, the plan's grad_mode), and copies loss [B] and grad_pred [B][N][3]
+ * back to loss_host / grad_pred_host.  The device part is captured once into a CUDA graph
+ * owned by the plan and replayed on later calls (not on the legacy NULL stream, nor with
+ * APML_HOST_GRAPH=0 in the environment).  Synchronises `stream` (NULL: the plan's stream)
+ * before returning.  A pair whose support exceeds the plan's capacity gets NaN outputs.
+ * Errors: APML_ERR_STATE (not a plan), APML_ERR_INVALID_ARG (NULL buffer), APML_ERR_OOM,
+ * APML_ERR_CUDA; nothing is written to the host outputs on error. */
+APML_API apml_status apml_plan_step_host(apml_ctx* plan, const float* pred_host, const float* gt_host,
+                                         void* stream, float* loss_host, float* grad_pred_host);
 
 /* Diagnostics; SYNCHRONISES the context's stream.  nnz_per_pair: host [B] or NULL. */
 APML_API apml_status apml_ctx_stats(const apml_ctx* ctx, int64_t* nnz_per_pair, apml_stats* out);

@@ -6,5 +6,5 @@ reference`` legs may import this package.  The product path
 algorithm and its PAPER.md citations.
 """
 from .oracle import (  # noqa: F401
-    OracleConfig, SparsePlan, build_oracle, dense_forward, sparse_forward, batch, temperature,
+    OracleConfig, SparsePlan, build_oracle, dense_forward, sparse_forward, batch, temperature, line,
 )

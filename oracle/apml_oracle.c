@@ -311,6 +311,30 @@ void oracle_plan_lines(const oracle_plan* P, int32_t dir, int64_t* ints, double*
     }
 }
 
+/* One line of Algorithm 1 on its own (P:161 rows / P:162 columns): the costs of point
+ * `own` against the K points of `other` (fp32 widened exactly), then the directional
+ * adaptive softmax of that line (Eq. (1)) -- the same line_softmax the
+ * sparse plan runs.  For sampled-line checks at sizes where the whole oracle is too slow
+ * (C5).  ints[6] = a, b, clamped, uniform, k1, kept; dbl[4] = m, c2, g, T; idx / p (capacity
+ * K) receive the kept indices and P values in index order.  Returns the kept count. */
+int64_t oracle_line(const float* own, const float* other, int64_t K, const oracle_cfg* cfg,
+                    int64_t* ints, double* dbl, int64_t* idx, double* p) {
+    if (K < 1 || !cfg) return -1;
+    double o[3] = {(double)own[0], (double)own[1], (double)own[2]};
+    double* line = (double*)malloc(sizeof(double) * K);
+    double* scratch = (double*)malloc(sizeof(double) * K);
+    for (int64_t k = 0; k < K; ++k) {
+        double q[3] = {(double)other[3 * k], (double)other[3 * k + 1], (double)other[3 * k + 2]};
+        line[k] = cost(o, q);
+    }
+    line_info li;
+    int64_t n = line_softmax(line, K, cfg, &li, idx, p, scratch);
+    ints[0] = li.a; ints[1] = li.b; ints[2] = li.clamped; ints[3] = li.uniform; ints[4] = li.k1; ints[5] = li.kept;
+    dbl[0] = li.m; dbl[1] = li.c2; dbl[2] = li.g; dbl[3] = li.T;
+    free(line); free(scratch);
+    return n;
+}
+
 /* ---------------------------------------------------------------- backward */
 
 /* Reverse of u = w / (S_seg + eps) (Eqs. (3)/(4)): wbar_t = (ubar_t - sum_seg ubar*u) / (S_seg + eps). */

@@ -84,6 +84,8 @@ def _L():
         lib.oracle_plan_free.argtypes = [P]
         lib.oracle_dense_forward.restype = C.c_double
         lib.oracle_dense_forward.argtypes = [f32p, f32p, C.c_int64, C.c_int64, C.POINTER(_Cfg), P]
+        lib.oracle_line.restype = C.c_int64
+        lib.oracle_line.argtypes = [f32p, f32p, C.c_int64, C.POINTER(_Cfg), i64p, f64p, i64p, f64p]
         lib.oracle_batch.restype = C.c_int
         lib.oracle_batch.argtypes = [f32p, f32p, C.c_int64, C.c_int64, C.c_int64, C.POINTER(_Cfg),
                                      P, f64p, P, P, C.c_int]
@@ -182,3 +184,18 @@ def batch(x, y, cfg: OracleConfig | None = None, gbar=None, want_grad: bool = Tr
                              None if grad is None else grad.ctypes.data_as(C.c_void_p),
                              nnz.ctypes.data_as(C.c_void_p), nthreads)
     return loss, grad, nnz, used
+
+
+def line(own_point, others, cfg: OracleConfig | None = None) -> dict:
+    """One line of Algorithm 1 (P:161 / P:162) on its own: point `own_point` [3] against
+    `others` [K, 3] -- m, c2, g, T, argmin a, second b, clamped, and the kept (index, P)."""
+    cfg = cfg or OracleConfig()
+    o = _f32(own_point).reshape(3)
+    y = _f32(others).reshape(-1, 3)
+    K = y.shape[0]
+    ints = np.zeros(6, np.int64); dbl = np.zeros(4)
+    idx = np.zeros(K, np.int64); p = np.zeros(K)
+    c = cfg._c()
+    n = _L().oracle_line(o, y.reshape(-1), K, C.byref(c), ints, dbl, idx, p)
+    return dict(a=int(ints[0]), b=int(ints[1]), clamped=int(ints[2]), uniform=int(ints[3]), k1=int(ints[4]),
+                kept=int(ints[5]), m=dbl[0], c2=dbl[1], g=dbl[2], T=dbl[3], idx=idx[:n].copy(), p=p[:n].copy())

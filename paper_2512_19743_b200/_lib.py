@@ -25,7 +25,7 @@ EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forw
            "apml_backward", "apml_backward_ex", "apml_plan_create", "apml_plan_forward",
            "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
            "apml_ctx_destroy",
-           "apml_loss_grad_host", "apml_last_error")
+           "apml_loss_grad_host", "apml_plan_step_host", "apml_last_error")
 
 
 class ApmlConfig(C.Structure):
@@ -112,6 +112,8 @@ def lib() -> C.CDLL:
         L.apml_loss_grad_host.restype = C.c_int
         L.apml_loss_grad_host.argtypes = [vp, vp, i64, i64, i64, C.POINTER(ApmlConfig),
                                           C.POINTER(ApmlAllocator), vp, vp, vp]
+        L.apml_plan_step_host.restype = C.c_int
+        L.apml_plan_step_host.argtypes = [vp, vp, vp, vp, vp, vp]
         L.apml_last_error.restype = C.c_char_p
         L.apml_last_error.argtypes = []
         if L.apml_abi_version() != 2:

@@ -195,6 +195,22 @@ class Plan(Context):
         return loss
 
 
+    def step_host(self, pred_host: torch.Tensor, gt_host: torch.Tensor, loss_out: torch.Tensor | None = None,
+                  grad_out: torch.Tensor | None = None):
+        """apml_plan_step_host: host fp32 [B,N,3] / [B,M,3] in, host loss [B] and grad [B,N,3] out
+        (sum reduction); copies both ways and a graph replay of forward + backward inside the call."""
+        for t, n, k in ((pred_host, "pred", self.N), (gt_host, "gt", self.M)):
+            if t.is_cuda or t.dtype != torch.float32 or tuple(t.shape) != (self.B, k, 3) or not t.is_contiguous():
+                raise ValueError(f"{n} must be a contiguous float32 host tensor [{self.B}, {k}, 3]")
+        loss = loss_out if loss_out is not None else torch.empty(self.B, dtype=torch.float32, pin_memory=True)
+        grad = grad_out if grad_out is not None else torch.empty(self.B, self.N, 3, dtype=torch.float32,
+                                                                 pin_memory=True)
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        A.check(A.lib().apml_plan_step_host(self._h, pred_host.data_ptr(), gt_host.data_ptr(), s,
+                                            loss.data_ptr(), grad.data_ptr()))
+        return loss, grad
+
+
 class _APMLFunction(torch.autograd.Function):
     @staticmethod
     def forward(fctx, pred, gt, cfg, n_sizes=None, m_sizes=None):

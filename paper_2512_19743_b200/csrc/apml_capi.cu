@@ -138,6 +138,10 @@ struct apml_ctx {
   int2 *rowidx, *colidx;
   float *a_hist, *b_hist, *gvec;
   LineBack *rowback, *colback;
+  // apml_plan_step_host: device copies of the host inputs / outputs and the captured step
+  char* hbuf = nullptr;
+  size_t hbytes = 0;
+  cudaGraphExec_t hstep = nullptr;
 };
 
 namespace {
@@ -183,6 +187,12 @@ void* ctx_alloc(apml_ctx* c, size_t bytes) {
 void ctx_free(apml_ctx* c) {
   for (auto& e : c->ev)
     if (e) { cudaEventDestroy(e); e = nullptr; }
+  if (c->hstep) { cudaGraphExecDestroy(c->hstep); c->hstep = nullptr; }
+  if (c->hbuf) {
+    if (c->has_alloc) c->alloc.free(c->hbuf, c->hbytes, c->stream, c->alloc.user);
+    else cudaFreeAsync(c->hbuf, c->stream);
+    c->hbuf = nullptr;
+  }
   if (!c->base) return;
   if (c->has_alloc) c->alloc.free(c->base, c->bytes, c->stream, c->alloc.user);
   else cudaFreeAsync(c->base, c->stream);
@@ -194,7 +204,8 @@ apml_status validate(const float* pred, const float* gt, int64_t B, int64_t N, i
   if (!pred || !gt) return fail(APML_ERR_INVALID_ARG, "pred / gt must be non-NULL device pointers");
   if (B < 1 || N < 1 || M < 1) return fail(APML_ERR_SHAPE, "B, N and M must be >= 1 (EmptyCloud)");
   if (N >= (1 << 30) || M >= (1 << 30)) return fail(APML_ERR_SHAPE, "N and M must be < 2^30");
-  if (B > 65535) return fail(APML_ERR_SHAPE, "B must be <= 65535 (grid.y / grid.z limit)");
+  // k_stage_both / k_line_top2_both put (pair, direction) on grid.z = 2 B (limit 65535)
+  if (B > 32767) return fail(APML_ERR_SHAPE, "B must be <= 32767 (grid.z = 2 B limit)");
   if (!(c.p_min > 0.f && c.p_min < 1.f)) return fail(APML_ERR_INVALID_ARG, "p_min must lie in (0, 1) (Eq. 1)");
   for (int64_t K : {N, M})
     if (K > 1 && !((double)c.p_min * (double)K > 1.0))
@@ -850,6 +861,27 @@ apml_status check_finite(const float* p, int64_t n, cudaStream_t s) {
   return APML_OK;
 }
 
+// `waiter` waits (on the device) for all work enqueued so far on `src`.
+// Not while either stream is being captured into a CUDA graph: an event recorded outside the
+// capture cannot be waited on inside it, and inside a graph the caller's capture orders the
+// nodes (the plan's own stream is switched to the capturing one).
+bool capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  return cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+cudaError_t order_after(cudaStream_t waiter, cudaStream_t src) {
+  if (waiter == src || capturing(waiter) || capturing(src)) return cudaSuccess;
+  cudaEvent_t ev;
+  cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;
+  e = cudaEventRecord(ev, src);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(waiter, ev, 0);
+  cudaEventDestroy(ev);
+  return e;
+}
+
+apml_status backward_on(apml_ctx* x, const float* grad_loss, float* grad_pred, float* grad_gt, cudaStream_t s);
+
 }  // namespace
 
 extern "C" {
@@ -919,8 +951,8 @@ apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, i
   int64_t cap64 = per * (N + M);
   if (cap64 > N * M) cap64 = N * M;
   if (cap64 < 1) cap64 = 1;
-  if (cap64 * B > (int64_t)1 << 40 || cap64 >= ((int64_t)1 << 32))
-    return fail(APML_ERR_SHAPE, "emit capacity exceeds 32-bit per-pair positions");
+  if (cap64 * B > (int64_t)1 << 40 || cap64 >= ((int64_t)1 << 31))
+    return fail(APML_ERR_SHAPE, "emit capacity exceeds 2^31 per-pair positions");
   for (int attempt = 0; attempt < 2; ++attempt) {
     apml_ctx* x = new apml_ctx();
     x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = s;
@@ -958,6 +990,7 @@ apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, i
       if (mx > x->cap) {
         apml_ctx_destroy(x);
         if (attempt == 1) return fail(APML_ERR_CAPACITY, "support exceeded capacity after retry");
+        if (mx >= 0x80000000u) return fail(APML_ERR_CAPACITY, "support exceeds 2^31 entries per pair");
         cap64 = round_up((int64_t)mx + (int64_t)mx / 16 + 16, 64);
         if (cap64 > N * M) cap64 = N * M;
         continue;
@@ -993,7 +1026,7 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
   const int64_t per = c.capacity > 0 ? c.capacity : 6;
   int64_t cap64 = std::min<int64_t>(per * (N + M), N * M);
   if (cap64 < 1) cap64 = 1;
-  if (cap64 >= ((int64_t)1 << 32)) return fail(APML_ERR_SHAPE, "emit capacity exceeds 32-bit positions");
+  if (cap64 >= ((int64_t)1 << 31)) return fail(APML_ERR_SHAPE, "emit capacity exceeds 2^31 per-pair positions");
   for (int attempt = 0; attempt < 2; ++attempt) {
     apml_ctx* x = new apml_ctx();
     x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = s;
@@ -1020,7 +1053,7 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
       if (e != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, cudaGetErrorString(e)); }
       unsigned mx = 0;
       for (unsigned v : cnt) mx = v > mx ? v : mx;
-      float over = mx > x->cap ? 1.f : 0.f;
+      float over = mx >= 0x80000000u ? 65536.f : mx > x->cap ? 1.f : 0.f;  // saturated: every rank fails
       e = cudaMemcpyAsync(x->flag, &over, sizeof(float), cudaMemcpyHostToDevice, s);
       if (e != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, cudaGetErrorString(e)); }
       if ((st = coll_sum(x, x->flag, 1)) != APML_OK) { apml_ctx_destroy(x); return st; }
@@ -1030,6 +1063,7 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
       if (over > 0.f) {
         apml_ctx_destroy(x);
         if (attempt == 1) return fail(APML_ERR_CAPACITY, "support exceeded capacity after retry");
+        if (over >= 65536.f) return fail(APML_ERR_CAPACITY, "support exceeds 2^31 entries per pair");
         cap64 = std::min<int64_t>(std::max<int64_t>(cap64, round_up((int64_t)mx + (int64_t)mx / 16 + 16, 64)), N * M);
         continue;
       }
@@ -1054,13 +1088,20 @@ apml_status apml_backward_ex(apml_ctx* x, const float* grad_loss, float* grad_pr
   if (x->plan && !x->forward_done) return fail(APML_ERR_STATE, "plan: apml_plan_forward has not run");
   if (!grad_loss || !grad_pred) return fail(APML_ERR_INVALID_ARG, "grad_loss / grad_pred must be non-NULL");
   cudaStream_t s = stream ? (cudaStream_t)stream : x->stream;
-  if (s != x->stream) {  // order after the forward's stream
-    cudaEvent_t ev;
-    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CK(cudaEventRecord(ev, x->stream));
-    CK(cudaStreamWaitEvent(s, ev, 0));
-    CK(cudaEventDestroy(ev));
+  if (s != x->stream) {
+    CK(order_after(s, x->stream));  // the backward reads what the forward wrote
+    // and the context's stream (its stream-ordered free in apml_ctx_destroy, the next plan
+    // forward) must not overtake the backward's reads of the workspace
+    struct Join { apml_ctx* c; cudaStream_t s; ~Join() { order_after(c->stream, s); } } join{x, s};
+    return backward_on(x, grad_loss, grad_pred, grad_gt, s);
   }
+  return backward_on(x, grad_loss, grad_pred, grad_gt, s);
+}
+
+}  // extern "C"
+
+namespace {
+apml_status backward_on(apml_ctx* x, const float* grad_loss, float* grad_pred, float* grad_gt, cudaStream_t s) {
   mark(x, 7, s);
   x->bwd_timed = x->timing;
   if (x->rs) {
@@ -1094,6 +1135,9 @@ apml_status apml_backward_ex(apml_ctx* x, const float* grad_loss, float* grad_pr
   x->backward_done = true;
   return APML_OK;
 }
+}  // namespace
+
+extern "C" {
 
 apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats* out) {
   if (!x) return fail(APML_ERR_STATE, "NULL context");
@@ -1245,8 +1289,8 @@ apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config*
   int64_t cap64 = per * (N + M);
   if (cap64 > N * M) cap64 = N * M;
   if (cap64 < 1) cap64 = 1;
-  if (cap64 * B > (int64_t)1 << 40 || cap64 >= ((int64_t)1 << 32))
-    return fail(APML_ERR_SHAPE, "emit capacity exceeds 32-bit per-pair positions");
+  if (cap64 * B > (int64_t)1 << 40 || cap64 >= ((int64_t)1 << 31))
+    return fail(APML_ERR_SHAPE, "emit capacity exceeds 2^31 per-pair positions");
   apml_ctx* x = new apml_ctx();
   x->B = B; x->N = N; x->M = M; x->cfg = c; x->stream = (cudaStream_t)stream;
   x->plan = true;
@@ -1262,6 +1306,7 @@ apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config*
   const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;
   x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
   x->rho_c = N > 1 ? (float)(lt / lambda_K(N, p)) : INFINITY;
+  x->cap = (uint32_t)cap64;  // plan_sparse (inside use_grid_path) sizes the support from it
   if (use_grid_path(x)) {
     x->rs = true;
     x->comm = apml_comm{0, 1, local_allreduce, local_allgather, nullptr};
@@ -1276,7 +1321,10 @@ apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config*
 apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, void* stream, float* loss) {
   if (!x || !x->plan) return fail(APML_ERR_STATE, "not a plan (apml_plan_create)");
   if (!pred || !gt || !loss) return fail(APML_ERR_INVALID_ARG, "pred / gt / loss must be non-NULL device pointers");
-  if (stream) x->stream = (cudaStream_t)stream;
+  if (stream && (cudaStream_t)stream != x->stream) {  // earlier work on the old stream first
+    CK(order_after((cudaStream_t)stream, x->stream));
+    x->stream = (cudaStream_t)stream;
+  }
   // per-call state: counters zeroed on the stream (capturable), one backward allowed again
   CK(cudaMemsetAsync(static_cast<char*>(x->base) + x->zero_off, 0, x->zero_bytes, x->stream));
   x->backward_done = false;
@@ -1286,6 +1334,61 @@ apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, v
   if (st == APML_OK) st = x->rs ? launch_sparse_fwd_rs(x, loss) : launch_sparse_fwd(x, loss);
   if (st == APML_OK) x->forward_done = true;
   return st;
+}
+
+apml_status apml_plan_step_host(apml_ctx* x, const float* pred_host, const float* gt_host, void* stream,
+                                float* loss_host, float* grad_pred_host) {
+  if (!x || !x->plan) return fail(APML_ERR_STATE, "not a plan (apml_plan_create)");
+  if (!pred_host || !gt_host || !loss_host || !grad_pred_host)
+    return fail(APML_ERR_INVALID_ARG, "host buffers must be non-NULL");
+  cudaStream_t s = stream ? (cudaStream_t)stream : x->stream;
+  if (s != x->stream) {
+    CK(order_after(s, x->stream));
+    x->stream = s;
+  }
+  const int64_t B = x->B, N = x->N, M = x->M;
+  const size_t bp = sizeof(float) * (size_t)(B * N * 3), bg = sizeof(float) * (size_t)(B * M * 3);
+  const size_t o_gt = round_up(bp, 256), o_loss = o_gt + round_up(bg, 256);
+  const size_t o_gl = o_loss + round_up(4 * B, 256), o_grad = o_gl + round_up(4 * B, 256);
+  if (!x->hbuf) {
+    x->hbytes = o_grad + bp;
+    x->hbuf = (char*)ctx_alloc(x, x->hbytes);
+    if (!x->hbuf) return fail(APML_ERR_OOM, "allocation of the host-step buffers failed");
+    k_fill<<<(unsigned)((B + 255) / 256), 256, 0, s>>>((float*)(x->hbuf + o_gl), (int)B, 1.f);
+    CK(cudaGetLastError());
+  }
+  float *d_pred = (float*)x->hbuf, *d_gt = (float*)(x->hbuf + o_gt), *d_loss = (float*)(x->hbuf + o_loss);
+  float *d_gl = (float*)(x->hbuf + o_gl), *d_grad = (float*)(x->hbuf + o_grad);
+  CK(cudaMemcpyAsync(d_pred, pred_host, bp, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_gt, gt_host, bg, cudaMemcpyHostToDevice, s));
+  // the device part (forward + backward, ~6 launches) is captured once into a graph owned by
+  // the plan; the legacy default stream cannot be captured (eager there, and APML_HOST_GRAPH=0)
+  const bool graph = s != nullptr && env_long("APML_HOST_GRAPH", 1) != 0;
+  apml_status st = APML_OK;
+  if (graph && !x->hstep) {
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    st = apml_plan_forward(x, d_pred, d_gt, s, d_loss);
+    if (st == APML_OK) st = apml_backward(x, d_gl, d_grad, s);
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(s, &g);
+    if (st != APML_OK) { if (g) cudaGraphDestroy(g); return st; }
+    if (e != cudaSuccess) return fail(APML_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    const cudaError_t e2 = cudaGraphInstantiate(&x->hstep, g, 0);
+    cudaGraphDestroy(g);
+    if (e2 != cudaSuccess) { x->hstep = nullptr; return fail(APML_ERR_CUDA, cudaGetErrorString(e2)); }
+  }
+  if (graph) {
+    CK(cudaGraphLaunch(x->hstep, s));
+    x->forward_done = true;
+    x->backward_done = true;
+  } else {
+    if ((st = apml_plan_forward(x, d_pred, d_gt, s, d_loss)) != APML_OK) return st;
+    if ((st = apml_backward(x, d_gl, d_grad, s)) != APML_OK) return st;
+  }
+  CK(cudaMemcpyAsync(loss_host, d_loss, 4 * (size_t)B, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(grad_pred_host, d_grad, bp, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return APML_OK;
 }
 
 apml_status apml_loss_grad_host(const float* pred_host, const float* gt_host, int64_t B,

@@ -260,6 +260,7 @@ __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int
 // per step); the warp flushes all queues with one shuffle scan and one returning atomic when a
 // queue is nearly full and at the end.
 constexpr int kLaneQ = 16;  // queue slots per lane
+constexpr unsigned kCursorSat = 0x80000000u, kCursorPark = 0xC0000000u;
 
 __device__ __forceinline__ void lane_flush(int b, const uint2* q, int cnt, uint32_t cap, uint2* __restrict__ ebuf,
                                            unsigned* __restrict__ cursor, unsigned* __restrict__ aux_cnt,
@@ -275,7 +276,13 @@ __device__ __forceinline__ void lane_flush(int b, const uint2* q, int cnt, uint3
   const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
   if (total == 0) return;
   unsigned base = 0;
-  if (lane == 31) base = atomicAdd(cursor + b, total);
+  if (lane == 31) {
+    base = atomicAdd(cursor + b, total);
+    // saturate: a count past 2^31 is parked at 3 * 2^30, so that no amount of emission
+    // (tau = 0 on N M >= 2^32 pairs) wraps the 32-bit cursor back under the capacity; the
+    // concurrent flushes between the add and the exchange total far less than 2^30
+    if (base >= kCursorSat) atomicExch(cursor + b, kCursorPark);
+  }
   base = __shfl_sync(0xffffffffu, base, 31) + inc - (unsigned)cnt;
   unsigned aux = 0;
   for (int k = 0; k < cnt; ++k) {

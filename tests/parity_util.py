@@ -62,17 +62,23 @@ def flags_map(sup) -> dict:
     return {(int(a), int(b)): int(f) for a, b, f in zip(sup["i"], sup["j"], sup["flags"])}
 
 
-def well_conditioned(x, y, plan, cfg, thresh=1e6) -> np.ndarray:
-    """Boolean mask over pred points (see module doc)."""
+def well_conditioned(x, y, plan, cfg, thresh=1e6, skip_clamped=False) -> np.ndarray:
+    """Boolean mask over pred points (see module doc).  skip_clamped: lines whose gap clamp is
+    active are not excluded -- the clamp zeroes their T-path gradient (g-bar = 0), the
+    path through which near-tie lines amplify rounding."""
     N, M = x.shape[0], y.shape[0]
     rows, cols = plan.lines(0), plan.lines(1)
     s = float(np.median(rows["m"]))
     ok = np.ones(N, bool)
     if M > 1:
         bad_r = _lam(M, cfg.p_min) * s * s / np.maximum(rows["g"], 1e-300) ** 2 >= thresh
+        if skip_clamped:
+            bad_r &= rows["clamped"] == 0
         ok &= ~bad_r
     if N > 1:
         bad_c = _lam(N, cfg.p_min) * s * s / np.maximum(cols["g"], 1e-300) ** 2 >= thresh
+        if skip_clamped:
+            bad_c &= cols["clamped"] == 0
         for j in np.nonzero(bad_c)[0]:
             for i in (cols["a"][j], cols["b"][j]):
                 if i >= 0:
@@ -102,3 +108,37 @@ def well_conditioned_gt(x, y, plan, cfg, thresh=1e6) -> np.ndarray:
                 if j >= 0:
                     ok[j] = False
     return ok
+
+
+def p0_bound(plan, cfg, oi, oj, oflags) -> np.ndarray:
+    """Derived per-entry relative bound on the fp32 P0.  Per direction,
+    with u the fp32 unit roundoff and the GPU evaluating c = sqrt(d2) (rel. err ~2u),
+    g = c2 - m + delta (abs. err ~2u (c2 + m)), T = Lambda / g (rel. err ~2u (c2 + m) / g + u),
+    e = T (c - m) <= ln(1/tau) on kept entries (abs. err <= e relT + 2u T (c + m)), s = exp(-e)
+    (+2u), Z = sum s and P = s / Z (each at most the worst s error of the line):
+        eps_dir <= u [ (74 (c2 + m) + 8 Lambda m) / g + 110 ]     (ln(1/tau) = 18.4 folded in)
+    and P0 = (P_row + P_col) / 2 takes the larger of its directions."""
+    rows, cols = plan.lines(0), plan.lines(1)
+    N, M = plan.N, plan.M
+
+    def line_bound(ln, k, K):
+        m, c2, g = ln["m"][k], ln["c2"][k], ln["g"][k]
+        c2 = np.where(np.isfinite(c2), c2, m)
+        return U * ((74.0 * (c2 + m) + 8.0 * _lam(K, cfg.p_min) * m) / np.maximum(g, 1e-300) + 110.0)
+
+    br = np.where(oflags & 1, line_bound(rows, oi, M), 0.0) if M > 1 else np.zeros(len(oi))
+    bc = np.where(oflags & 2, line_bound(cols, oj, N), 0.0) if N > 1 else np.zeros(len(oi))
+    return np.maximum(np.maximum(br, bc), 4 * U)
+
+
+def match_support(gpu_sup, orc_sup):
+    """Index arrays (gpu positions, oracle positions) of the entries both sides keep (flags != 0)."""
+    key_o = {(int(i), int(j)): k for k, (i, j) in enumerate(zip(orc_sup["i"], orc_sup["j"]))}
+    ga, oa = [], []
+    for k, (i, j, f) in enumerate(zip(gpu_sup["i"], gpu_sup["j"], gpu_sup["flags"])):
+        if f:
+            o = key_o.get((int(i), int(j)))
+            if o is not None:
+                ga.append(k)
+                oa.append(o)
+    return np.asarray(ga, np.int64), np.asarray(oa, np.int64)

@@ -420,3 +420,39 @@ def test_gradient_readings_differ():
     gf, _ = sparse_forward(x, y, OracleConfig(grad_mode=0)).backward()
     gd, _ = sparse_forward(x, y, OracleConfig(grad_mode=1)).backward()
     assert np.linalg.norm(gf - gd) / np.linalg.norm(gf) > 0.2
+
+
+# ---------------------------------------------------------------- single-line entry point
+def test_single_line_matches_plan_and_pmin_identity():
+    """oracle.line (one row / column of Algorithm 1 on its own, used by the sampled C5 GPU
+    check) is the plan's line: same m, c2, g, T, argmin, kept set and P_row / P_col as the
+    pinned sparse plan; and on a line of costs {m, m+g, ..., m+g} with delta = 0 it puts
+    exactly p_min on the argmin (Eq. (1) + softmax)."""
+    from oracle import line
+    x, y = clouds.pair("shapenet", 60, 45, 3)
+    P = sparse_forward(x, y, OracleConfig())
+    rows, cols = P.lines(0), P.lines(1)
+    s = P.support()
+    for i in (0, 7, 59):
+        L = line(x[i], y, OracleConfig())
+        for k in ("m", "c2", "g", "T"):
+            assert L[k] == rows[k][i]
+        assert L["a"] == rows["a"][i] and L["b"] == rows["b"][i]
+        sel = (s["i"] == i) & ((s["flags"] & 1) != 0)
+        np.testing.assert_array_equal(L["idx"], s["j"][sel])
+        np.testing.assert_array_equal(L["p"], s["prow"][sel])
+    for j in (0, 44):
+        L = line(y[j], x, OracleConfig())
+        assert L["T"] == cols["T"][j] and L["a"] == cols["a"][j]
+        sel = (s["j"] == j) & ((s["flags"] & 2) != 0)
+        np.testing.assert_array_equal(L["idx"], s["i"][sel])
+        np.testing.assert_array_equal(L["p"], s["pcol"][sel])
+    # p_min identity: other points on the axes at distances 2 (the minimum) and 2.5 (K - 1 ties)
+    for K, p in ((5, 0.9), (12, 0.8)):
+        pts = np.zeros((K, 3), np.float32)
+        pts[0] = (2.0, 0, 0)
+        for k in range(1, K):
+            pts[k] = (0, 2.5, 0) if k % 2 else (0, 0, -2.5)
+        L = line(np.zeros(3, np.float32), pts, OracleConfig(p_min=p, delta=0.0, tau=0.0))
+        assert L["a"] == 0 and abs(L["g"] - 0.5) < 1e-15
+        assert abs(L["p"][0] - p) < 1e-12
