@@ -106,7 +106,9 @@ typedef struct {
     float   eps_dist;     /* Eq. (5) denominator, > 0; default 1e-8 */
     int32_t grad_mode;    /* apml_grad_mode; default APML_GRAD_FULL */
     int32_t capacity;     /* emit capacity per pair in entries per point: cap = capacity*(N+M),
-                             clipped to N*M; 0 = default (6) */
+                             clipped to N*M; 0 = default: plans 6; eager calls 6 / 5 / 4 / 3
+                             for N+M < 2048 / 8192 / 65536 / larger (Fig. 2's falling support
+                             per point; an overflow is retried with the exact count) */
     uint32_t flags;       /* APML_FLAG_*; default APML_FLAG_SYNC_CHECK */
 } apml_config;
 
@@ -122,9 +124,10 @@ typedef struct {
     int64_t nnz_total;      /* |Omega_tau| summed over pairs (entries carrying a row or column flag) */
     int64_t emitted_total;  /* emitted entries incl. second-argmin-only entries (tau > tau*) */
     int64_t clamp_count;    /* lines whose gap was clamped to eps_g */
-    int64_t capacity;       /* emit capacity per pair actually used (entries) */
+    int64_t capacity;       /* per-entry capacity per pair actually used (entries; after the
+                               support read-back: the largest pair's count, + 64) */
     int64_t overflow_pairs; /* pairs whose support exceeded capacity (their loss is NaN) */
-    int64_t bytes_ctx;      /* device bytes owned by the context */
+    int64_t bytes_ctx;      /* device bytes owned by the context (both allocations) */
     int64_t launches;       /* kernels launched so far by this context (forward + backward) */
     int64_t sweep_evals[3]; /* (i, j) distance evaluations executed by the sweeps of the last
                                forward: [0] Pass A rows, [1] Pass A columns, [2] emit.  Full
@@ -214,7 +217,13 @@ APML_API apml_status apml_backward_ex(apml_ctx* ctx, const float* grad_loss, flo
  * pair) and returns a context; apml_plan_forward then runs the forward on new pred / gt with
  * NO allocation, NO host synchronisation and NO host read (APML_FLAG_SYNC_CHECK and
  * APML_FLAG_CHECK_FINITE are ignored), so a training step `apml_plan_forward +
- * apml_backward[_ex]` can be captured into a CUDA graph and replayed.  A pair whose support
+ * apml_backward[_ex]` can be captured into a CUDA graph and replayed.  Exception: with
+ * cfg->capacity == 0 (the default) the per-entry arrays (CSR / CSC, ~64 B per entry) are
+ * sized by the plan's FIRST forward -- 1.5 x the largest per-pair support it emits, one count
+ * read-back and one allocation in that call only -- so that memory follows the support, not
+ * the emit capacity; if that first forward is itself being captured they take the emit
+ * capacity.  A later input whose support exceeds that size is reported like a capacity
+ * overflow (below).  A pair whose support
  * exceeds the capacity gets a NaN loss / gradient (apml_ctx_stats reports it).  Each
  * apml_plan_forward allows one backward; the introspection calls read the last forward.
  * Destroy with apml_ctx_destroy.  Errors: as apml_forward; APML_ERR_STATE for a context that

@@ -75,7 +75,11 @@ struct apml_ctx {
   bool has_alloc = false;
   char* base = nullptr;
   size_t bytes = 0;
-  uint32_t cap = 0;
+  char* ebase = nullptr;  // the per-entry arrays (stride cap), a second allocation
+  size_t ebytes = 0;
+  uint32_t cap = 0;       // per-pair stride of the per-entry arrays (sized from the support)
+  uint32_t cap_e = 0;     // per-pair stride of the emit buffer (the emit capacity)
+  bool calibrate = false; // plan: size the per-entry arrays on the first forward
   int S_rows = 1, S_cols = 1, chunk_rows = 0, chunk_cols = 0;
   int S_emit = 1, chunk_emit = 0;  // column split of the emit sweep (its own wave target)
   bool backward_done = false;
@@ -193,6 +197,11 @@ void ctx_free(apml_ctx* c) {
     else cudaFreeAsync(c->hbuf, c->stream);
     c->hbuf = nullptr;
   }
+  if (c->ebase) {
+    if (c->has_alloc) c->alloc.free(c->ebase, c->ebytes, c->stream, c->alloc.user);
+    else cudaFreeAsync(c->ebase, c->stream);
+    c->ebase = nullptr;
+  }
   if (!c->base) return;
   if (c->has_alloc) c->alloc.free(c->base, c->bytes, c->stream, c->alloc.user);
   else cudaFreeAsync(c->base, c->stream);
@@ -218,6 +227,15 @@ apml_status validate(const float* pred, const float* gt, int64_t B, int64_t N, i
     return fail(APML_ERR_INVALID_ARG, "unknown grad_mode");
   if (c.capacity < 0) return fail(APML_ERR_INVALID_ARG, "capacity must be >= 0");
   return APML_OK;
+}
+
+// Default emit capacity per point of N + M for the eager calls (a capacity overflow is
+// retried there with the exact count): the union support per point falls with the cloud size
+// (Fig. 2; profiles/fig2_nnz.md: 4.9 at N = M = 64, 2.7 at 2048, 2.1 at 16384,
+// 1.7 at 262144), so the first attempt keeps ~1.6-2x headroom over it.
+int64_t default_per(int64_t N, int64_t M) {
+  const int64_t nm = N + M;
+  return nm < 2048 ? 6 : nm < 8192 ? 5 : nm < 65536 ? 4 : 3;
 }
 
 // Lambda_K = -log((1 - p) / ((K - 1) p)) (numerator of Eq. (1)), fp64.
@@ -308,9 +326,50 @@ void plan_sparse(apml_ctx* c) {
   if (c->fwd2) c->smem_bytes = mx;
 }
 
-apml_status build_ctx(apml_ctx* c, uint32_t cap) {
+// The per-entry arrays (CSR / CSC and the per-entry values, stride cap): a second allocation,
+// sized after the emit when the support counts are read back (eager calls with
+// APML_FLAG_SYNC_CHECK, a plan's first forward), else at the emit capacity.  Memory is then
+// linear in the support actually emitted, not in the capacity guess.
+apml_status alloc_entries(apml_ctx* c, uint32_t cap) {
+  const int64_t B = c->B;
+  c->cap = cap;
+  Carve k;
+  const int64_t E = B * (int64_t)cap;
+  // k_sparse_fwd2 needs no emit-index / d2 scratch of its own (csr_t / csc_t alias cs / csc_c
+  // when a slice is in global memory; the Eq. (5) weights of grad_gt alias inv, dead after
+  // the forward); the global-memory and grid-wide paths do
+  const bool f2 = c->fwd2 && !c->rs;  // (the grid-wide path ignores the cluster plan's fwd2)
+  const int64_t E1 = f2 ? 0 : E;
+  size_t o_csr_t = k.take<uint32_t>(E1), o_csc_t = k.take<uint32_t>(E1), o_inv = k.take<uint32_t>(E);
+  size_t o_csr_jf = k.take<uint32_t>(E), o_csc_i = k.take<uint32_t>(E), o_csc_perm = k.take<uint32_t>(E);
+  size_t o_d2 = k.take<float>(E1), o_cs = k.take<float>(E), o_prow = k.take<float>(E), o_pcol = k.take<float>(E);
+  size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
+  const int64_t E2 = f2 ? E : 0;  // CSC-order copies written by k_sparse_fwd2
+  size_t o_csc_if = k.take<uint32_t>(E2), o_csc_c = k.take<float>(E2), o_csc_pc = k.take<float>(E2);
+  c->ebytes = k.off;
+  c->ebase = (char*)ctx_alloc(c, c->ebytes);
+  if (!c->ebase) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->ebytes) + " bytes failed");
+  char* p = c->ebase;
+  c->csr_t = (uint32_t*)(p + o_csr_t); c->csc_t = (uint32_t*)(p + o_csc_t); c->inv = (uint32_t*)(p + o_inv);
+  c->csr_jf = (uint32_t*)(p + o_csr_jf); c->csc_i = (uint32_t*)(p + o_csc_i); c->csc_perm = (uint32_t*)(p + o_csc_perm);
+  c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
+  c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
+  c->csc_if = (uint32_t*)(p + o_csc_if); c->csc_c = (float*)(p + o_csc_c); c->csc_pc = (float*)(p + o_csc_pc);
+  return APML_OK;
+}
+
+// Per-entry capacity from the largest emitted count (read back): exact + a little.
+uint32_t fitted_cap(unsigned mx, uint32_t cap_e, double headroom) {
+  int64_t v = (int64_t)((double)mx * headroom) + 64;
+  v = (v + 63) / 64 * 64;
+  return (uint32_t)std::min<int64_t>(std::max<int64_t>(v, 64), cap_e);
+}
+
+// entries: allocate the per-entry arrays now (stride cap_e); else alloc_entries runs later.
+apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   const int64_t B = c->B, N = c->N, M = c->M, L = c->cfg.l_iter;
   c->cap = cap;
+  c->cap_e = cap;
   c->Np = round_up(N, kOwnTile);
   c->Mp = round_up(M, kOwnTile);
   // exact spatial culling of the sweeps pays off once a 512-point block is a small part of
@@ -333,10 +392,13 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   plan_sparse(c);
   Carve k;
   const int64_t E = B * (int64_t)cap;
+  // culled sweeps leave one (min, second) partial per line ([B][n], S = 1)
+  const int64_t parts_r = c->cull ? B * N : (int64_t)c->S_rows * B * c->Np;
+  const int64_t parts_c = c->cull ? B * M : (int64_t)c->S_cols * B * c->Mp;
   size_t o_predS = k.take<float>(B * 3 * c->Np), o_gtS = k.take<float>(B * 3 * c->Mp);
   size_t o_pred4 = k.take<float4>(B * N), o_gt4 = k.take<float4>(B * M);
-  size_t o_part_r = k.take<float2>((int64_t)c->S_rows * B * c->Np);
-  size_t o_part_c = k.take<float2>((int64_t)c->S_cols * B * c->Mp);
+  size_t o_part_r = k.take<float2>(parts_r);
+  size_t o_part_c = k.take<float2>(parts_c);
   size_t o_rowA = k.take<LineA>(B * N), o_colA = k.take<LineA>(B * M);
   size_t o_rowB = k.take<LineB>(B * N), o_colB = k.take<LineB>(B * M);
   const int64_t cells1 = c->cull ? ((int64_t)1 << (3 * c->cell_bits)) + 1 : 0;
@@ -349,14 +411,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   size_t z1 = k.off;
   size_t o_row_ptr = k.take<unsigned>(B * (N + 1)), o_col_ptr = k.take<unsigned>(B * (M + 1));
   size_t o_ebuf = k.take<uint2>(E);
-  size_t o_csr_t = k.take<uint32_t>(E), o_csc_t = k.take<uint32_t>(E), o_inv = k.take<uint32_t>(E);
-  size_t o_csr_jf = k.take<uint32_t>(E), o_csc_i = k.take<uint32_t>(E), o_csc_perm = k.take<uint32_t>(E);
-  size_t o_d2 = k.take<float>(E), o_cs = k.take<float>(E), o_prow = k.take<float>(E), o_pcol = k.take<float>(E);
-  size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
-  const int64_t E2 = c->fwd2 ? E : 0;  // CSC-order copies written by k_sparse_fwd2
   size_t o_nb = k.take<int>(c->ragged ? B : 0), o_mb = k.take<int>(c->ragged ? B : 0);
   size_t o_lr = k.take<float>(c->ragged ? 4 * B : 0);
-  size_t o_csc_if = k.take<uint32_t>(E2), o_csc_c = k.take<float>(E2), o_csc_pc = k.take<float>(E2);
   size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
   size_t o_ah = k.take<float>(B * N * (L + 1)), o_bh = k.take<float>(B * M * (L + 1));
   size_t o_gv = k.take<float>(B * 2 * (N + M));
@@ -393,11 +449,6 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->row_cnt = (unsigned*)(p + o_row_cnt); c->col_cnt = (unsigned*)(p + o_col_cnt);
   c->row_ptr = (unsigned*)(p + o_row_ptr); c->col_ptr = (unsigned*)(p + o_col_ptr);
   c->ebuf = (uint2*)(p + o_ebuf);
-  c->csr_t = (uint32_t*)(p + o_csr_t); c->csc_t = (uint32_t*)(p + o_csc_t); c->inv = (uint32_t*)(p + o_inv);
-  c->csr_jf = (uint32_t*)(p + o_csr_jf); c->csc_i = (uint32_t*)(p + o_csc_i); c->csc_perm = (uint32_t*)(p + o_csc_perm);
-  c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
-  c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
-  c->csc_if = (uint32_t*)(p + o_csc_if); c->csc_c = (float*)(p + o_csc_c); c->csc_pc = (float*)(p + o_csc_pc);
   if (c->ragged) {  // pageable host vectors: the copies are staged before the calls return
     c->nb_d = (int*)(p + o_nb); c->mb_d = (int*)(p + o_mb); c->lr_d = (float*)(p + o_lr);
     CK(cudaMemcpyAsync(c->nb_d, c->nb_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice, c->stream));
@@ -422,16 +473,17 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap) {
   c->zero_off = z0;
   c->zero_bytes = z1 - z0;
   CK(cudaMemsetAsync(p + z0, 0, z1 - z0, c->stream));
-  return APML_OK;
+  return entries ? alloc_entries(c, cap) : APML_OK;
 }
 
 SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, float* grad_pred) {
   SparseArgs a;
   a.N = (int)c->N; a.M = (int)c->M; a.L = c->cfg.l_iter; a.full = c->cfg.grad_mode == APML_GRAD_FULL;
-  a.cap = c->cap; a.eps = c->cfg.eps_stab; a.eps_dist = c->cfg.eps_dist;
+  a.cap = c->cap; a.cap_e = c->cap_e; a.eps = c->cfg.eps_stab; a.eps_dist = c->cfg.eps_dist;
   a.pred4 = c->pred4; a.gt4 = c->gt4; a.rowA = c->rowA; a.rowB = c->rowB; a.colA = c->colA; a.colB = c->colB;
   a.grad_gt = c->grad_gt;
-  a.gw = c->grad_gt ? c->d2s : nullptr;  // d2s is forward-only scratch: free in the backward
+  // Eq. (5) weights for grad_gt: forward-only scratch, free in the backward (fwd2: inv; else d2s)
+  a.gw = c->grad_gt ? ((c->fwd2 && !c->rs) ? (float*)c->inv : c->d2s) : nullptr;
   a.ebuf = c->ebuf; a.cursor = c->cursor; a.row_cnt = c->row_cnt; a.col_cnt = c->col_cnt;
   a.row_ptr = c->row_ptr; a.col_ptr = c->col_ptr; a.csr_t = c->csr_t; a.csc_t = c->csc_t; a.inv = c->inv;
   a.csr_jf = c->csr_jf; a.csc_i = c->csc_i; a.csc_perm = c->csc_perm;
@@ -605,11 +657,11 @@ apml_status launch_emit_cull(apml_ctx* c) {
   // here: C5 emit 0.532 -> 0.546 ms, C4 0.601 -> 0.648 ms
   if (env_long("APML_EMIT_R", kRc) == 1)
     k_emit_cull<1><<<dim3(Np / kSweepThreads, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
-        c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf,
+        c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap_e, c->ebuf,
         c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
   else
     k_emit_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
-        c->rowA, c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap, c->ebuf,
+        c->rowA, c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap_e, c->ebuf,
         c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
   c->launches += 2;
   CK(cudaGetLastError());
@@ -661,7 +713,7 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 4, s);
   // S3 Pass B emit
   k_emit<kR><<<dim3(Np / kOwnTile, c->S_emit, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_emit, c->cap, c->ebuf, c->cursor,
+      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_emit, c->cap_e, c->ebuf, c->cursor,
       c->aux, c->row_cnt, c->col_cnt, c->nb_d, c->mb_d);
   mark(c, 5, s);
   c->launches += 4;
@@ -750,7 +802,7 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
     if ((st = launch_emit_cull(c)) != APML_OK) return st;
   } else {
     k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
-        c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap, c->ebuf, c->cursor,
+        c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap_e, c->ebuf, c->cursor,
         c->aux, c->row_cnt, c->col_cnt, nullptr, nullptr);
   }
   mark(c, 5, s);
@@ -947,7 +999,7 @@ apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, i
     if ((st = check_finite(pred, B * N * 3, s)) != APML_OK) return st;
     if ((st = check_finite(gt, B * M * 3, s)) != APML_OK) return st;
   }
-  const int64_t per = c.capacity > 0 ? c.capacity : 6;
+  const int64_t per = c.capacity > 0 ? c.capacity : default_per(N, M);
   int64_t cap64 = per * (N + M);
   if (cap64 > N * M) cap64 = N * M;
   if (cap64 < 1) cap64 = 1;
@@ -976,10 +1028,11 @@ apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, i
       x->row_offset = 0;
       x->N_global = N;
     }
-    st = build_ctx(x, (uint32_t)cap64);
+    const bool sync = (c.flags & APML_FLAG_SYNC_CHECK) != 0;
+    st = build_ctx(x, (uint32_t)cap64, !sync);
     if (st == APML_OK) st = x->rs ? launch_forward_rs(x, pred, gt) : launch_forward(x, pred, gt);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
-    if (c.flags & APML_FLAG_SYNC_CHECK) {
+    if (sync) {
       std::vector<unsigned> cnt((size_t)B);
       cudaError_t e = cudaMemcpyAsync(cnt.data(), x->cursor, sizeof(unsigned) * (size_t)B,
                                       cudaMemcpyDeviceToHost, s);
@@ -995,6 +1048,8 @@ apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, i
         if (cap64 > N * M) cap64 = N * M;
         continue;
       }
+      // the per-entry arrays at the support actually emitted (the largest pair's count)
+      if ((st = alloc_entries(x, fitted_cap(mx, x->cap_e, 1.0))) != APML_OK) { apml_ctx_destroy(x); return st; }
     }
     st = x->rs ? launch_sparse_fwd_rs(x, loss) : launch_sparse_fwd(x, loss);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
@@ -1023,7 +1078,7 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
   if (!loss) return fail(APML_ERR_INVALID_ARG, "loss must be a non-NULL device pointer");
   if (alloc && (!alloc->alloc || !alloc->free)) return fail(APML_ERR_INVALID_ARG, "allocator needs alloc and free");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t per = c.capacity > 0 ? c.capacity : 6;
+  const int64_t per = c.capacity > 0 ? c.capacity : default_per(N_global, M);
   int64_t cap64 = std::min<int64_t>(per * (N + M), N * M);
   if (cap64 < 1) cap64 = 1;
   if (cap64 >= ((int64_t)1 << 31)) return fail(APML_ERR_SHAPE, "emit capacity exceeds 2^31 per-pair positions");
@@ -1043,10 +1098,11 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
     const double lt = c.tau > 0.f ? -std::log((double)c.tau) : INFINITY;
     x->rho_r = M > 1 ? (float)(lt / lambda_K(M, p)) : INFINITY;
     x->rho_c = N_global > 1 ? (float)(lt / lambda_K(N_global, p)) : INFINITY;
-    st = build_ctx(x, (uint32_t)cap64);
+    const bool sync = (c.flags & APML_FLAG_SYNC_CHECK) != 0;
+    st = build_ctx(x, (uint32_t)cap64, !sync);
     if (st == APML_OK) st = launch_forward_rs(x, pred, gt);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
-    if (c.flags & APML_FLAG_SYNC_CHECK) {  // collective: every rank retries together
+    if (sync) {  // collective: every rank retries together
       std::vector<unsigned> cnt((size_t)B);
       cudaError_t e = cudaMemcpyAsync(cnt.data(), x->cursor, sizeof(unsigned) * (size_t)B, cudaMemcpyDeviceToHost, s);
       if (e == cudaSuccess) e = cudaStreamSynchronize(s);
@@ -1067,6 +1123,7 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
         cap64 = std::min<int64_t>(std::max<int64_t>(cap64, round_up((int64_t)mx + (int64_t)mx / 16 + 16, 64)), N * M);
         continue;
       }
+      if ((st = alloc_entries(x, fitted_cap(mx, x->cap_e, 1.0))) != APML_OK) { apml_ctx_destroy(x); return st; }
     }
     st = launch_sparse_fwd_rs(x, loss);
     if (st != APML_OK) { apml_ctx_destroy(x); return st; }
@@ -1160,7 +1217,7 @@ apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats*
   for (int k = 0; k < 3; ++k)  // culled: counted on the device; otherwise every padded (i, j)
     st.sweep_evals[k] = x->cull ? (int64_t)cnt[1 + k] : B * x->Np * x->Mp;
   st.capacity = x->cap;
-  st.bytes_ctx = (int64_t)x->bytes;
+  st.bytes_ctx = (int64_t)(x->bytes + x->ebytes);
   st.launches = x->launches;
   if (out) *out = st;
   return APML_OK;
@@ -1313,7 +1370,10 @@ apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config*
     x->row_offset = 0;
     x->N_global = N;
   }
-  if ((st = build_ctx(x, (uint32_t)cap64)) != APML_OK) { apml_ctx_destroy(x); return st; }
+  // per-entry arrays: sized on the first forward from its support (x 1.5 headroom) unless the
+  // caller fixed the capacity (cfg->capacity > 0)
+  x->calibrate = c.capacity <= 0;
+  if ((st = build_ctx(x, (uint32_t)cap64, !x->calibrate)) != APML_OK) { apml_ctx_destroy(x); return st; }
   *plan_out = x;
   return APML_OK;
 }
@@ -1331,6 +1391,21 @@ apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, v
   x->bwd_timed = false;
   x->grad_gt = nullptr;
   apml_status st = x->rs ? launch_forward_rs(x, pred, gt) : launch_forward(x, pred, gt);
+  if (st == APML_OK && !x->ebase) {
+    // first forward of a calibrating plan: the per-entry arrays at 1.5 x the largest support
+    // of this forward (one count read-back, this call only); inside a graph capture (no
+    // read-back possible) at the emit capacity
+    uint32_t cap = x->cap_e;
+    if (!capturing(x->stream)) {
+      std::vector<unsigned> cnt((size_t)x->B);
+      CK(cudaMemcpyAsync(cnt.data(), x->cursor, sizeof(unsigned) * (size_t)x->B, cudaMemcpyDeviceToHost, x->stream));
+      CK(cudaStreamSynchronize(x->stream));
+      unsigned mx = 0;
+      for (unsigned v : cnt) mx = v > mx ? v : mx;
+      cap = fitted_cap(mx, x->cap_e, 1.5);
+    }
+    st = alloc_entries(x, cap);
+  }
   if (st == APML_OK) st = x->rs ? launch_sparse_fwd_rs(x, loss) : launch_sparse_fwd(x, loss);
   if (st == APML_OK) x->forward_done = true;
   return st;
@@ -1363,7 +1438,8 @@ apml_status apml_plan_step_host(apml_ctx* x, const float* pred_host, const float
   CK(cudaMemcpyAsync(d_gt, gt_host, bg, cudaMemcpyHostToDevice, s));
   // the device part (forward + backward, ~6 launches) is captured once into a graph owned by
   // the plan; the legacy default stream cannot be captured (eager there, and APML_HOST_GRAPH=0)
-  const bool graph = s != nullptr && env_long("APML_HOST_GRAPH", 1) != 0;
+  // (a calibrating plan's first forward sizes its per-entry arrays eagerly: captured later)
+  const bool graph = s != nullptr && env_long("APML_HOST_GRAPH", 1) != 0 && x->ebase != nullptr;
   apml_status st = APML_OK;
   if (graph && !x->hstep) {
     CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));

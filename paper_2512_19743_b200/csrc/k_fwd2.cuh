@@ -453,11 +453,11 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
     C.pr = reinterpret_cast<float*>(carve(sm, 4 * (size_t)nnzc));
   } else {
     R.idx = A.csr_jf + pb + gr;
-    R.t = A.csr_t + pb + gr;
+    R.t = reinterpret_cast<uint32_t*>(A.cs + pb + gr);  // emit indices, then c (R.c aliases R.t)
     R.val = A.P0 + pb + gr;
     R.pr = A.prow + pb + gr;
     C.idx = A.csc_i + pb + gc;
-    C.t = A.csc_t + pb + gc;
+    C.t = reinterpret_cast<uint32_t*>(A.csc_c + pb + gc);
     C.val = A.P0c + pb + gc;
     C.pr = A.pbar + pb + gc;
   }
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
     for (uint32_t t0 = threadIdx.x; t0 < total; t0 += kU * bd) {
       uint2 e[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) e[u] = t0 + u * bd < total ? A.ebuf[pb + t0 + u * bd] : make_uint2(~0u, ~0u);
+      for (int u = 0; u < kU; ++u) e[u] = t0 + u * bd < total ? ebuf_of(A, b)[t0 + u * bd] : make_uint2(~0u, ~0u);
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const uint32_t t = t0 + u * bd;

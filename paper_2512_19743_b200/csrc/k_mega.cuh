@@ -36,7 +36,9 @@ constexpr int kMaxCluster = 16;
 
 struct SparseArgs {
   int N, M, L, full;
-  uint32_t cap;
+  uint32_t cap;    // per-pair stride of the per-entry arrays (>= every pair's emitted count, or
+                   // the pair is skipped as overflowed)
+  uint32_t cap_e;  // per-pair stride of the emit buffer (the emit capacity, >= cap)
   float eps, eps_dist;
   const float4* pred4;
   const float4* gt4;
@@ -44,7 +46,7 @@ struct SparseArgs {
   const LineB* rowB;
   const LineA* colA;
   const LineB* colB;
-  const uint2* ebuf;
+  const uint2* ebuf;  // [B][cap_e]
   const unsigned* cursor;
   unsigned* row_cnt;  // counts from k_emit; zeroed here and reused as fill cursors
   unsigned* col_cnt;
@@ -96,6 +98,8 @@ struct SparseArgs {
   const int* ipperm;
   int perm_np, perm_mp;
 };
+
+__device__ __forceinline__ const uint2* ebuf_of(const SparseArgs& A, int b) { return A.ebuf + (size_t)b * A.cap_e; }
 
 __device__ __forceinline__ uint32_t orig_row(const SparseArgs& A, int b, uint32_t i) {
   return A.pperm ? (uint32_t)A.pperm[(size_t)b * A.perm_np + i] : i;
@@ -222,7 +226,7 @@ __device__ void sort_lines(const SparseArgs& A, int b, Slice s, const LongList& 
   const int n = kRows ? A.N : A.M;
   const unsigned* ptr = (kRows ? A.row_ptr : A.col_ptr) + (size_t)b * (n + 1);
   const uint32_t* seg_t = (kRows ? A.csr_t : A.csc_t) + pb;
-  const uint2* e = A.ebuf + pb;
+  const uint2* e = ebuf_of(A, b);
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   (void)nw;
   APML_FOR_LINES(32, s, ll, line) {
@@ -397,7 +401,7 @@ __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
 #pragma unroll
       for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
 #pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? A.ebuf[pb + t[k]].y : 0u;
+      for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? ebuf_of(A, b)[t[k]].y : 0u;
 #pragma unroll
       for (uint32_t k = 0; k < kRegLine; ++k) ok[k] = k < L ? orig_col(A, b, jf[k] & kIdxMask) : 0xffffffffu;
 #pragma unroll
@@ -466,7 +470,7 @@ __device__ void col_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
       for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csc_t[pb + beg + k] : 0u;
 #pragma unroll
       for (uint32_t k = 0; k < kRegLine; ++k) {
-        key[k] = k < L ? A.ebuf[pb + t[k]].x : 0xffffffffu;
+        key[k] = k < L ? ebuf_of(A, b)[t[k]].x : 0xffffffffu;
         pp[k] = k < L ? A.inv[pb + t[k]] : 0u;
       }
 #pragma unroll
@@ -910,7 +914,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs
 #pragma unroll
       for (int u = 0; u < kSc; ++u) {
         const uint32_t t = t0 + u * stride;
-        const uint2 e = t < total ? A.ebuf[pb + t] : make_uint2(0u, 0u);
+        const uint2 e = t < total ? ebuf_of(A, b)[t] : make_uint2(0u, 0u);
         ii[u] = e.x;
         jj[u] = e.y & kIdxMask;
       }

@@ -159,7 +159,7 @@ __global__ void k_rs_scatter(const SparseArgs A) {
   const unsigned total = A.cursor[b];
   if (total > A.cap || t >= total) return;
   const size_t pb = (size_t)b * A.cap;
-  const uint2 e = A.ebuf[pb + t];
+  const uint2 e = ebuf_of(A, b)[t];
   const uint32_t i = e.x, j = e.y & kIdxMask;
   const size_t rb = (size_t)b * (A.N + 1), cb = (size_t)b * (A.M + 1);
   A.csr_t[pb + A.row_ptr[rb + i] + atomicAdd(A.row_cnt + rb + i, 1u)] = t;
@@ -205,9 +205,9 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
     const size_t pb = (size_t)b * A.cap;
     for (uint32_t q = beg + 1; q < end; ++q) {
       const uint32_t t = A.csc_t[pb + q];
-      const uint32_t key = orig_row(A, b, A.ebuf[pb + t].x);
+      const uint32_t key = orig_row(A, b, ebuf_of(A, b)[t].x);
       uint32_t r = q;
-      while (r > beg && orig_row(A, b, A.ebuf[pb + A.csc_t[pb + r - 1]].x) > key) {
+      while (r > beg && orig_row(A, b, ebuf_of(A, b)[A.csc_t[pb + r - 1]].x) > key) {
         A.csc_t[pb + r] = A.csc_t[pb + r - 1];
         --r;
       }
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
     }
     for (uint32_t q = beg; q < end; ++q) {
       const uint32_t t = A.csc_t[pb + q];
-      A.csc_i[pb + q] = A.ebuf[pb + t].x;
+      A.csc_i[pb + q] = ebuf_of(A, b)[t].x;
       A.csc_perm[pb + q] = A.inv[pb + t];
     }
   }

@@ -7,6 +7,10 @@
 //   mode 4: local stores + barrier.cluster only (lower bound: no data movement)
 //   mode 5: mode 0 + a global store per element per round (the Sinkhorn history)
 //   mode 6: mode 0 + a 6-entry gather dot product per element (idx/val in shared memory)
+//   mode 7: mode 0 with v4 pushes: each group of 4 lanes gathers its 4 consecutive values by
+//           shuffles and lane q of the group sends the 16-byte vector to rank q (one st.async
+//           per lane instead of CL)
+//   mode 8: mode 7 + the 6-entry gather dot product of mode 6
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o xb xchg_bench.cu && ./xb
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -34,7 +38,7 @@ __global__ void __launch_bounds__(512, 1) xb(int rounds, int n, unsigned long lo
   const int per = n / CL, lo = me * per, hi = lo + per;
   float* rep[2] = {sm, sm + n};
   for (int k = threadIdx.x; k < 2 * n; k += blockDim.x) sm[k] = 1.f;
-  if (MODE == 6) {
+  if (MODE == 6 || MODE == 8) {
     unsigned short* ix = reinterpret_cast<unsigned short*>(sm + 2 * n);
     float* vv = sm + 2 * n + 3 * n;
     for (int k = threadIdx.x; k < 6 * per; k += blockDim.x) { ix[k] = (unsigned short)((k * 2654435761u) % n); vv[k] = 0.1f; }
@@ -43,7 +47,7 @@ __global__ void __launch_bounds__(512, 1) xb(int rounds, int n, unsigned long lo
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sa(&mbar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(sa(&mbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const uint32_t e = (MODE == 0 || MODE >= 5) ? 4u * n : 4u * (n - per);
+    const uint32_t e = (MODE == 0 || MODE >= 5) ? 4u * n : 4u * (n - per);  // modes 7/8: CL == 4
     arm(sa(&mbar[0]), e); arm(sa(&mbar[1]), e);
   }
   cl.sync();
@@ -64,6 +68,28 @@ __global__ void __launch_bounds__(512, 1) xb(int rounds, int n, unsigned long lo
 #pragma unroll
         for (int u = 0; u < 6; ++u) s = fmaf(src[ix[6 * (k - lo) + u]], vv[6 * (k - lo) + u], s);
         v = __fdividef(v, fmaf(v, s, 1e-8f));
+      }
+      if (MODE == 8) {
+        const unsigned short* ix = reinterpret_cast<const unsigned short*>(sm + 2 * n);
+        const float* vv = sm + 2 * n + 3 * n;
+        float s = 0.f;
+#pragma unroll
+        for (int u = 0; u < 6; ++u) s = fmaf(src[ix[6 * (k - lo) + u]], vv[6 * (k - lo) + u], s);
+        v = __fdividef(v, fmaf(v, s, 1e-8f));
+      }
+      if (MODE == 7 || MODE == 8) {  // (k - lo) % 4 == lane % 4: per multiple of 4, CL == 4
+        const int lane = threadIdx.x & 31, q = lane & 3, g0 = lane & ~3;
+        float4 v4;
+        v4.x = __shfl_sync(0xffffffffu, v, g0);
+        v4.y = __shfl_sync(0xffffffffu, v, g0 + 1);
+        v4.z = __shfl_sync(0xffffffffu, v, g0 + 2);
+        v4.w = __shfl_sync(0xffffffffu, v, g0 + 3);
+        if (q < CL) {
+          const uint32_t a = sa(dst + (k & ~3));
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
+                       :: "r"(mapa(a, q)), "r"(__float_as_uint(v4.x)), "r"(__float_as_uint(v4.y)),
+                          "r"(__float_as_uint(v4.z)), "r"(__float_as_uint(v4.w)), "r"(mapa(mb, q)) : "memory");
+        }
       }
       if (MODE == 5) hist[(size_t)it * n + k] = v;
       if (MODE == 0 || MODE == 5 || MODE == 6) {
@@ -117,7 +143,7 @@ void run(int CL, int n, int B) {
   unsigned long long* d; cudaMalloc(&d, 8 * B * CL);
   float* hist; cudaMalloc(&hist, sizeof(float) * 200 * (size_t)n * 1);
   auto k = xb<MODE>;
-  const int smem = 8 * n + (MODE == 6 ? 4 * n * 6 : 0);
+  const int smem = 8 * n + ((MODE == 6 || MODE == 8) ? 4 * n * 6 : 0);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(B * CL); cfg.blockDim = dim3(512); cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = CL;
@@ -135,6 +161,7 @@ int main() {
   for (int CL : {4}) for (int n : {2048}) {
     const int B = 128 / CL;
     run<0>(CL, n, B); run<1>(CL, n, B); run<4>(CL, n, B); run<5>(CL, n, B); run<6>(CL, n, B);
+    run<7>(CL, n, B); run<8>(CL, n, B);
   }
   return 0;
 }
