@@ -80,6 +80,15 @@ typedef enum {
 #define APML_FLAG_CHECK_FINITE 2u /* scan the inputs for NaN/Inf first (one extra pass + sync) */
 #define APML_FLAG_STAGE_TIMING 4u /* record CUDA events between the stages below (on the launch
                                      stream); read them with apml_ctx_stage_times */
+#define APML_FLAG_UNIFORM_FALLBACK 8u /* stability mode of dense APML (the sparse kernel
+                                     "writes a uniform distribution over the corresponding row
+                                     or column") instead of the gap clamp of CUDA-APML
+                                     (the default): a line whose gap c~(2) = c2 - m is
+                                     below eps_g keeps all K entries with P = 1/K and passes no
+                                     gradient through its softmax.  Opt-in, for parity studies:
+                                     such a line is dense (K entries), outside the O(nnz) memory
+                                     contract; the capacity retry (APML_FLAG_SYNC_CHECK) sizes
+                                     for it. */
 
 /* Stages timed with APML_FLAG_STAGE_TIMING (indices into apml_ctx_stage_times' output). */
 enum {
@@ -133,6 +142,7 @@ typedef struct {
                                forward: [0] Pass A rows, [1] Pass A columns, [2] emit.  Full
                                sweeps: every padded pair (B Np Mp); spatially culled sweeps:
                                counted on the device (32 x 32 blocks actually evaluated) */
+    int64_t uniform_count;  /* lines given the uniform fallback (APML_FLAG_UNIFORM_FALLBACK) */
 } apml_stats;
 
 /* Caller-supplied, stream-ordered collectives for the row-sharded mode (torch.distributed /

@@ -16,7 +16,7 @@ APML_OK, APML_ERR_INVALID_ARG, APML_ERR_SHAPE, APML_ERR_NONFINITE, APML_ERR_CAPA
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NONFINITE", 4: "CAPACITY", 5: "CUDA",
                 6: "OOM", 7: "STATE"}
 APML_GRAD_FULL, APML_GRAD_PLAN_DETACHED = 0, 1
-APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE, APML_FLAG_STAGE_TIMING = 1, 2, 4
+APML_FLAG_SYNC_CHECK, APML_FLAG_CHECK_FINITE, APML_FLAG_STAGE_TIMING, APML_FLAG_UNIFORM_FALLBACK = 1, 2, 4, 8
 STAGES = ("staging", "passA_rows", "passA_cols", "line_info", "emit", "sparse_fwd", "sparse_bwd")
 
 # exported symbols declared in include/apml.h (checked by tests/test_abi.py)
@@ -55,7 +55,7 @@ class ApmlComm(C.Structure):
 class ApmlStats(C.Structure):
     _fields_ = [("nnz_total", C.c_int64), ("emitted_total", C.c_int64), ("clamp_count", C.c_int64),
                 ("capacity", C.c_int64), ("overflow_pairs", C.c_int64), ("bytes_ctx", C.c_int64),
-                ("launches", C.c_int64), ("sweep_evals", C.c_int64 * 3)]
+                ("launches", C.c_int64), ("sweep_evals", C.c_int64 * 3), ("uniform_count", C.c_int64)]
 
 
 class ApmlError(RuntimeError):

@@ -32,11 +32,15 @@ class Config:
     sync_check: bool = True          # read back support counts and retry on overflow
     check_finite: bool = False
     stage_timing: bool = False       # CUDA events between stages (apml_ctx_stage_times)
+    stability: str = "clamp"         # "clamp" (CUDA-APML) | "uniform" (P:64 / P:97 fallback)
 
     def to_c(self) -> A.ApmlConfig:
         if self.grad_mode not in ("full", "plan_detached"):
             raise ValueError(f"grad_mode must be 'full' or 'plan_detached', got {self.grad_mode!r}")
-        flags = (A.APML_FLAG_SYNC_CHECK if self.sync_check else 0) | \
+        if self.stability not in ("clamp", "uniform"):
+            raise ValueError(f"stability must be 'clamp' or 'uniform', got {self.stability!r}")
+        flags = (A.APML_FLAG_UNIFORM_FALLBACK if self.stability == "uniform" else 0) | \
+            (A.APML_FLAG_SYNC_CHECK if self.sync_check else 0) | \
             (A.APML_FLAG_CHECK_FINITE if self.check_finite else 0) | \
             (A.APML_FLAG_STAGE_TIMING if self.stage_timing else 0)
         return A.ApmlConfig(self.p_min, self.tau, self.l_iter, self.eps_stab, self.delta, self.eps_g,
@@ -78,7 +82,7 @@ class Context:
         return dict(nnz=list(nnz), nnz_total=st.nnz_total, emitted_total=st.emitted_total,
                     clamp_count=st.clamp_count, capacity=st.capacity,
                     overflow_pairs=st.overflow_pairs, bytes_ctx=st.bytes_ctx, launches=st.launches,
-                    sweep_evals=list(st.sweep_evals))
+                    sweep_evals=list(st.sweep_evals), uniform_count=st.uniform_count)
 
     def stage_times(self) -> dict:
         """Per-stage device milliseconds (needs Config(stage_timing=True)); synchronises."""

@@ -238,6 +238,8 @@ int64_t default_per(int64_t N, int64_t M) {
   return nm < 2048 ? 6 : nm < 8192 ? 5 : nm < 65536 ? 4 : 3;
 }
 
+int ufb(const apml_ctx* c) { return (c->cfg.flags & APML_FLAG_UNIFORM_FALLBACK) ? 1 : 0; }
+
 // Lambda_K = -log((1 - p) / ((K - 1) p)) (numerator of Eq. (1)), fp64.
 double lambda_K(int64_t K, double p) { return K > 1 ? -std::log((1.0 - p) / ((double)(K - 1) * p)) : 0.0; }
 
@@ -405,7 +407,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   // counters in one contiguous zeroed block
   size_t z0 = k.off;
   size_t o_phist = k.take<uint32_t>(B * cells1), o_ghist = k.take<uint32_t>(B * cells1);
-  size_t o_clamp = k.take<unsigned long long>(4);  // clamp count + culled-sweep evaluations [3]
+  size_t o_clamp = k.take<unsigned long long>(5);  // clamp count, culled-sweep evaluations [3], uniform lines
   size_t o_cursor = k.take<unsigned>(B), o_aux = k.take<unsigned>(B);
   size_t o_row_cnt = k.take<unsigned>(B * (N + 1)), o_col_cnt = k.take<unsigned>(B * (M + 1));
   size_t z1 = k.off;
@@ -677,9 +679,9 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     if (st != APML_OK) return st;
     mark(c, 3, s);
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, 1, B, N, N, M, c->lam_r, c->rho_r,
-        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
+        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0, ufb(c));
     k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, N, c->lam_c, c->rho_c,
-        c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
+        c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2, ufb(c));
     mark(c, 4, s);
     if ((st = launch_emit_cull(c)) != APML_OK) return st;
     mark(c, 5, s);
@@ -708,7 +710,7 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     const LineInfoDir lr_{c->part_r, c->S_rows, (int)Np, N, M, c->lam_r, c->rho_r, c->rowA, c->rowB, c->nb_d, c->mb_d, 0};
     const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2};
     k_line_info_both<<<dim3((std::max(N, M) + 255) / 256, B, 2), 256, 0, s>>>(lr_, lc_, B, c->cfg.delta, c->cfg.eps_g,
-                                                                             c->clamp, c->lr_d);
+                                                                             c->clamp, c->lr_d, ufb(c));
   }
   mark(c, 4, s);
   // S3 Pass B emit
@@ -791,12 +793,12 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
   mark(c, 3, s);
   if (c->cull)
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, 1, B, N, N, M, c->lam_r, c->rho_r,
-        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
+        c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0, ufb(c));
   else
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
-        c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0);
+        c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0, ufb(c));
   k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->gath, c->comm.world, B, M, M, (int)c->N_global,
-      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2);
+      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2, ufb(c));
   mark(c, 4, s);
   if (c->cull) {
     if ((st = launch_emit_cull(c)) != APML_OK) return st;
@@ -1200,7 +1202,7 @@ apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats*
   if (!x) return fail(APML_ERR_STATE, "NULL context");
   const int64_t B = x->B;
   std::vector<unsigned> cur((size_t)B), aux((size_t)B);
-  unsigned long long cnt[4] = {0, 0, 0, 0};
+  unsigned long long cnt[5] = {0, 0, 0, 0, 0};
   CK(cudaMemcpyAsync(cur.data(), x->cursor, sizeof(unsigned) * B, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaMemcpyAsync(aux.data(), x->aux, sizeof(unsigned) * B, cudaMemcpyDeviceToHost, x->stream));
   CK(cudaMemcpyAsync(cnt, x->clamp, sizeof(cnt), cudaMemcpyDeviceToHost, x->stream));
@@ -1214,6 +1216,7 @@ apml_status apml_ctx_stats(const apml_ctx* x, int64_t* nnz_per_pair, apml_stats*
     if (cur[b] > x->cap) st.overflow_pairs++;
   }
   st.clamp_count = (int64_t)cnt[0];
+  st.uniform_count = (int64_t)cnt[4];
   for (int k = 0; k < 3; ++k)  // culled: counted on the device; otherwise every padded (i, j)
     st.sweep_evals[k] = x->cull ? (int64_t)cnt[1 + k] : B * x->Np * x->Mp;
   st.capacity = x->cap;

@@ -21,6 +21,7 @@ constexpr uint32_t kIdxMask = (1u << 30) - 1u;
 // Line flags stored in LineB.w (as bits of a float via __int_as_float).
 constexpr int kLineK1 = 1;       // K == 1 line: P = 1 on its single entry
 constexpr int kLineClamped = 2;  // gap clamp active: no gradient through g
+constexpr int kLineUniform = 4;  // uniform fallback: T = 0, all K entries, P = 1/K
 
 // Per-line constants (S2).  LineA = {m2, s2, R2, E2}: squared min, squared second min,
 // squared kept radius (s >= tau  <=>  d2 <= R2), squared emit radius (max(R2, s2): the

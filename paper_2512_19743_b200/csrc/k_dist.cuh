@@ -172,6 +172,10 @@ __global__ void __launch_bounds__(kSweepThreads) k_line_top2_both(const Top2Dir 
 
 // S2: one thread per line.  lam = Lambda_K (fp64 on the host, rounded), rho = ln(1/tau) /
 // Lambda_K (+inf for tau = 0).  K == 1 lines keep their single entry with P = 1.
+// ufb (APML_FLAG_UNIFORM_FALLBACK, the stability mode of P:64 / P:97 instead of the clamp of
+// P:140): a line whose gap c~(2) = c2 - m is below eps_g keeps ALL K entries with P = 1/K --
+// T = 0 makes every similarity exp(-0 (c - m)) = 1, the infinite radii emit the whole line,
+// and with T = 0 the softmax reverse passes no gradient (P constant), as the oracle does.
 // Ragged batches (nown != NULL): pair b has nown[b] real lines of length K = kpair[b], with
 // lam / rho = lr[4 b + lr_off], lr[4 b + lr_off + 1]; the padding lines are inactive (radii
 // -1: nothing emitted; no entries downstream).
@@ -180,7 +184,7 @@ __device__ __forceinline__ void line_info(const float2* __restrict__ part, int S
                                           LineA* __restrict__ A, LineB* __restrict__ Bo,
                                           unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
                                           const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off,
-                                          int b, int k) {
+                                          int b, int k, int ufb) {
   if (k >= n) return;
   if (nown) {
     if (k >= nown[b]) {
@@ -211,15 +215,22 @@ __device__ __forceinline__ void line_info(const float2* __restrict__ part, int S
     o = {__fsqrt_rn(m2), 0.f, 0.f, kLineK1};
   } else {
     const float m = __fsqrt_rn(m2), c2 = __fsqrt_rn(s2);
-    float g = __fadd_rn(__fsub_rn(c2, m), delta);       // g = c~(2) + delta
-    int flags = 0;
-    if (g < eps_g) { g = eps_g; flags |= kLineClamped; } // max(gap, eps_g)
-    const float T = __fdiv_rn(lam, g);                   // Eq. (1)
-    const float R = __fadd_rn(m, __fmul_rn(rho, g));     // s >= tau <=> c <= R
-    float R2 = fmaxf(__fmul_rn(R, R), m2);               // the argmin (s = 1) is always kept
-    a = {m2, s2, R2, fmaxf(R2, s2)};
-    o = {m, T, g, flags};
-    if (flags & kLineClamped) atomicAdd(clamp_count, 1ull);
+    const float gap = __fsub_rn(c2, m);                  // c~(2)
+    if (ufb && gap < eps_g) {                            // uniform fallback
+      a = {m2, s2, inf, inf};
+      o = {m, 0.f, fmaxf(__fadd_rn(gap, delta), eps_g), kLineUniform};
+      atomicAdd(clamp_count + 4, 1ull);
+    } else {
+      float g = __fadd_rn(gap, delta);                   // g = c~(2) + delta
+      int flags = 0;
+      if (g < eps_g) { g = eps_g; flags |= kLineClamped; } // max(gap, eps_g)
+      const float T = __fdiv_rn(lam, g);                 // Eq. (1)
+      const float R = __fadd_rn(m, __fmul_rn(rho, g));   // s >= tau <=> c <= R
+      float R2 = fmaxf(__fmul_rn(R, R), m2);             // the argmin (s = 1) is always kept
+      a = {m2, s2, R2, fmaxf(R2, s2)};
+      o = {m, T, g, flags};
+      if (flags & kLineClamped) atomicAdd(clamp_count, 1ull);
+    }
   }
   A[(size_t)b * n + k] = a;
   Bo[(size_t)b * n + k] = o;
@@ -229,9 +240,9 @@ __global__ void k_line_info(const float2* __restrict__ part, int S, int B, int o
                             int K, float lam, float rho, float delta, float eps_g,
                             LineA* __restrict__ A, LineB* __restrict__ Bo,
                             unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
-                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off) {
+                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off, int ufb) {
   line_info(part, S, B, own_np, n, K, lam, rho, delta, eps_g, A, Bo, clamp_count, nown, kpair, lr, lr_off,
-            blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
+            blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb);
 }
 
 // Rows and columns in ONE launch (grid.z = 2: rows, columns; grid.y = pair).
@@ -246,10 +257,10 @@ struct LineInfoDir {
   int lr_off;
 };
 __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int B, float delta, float eps_g,
-                                 unsigned long long* __restrict__ clamp_count, const float* __restrict__ lr) {
+                                 unsigned long long* __restrict__ clamp_count, const float* __restrict__ lr, int ufb) {
   const LineInfoDir& d = blockIdx.z ? d1 : d0;
   line_info(d.part, d.S, B, d.own_np, d.n, d.K, d.lam, d.rho, delta, eps_g, d.A, d.Bo, clamp_count, d.nown,
-            d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
+            d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb);
 }
 
 // Emission (S3).  Counts keep running past the capacity so the host can size a retry;

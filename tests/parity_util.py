@@ -72,13 +72,13 @@ def well_conditioned(x, y, plan, cfg, thresh=1e6, skip_clamped=False) -> np.ndar
     ok = np.ones(N, bool)
     if M > 1:
         bad_r = _lam(M, cfg.p_min) * s * s / np.maximum(rows["g"], 1e-300) ** 2 >= thresh
-        if skip_clamped:
-            bad_r &= rows["clamped"] == 0
+        if skip_clamped:  # (and uniform-fallback lines: T = 0, no T-path gradient either)
+            bad_r &= (rows["clamped"] == 0) & (rows["uniform"] == 0)
         ok &= ~bad_r
     if N > 1:
         bad_c = _lam(N, cfg.p_min) * s * s / np.maximum(cols["g"], 1e-300) ** 2 >= thresh
         if skip_clamped:
-            bad_c &= cols["clamped"] == 0
+            bad_c &= (cols["clamped"] == 0) & (cols["uniform"] == 0)
         for j in np.nonzero(bad_c)[0]:
             for i in (cols["a"][j], cols["b"][j]):
                 if i >= 0:

@@ -33,7 +33,8 @@ def _gpu():
 def _ocfg(cfg) -> OracleConfig:
     return OracleConfig(p_min=cfg.p_min, tau=cfg.tau, l_iter=cfg.l_iter, eps_stab=cfg.eps_stab,
                         delta=cfg.delta, eps_g=cfg.eps_g, eps_dist=cfg.eps_dist,
-                        grad_mode=0 if cfg.grad_mode == "full" else 1)
+                        grad_mode=0 if cfg.grad_mode == "full" else 1,
+                        stability=1 if cfg.stability == "uniform" else 0)
 
 
 def _run(x, y, cfg):
@@ -695,3 +696,45 @@ def test_memory_follows_the_support():
     assert torch.equal(lp, lf) and torch.equal(gp, gf) and torch.equal(lp, loss) and torch.equal(gp, g)
     assert ps["bytes_ctx"] < fixed.stats()["bytes_ctx"]
     plan.close(); fixed.close()
+
+
+@pytest.mark.parametrize("env", [{}, {"APML_FWD2": "0"}, {"APML_GRID": "1"}, {"APML_CULL": "1"}],
+                         ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()) or "default")
+@pytest.mark.parametrize("mode", ["full", "plan_detached"])
+def test_uniform_fallback_mode(env, mode, monkeypatch):
+    """the uniform-fallback stability mode (APML_FLAG_UNIFORM_FALLBACK, P:64,
+    P:97) against the oracle's stability = 1 on a duplicated-point fixture: lines whose gap is
+    below eps_g keep all K entries with P = 1/K (T = 0, no softmax gradient); everything else
+    as the default mode.  Loss, support and flags, per-entry P0 / v, gradient."""
+    Config, _ = _gpu()
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(3)
+    B, N, M = 2, 300, 260
+    y = rng.uniform(size=(B, M, 3)).astype(np.float32)
+    y[:, 200:230] = y[:, 10:40]                 # duplicated gt points: rows with gap 0
+    x = rng.uniform(size=(B, N, 3)).astype(np.float32)
+    x[:, 250:270] = x[:, 0:20]                  # duplicated pred points: columns with gap 0
+    cfg = Config(stability="uniform", grad_mode=mode)
+    lg, gg, ctx = _run(x, y, cfg)
+    oc = _ocfg(cfg)
+    st = ctx.stats()
+    nu = 0
+    for b in range(B):
+        plan = SparsePlan(x[b], y[b], oc)
+        nu += int(plan.lines(0)["uniform"].sum() + plan.lines(1)["uniform"].sum())
+        rel = abs(lg[b] - plan.loss) / plan.loss
+        assert rel <= LOSS_RTOL, f"pair {b}: loss rel {rel:.3e}"
+        gs, os_ = ctx.support(b), plan.support()
+        only_g, only_o = support_diff(gs, os_)
+        assert not (only_g or only_o), f"pair {b}: support differs ({len(only_g)}, {len(only_o)})"
+        assert flags_map(gs) == flags_map(os_)
+        _check_plan_values(x[b], y[b], cfg, plan, gs, os_, b)
+        gx, _ = plan.backward(1.0)
+        mask = well_conditioned(x[b], y[b], plan, oc, skip_clamped=True) if mode == "full" else np.ones(N, bool)
+        assert mask.mean() > 0.9
+        e = normwise(gg[b][mask], gx[mask])
+        assert e <= GRAD_RTOL, f"pair {b}: grad normwise {e:.3e}"
+    assert st["uniform_count"] == nu and nu >= 20
+    # the uniform lines really are dense: each duplicated-minimum row keeps all M entries
+    assert st["nnz_total"] >= nu * min(N, M) // 2
