@@ -286,6 +286,8 @@ def main():
                     help="N > 1 batch sharding: weak = B pairs per rank; strong = the config's B split "
                          "over the ranks (auto: strong for C3/C3R/C4, whose BASELINE configs fix the "
                          "global batch; weak for C2)")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="initialise NCCL and take the multi-GPU code paths even at world size 1")
     ap.add_argument("--no-graph", action="store_true",
                     help="time eager calls instead of a CUDA-graph replay of a reusable plan")
     args = ap.parse_args()
@@ -303,11 +305,16 @@ def main():
     from synth import clouds
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    # --force-dist: the N > 1 code paths (NCCL process group, loss all-reduce, row-sharded C5
+    # with every collective through NCCL) even at world 1 -- the one-GPU test of the data plane
+    dist_on = world > 1 or args.force_dist
+    if args.force_dist:
+        os.environ["APML_RS_COLLECTIVES"] = "1"
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if dist_on:
         dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.config]
     B, N, M = c["B"], c["N"], c["M"]
@@ -319,7 +326,7 @@ def main():
         B = B // world  # this rank's share of the fixed global batch
     # C5 on several GPUs: one cloud, pred rows sharded (X2 all-gather + X3 column-sum
     # all-reduces inside the call); every other config: batch sharding (weak scaling)
-    rowshard = args.config == "C5" and world > 1
+    rowshard = args.config == "C5" and dist_on
     if rowshard:
         x, y = clouds.batch(c["kind"], B, N, M, args.seed)
         r0, r1 = shard_rows(N, rank, world)
@@ -388,7 +395,7 @@ def main():
     def step():
         if use_graph:
             graph.replay()
-            if world > 1:
+            if dist_on:
                 sharded_reduce(loss_buf)  # X1: NCCL all-reduce of the loss (batch sharding)
             return _GraphStep()
         if rowshard:
@@ -397,7 +404,7 @@ def main():
             return ctx
         loss, ctx = forward(pred, gt, cfg, loss_out=loss_buf, n_sizes=ns, m_sizes=ms)
         ctx.backward(ones, out=grad_buf)
-        if world > 1:
+        if dist_on:
             sharded_reduce(loss)  # X1: NCCL all-reduce of the loss (batch sharding)
         return ctx
 
@@ -412,7 +419,7 @@ def main():
     prev.close()
     torch.cuda.synchronize()
     st0 = None
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.reset_peak_memory_stats(dev)
     sampler = ClockSampler(local, _pci_bus_id(dev))
@@ -442,7 +449,7 @@ def main():
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = float(sum(step_ms))
     peak_gb = (torch.cuda.max_memory_allocated(dev) - flush.numel()) / 1e9  # without the L2-flush buffer
-    if world > 1:
+    if dist_on:
         t = torch.tensor([tot_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
@@ -559,7 +566,7 @@ def main():
                 go.copy_(grad_buf, non_blocking=True)
                 torch.cuda.current_stream(dev).synchronize()
                 ctx.close()
-            if world > 1 and not rowshard:  # X1 on the step's result
+            if dist_on and not rowshard:  # X1 on the step's result
                 lred.copy_(lo, non_blocking=True)
                 sharded_reduce(lred)
                 lo.copy_(lred)
@@ -574,7 +581,7 @@ def main():
             e2e_step()
             e2e_list.append((time.perf_counter() - t0) * 1e3)
         e2e_ms = float(np.mean(e2e_list))
-        if world > 1:
+        if dist_on:
             t = torch.tensor([e2e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = float(t.item())
@@ -594,7 +601,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and ns is None:
         cpu = cpu_baseline(args.config, args.seed)
 
-    if world > 1:
+    if dist_on:
         dist.barrier()
     if rank == 0:
         out = {
@@ -607,7 +614,7 @@ def main():
                        "global_batch": pairs_per_step, "pairs_per_rank": B,
                        "parallelism": (f"row-shard x{world} (NCCL all-gather + per-iteration column-sum all-reduce)"
                                        if rowshard else f"batch-shard dp{world}" +
-                                       (" + NCCL loss all-reduce" if world > 1 else "")),
+                                       (" + NCCL loss all-reduce" if dist_on else "")),
                        "l2": "flushed between timed steps (256 MiB write outside the step bracket)",
                        "cuda_graph": bool(use_graph)},
             "roofline": roof, "roofline_distance_pass": roof_dist,
@@ -619,7 +626,7 @@ def main():
             "step_ms_p90": float(np.percentile(step_ms, 90)),
         }
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

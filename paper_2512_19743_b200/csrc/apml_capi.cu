@@ -756,6 +756,11 @@ bool use_grid_path(apml_ctx* c) {
   return !c->rep_smem;
 }
 
+// World 1 with nothing to reduce: the column sums are fused into the column steps.
+// APML_RS_COLLECTIVES=1 keeps the multi-rank sequence (every collective call through the
+// caller's apml_comm) at world 1 -- how the NCCL data plane is exercised on a one-GPU box.
+bool rs_fused(const apml_ctx* c) { return c->comm.world == 1 && env_long("APML_RS_COLLECTIVES", 0) == 0; }
+
 apml_status coll_sum(apml_ctx* c, float* buf, int64_t n) {
   if (c->comm.allreduce_sum_f32(buf, n, c->stream, c->comm.user) != 0)
     return fail(APML_ERR_CUDA, "allreduce_sum_f32 collective failed");
@@ -834,7 +839,7 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
   k_rs_astep<<<gr256, 256, 0, s>>>(a, 0);
   c->launches += 6;  // + the scan's own
   for (int l = 1; l <= L; ++l) {  // Eq. (3) column sums all-reduced (X3), Eq. (4) local
-    if (c->comm.world == 1) {  // nothing to all-reduce: column sum + column step fused
+    if (rs_fused(c)) {  // nothing to all-reduce: column sum + column step fused
       k_rs_colsum_bstep<<<gc256, 256, 0, s>>>(a, l);
       c->launches += 1;
     } else {
@@ -877,7 +882,7 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
       c->launches += 1;
     }
     for (int l = L; l >= 1; --l) {  // row step reverse of l - 1 runs inside rowrev2 of l
-      if (c->comm.world == 1) {
+      if (rs_fused(c)) {
         k_rs_colsum_colrev<<<gc256, 256, 0, s>>>(a, l);
         c->launches += 1;
       } else {
@@ -1171,7 +1176,7 @@ apml_status backward_on(apml_ctx* x, const float* grad_loss, float* grad_pred, f
           sparse_args(x, nullptr, grad_loss, grad_pred));
       x->launches += 1;
       CK(cudaGetLastError());
-      if (x->comm.world > 1 && (st = coll_sum(x, grad_gt, 3 * x->B * x->M)) != APML_OK) return st;
+      if (!rs_fused(x) && (st = coll_sum(x, grad_gt, 3 * x->B * x->M)) != APML_OK) return st;
     }
     mark(x, 8, s);
     x->backward_done = true;

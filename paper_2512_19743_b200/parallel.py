@@ -93,13 +93,15 @@ class Collectives:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.backend = dist.get_backend(group) if dist.is_initialized() else "none"
         self.errors = []
+        self.calls = 0  # collective invocations made on behalf of the library
         self._ar = A.ALLREDUCE_FN(self.allreduce)
         self._ag = A.ALLGATHER_FN(self.allgather)
         self.c = A.ApmlComm(self.rank, self.world, self._ar, self._ag, None)
 
     def allreduce(self, buf, n, stream, user) -> int:
-        try:
-            if self.world > 1:
+        self.calls += 1
+        try:  # (a world-1 NCCL group still runs the collective: the one-GPU test of the data plane)
+            if self.world > 1 or self.backend == "nccl":
                 dist.all_reduce(_view(buf, n, self.device), op=dist.ReduceOp.SUM, group=self.group)
             return 0
         except Exception as e:  # reported to the library as a non-zero status
@@ -107,13 +109,14 @@ class Collectives:
             return 1
 
     def allgather(self, send, recv, n, stream, user) -> int:
+        self.calls += 1
         try:
             s = _view(send, n, self.device)
             r = _view(recv, n * self.world, self.device)
-            if self.world == 1:
-                r.copy_(s)
-            elif self.backend == "nccl":
+            if self.backend == "nccl":
                 dist.all_gather_into_tensor(r, s, group=self.group)
+            elif self.world == 1:
+                r.copy_(s)
             else:
                 parts = [torch.empty(n, dtype=torch.float32) for _ in range(self.world)]
                 dist.all_gather(parts, s.cpu(), group=self.group)

@@ -1,0 +1,81 @@
+"""NCCL data plane on a one-GPU box (run by tests/test_gpu_nccl.py in its own process):
+a world-1 NCCL process group, APML_RS_COLLECTIVES=1 so the row-sharded mode issues every
+collective of its multi-rank sequence (column-statistics all-gather X2, per-iteration column-sum
+all-reduces X3, loss / grad_gt all-reduces) through parallel.Collectives -> NCCL on device
+buffers, and the batch-shard loss all-reduce X1.  Compared with the fp64 oracle and with the
+single-GPU path.  Prints one JSON line."""
+import json
+import os
+import socket
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+os.environ["APML_RS_COLLECTIVES"] = "1"
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from oracle import OracleConfig, SparsePlan  # noqa: E402
+from synth import clouds  # noqa: E402
+from tests.parity_util import normwise, well_conditioned  # noqa: E402
+
+
+def main():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1, device_id=dev)
+    from paper_2512_19743_b200 import Config, apml_loss
+    from paper_2512_19743_b200.parallel import Collectives, forward_rowsharded, sharded_reduce
+    out = {"backend": dist.get_backend()}
+    for grid in ("0", "1"):
+        os.environ["APML_CULL"] = grid  # plain and culled sweeps under the row-sharded sparse stage
+        B, N, M = 2, 700, 650
+        x, y = clouds.batch("shapenet", B, N, M, 90)
+        pred = torch.tensor(x, device=dev)
+        gt = torch.tensor(y, device=dev)
+        comm = Collectives(device=dev)
+        cfg = Config()
+        loss, ctx = forward_rowsharded(pred, gt, 0, N, cfg, comm)
+        g, gg = ctx.backward(torch.ones(B, device=dev), want_gt=True)
+        torch.cuda.synchronize()
+        assert not comm.errors, comm.errors
+        calls = comm.calls
+        oc = OracleConfig()
+        for b in range(B):
+            plan = SparsePlan(x[b], y[b], oc)
+            rel = abs(loss[b].item() - plan.loss) / plan.loss
+            assert rel <= 1e-5, f"loss rel {rel}"
+            gx, gy = plan.backward(1.0)
+            mask = well_conditioned(x[b], y[b], plan, oc)
+            e = normwise(g[b].double().cpu().numpy()[mask], gx[mask])
+            assert e <= 1e-4, f"grad {e}"
+            t = (g[b].double().sum(0) + gg[b].double().sum(0)).abs().max().item()
+            assert t <= 1e-5 * (g[b].abs().sum() + gg[b].abs().sum()).item()
+        out[f"rowshard_cull{grid}_calls"] = calls
+        assert calls >= 2 * cfg.l_iter, calls
+    # X1: batch-shard loss all-reduce through NCCL, straight-through gradient
+    x, y = clouds.batch("mmfi", 3, 512, 300, 91)
+    p1 = torch.tensor(x, device=dev, requires_grad=True)
+    p2 = torch.tensor(x, device=dev, requires_grad=True)
+    gt = torch.tensor(y, device=dev)
+    from paper_2512_19743_b200.apml import apml_loss as plain
+    a = plain(p1, gt, reduction="none")
+    l1 = sharded_reduce(a)
+    l2 = plain(p2, gt)
+    l1.backward()
+    l2.backward()
+    assert l1.item() == l2.item() and torch.equal(p1.grad, p2.grad)
+    out["batchshard"] = "ok"
+    dist.destroy_process_group()
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
