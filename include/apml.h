@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define APML_ABI_VERSION 2
+#define APML_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define APML_API __attribute__((visibility("default")))
@@ -151,12 +151,44 @@ typedef struct {
  *   allreduce_sum_f32: buf[0..n) <- sum over ranks of buf[0..n), in place, device memory.
  *   allgather_f32:     recv[r*n .. (r+1)*n) <- rank r's send[0..n), device memory (the
  *                      library also moves int32 bit patterns through it; no arithmetic). */
+typedef struct apml_nvls apml_nvls; /* opaque: an NVLink SHARP (NVLS) multicast team, below */
+
 typedef struct {
     int32_t rank, world;
     int (*allreduce_sum_f32)(float* buf, int64_t n, void* stream, void* user);
     int (*allgather_f32)(const float* send, float* recv, int64_t n, void* stream, void* user);
     void* user;
+    /* ABI 3.  Optional (NULL = unused):
+     *   allgather_bytes: HOST all-gather of n bytes per rank, recv[r*n ..) <- rank r's send;
+     *                    blocking; used only by apml_nvls_create to exchange handles.
+     *   nvls:            a team from apml_nvls_create; when set, every per-iteration Sinkhorn
+     *                    column sum (Eq. (3) forward and its reverse, X3) is reduced INSIDE the
+     *                    library's kernels through NVSwitch multicast memory (multimem
+     *                    ld_reduce) instead of the allreduce_sum_f32 callback. */
+    int (*allgather_bytes)(const void* send, void* recv, int64_t n, void* user);
+    apml_nvls* nvls;
 } apml_comm;
+
+/* NVLS team for the row-sharded mode (north_star "per-iteration column sums
+ * are allreduced over NVLink"): one multicast object of `bytes` bytes bound to a buffer on
+ * every rank's device (driver API: cuMulticastCreate / AddDevice / BindMem; rank 0 creates it
+ * and passes its POSIX file descriptor to the other ranks of the node over a Unix socket,
+ * SCM_RIGHTS; comm->allgather_bytes carries the rendezvous).  Each rank writes its partial
+ * column sums into its own copy; a kernel then reads the sum over all ranks with ONE
+ * multimem.ld_reduce per value, after a cross-GPU barrier made of a multicast red.add on a
+ * flag word in the same memory -- compute and collective in one stream-ordered pair of
+ * kernels, no NCCL call and no host involvement per iteration.  Collective over comm (every
+ * rank, same bytes); ranks must share one node.  bytes >= 8 * B * M + 256 for a problem of B
+ * pairs with M gt points.  Errors: APML_ERR_INVALID_ARG (no allgather_bytes for world > 1),
+ * APML_ERR_CUDA (no multicast support, driver failure); *out = NULL then. */
+APML_API apml_status apml_nvls_create(const apml_comm* comm, size_t bytes, apml_nvls** out);
+/* 1 when the team is a real multicast object; 0 for a one-device team that the driver would
+ * not build as one (a one-GPU box: cuMulticastCreate returns CUDA_ERROR_INVALID_VALUE for
+ * numDevices = 1), which then lives in plain device memory and runs the same kernels with
+ * ordinary atomics and loads (the sum over one rank; APML_NVLS_STRICT=1 makes it an error). */
+APML_API int apml_nvls_is_multicast(const apml_nvls* team);
+/* Collective: unmap and release (every rank). */
+APML_API void apml_nvls_destroy(apml_nvls* team);
 
 typedef struct apml_ctx apml_ctx; /* opaque: state saved by forward for backward */
 

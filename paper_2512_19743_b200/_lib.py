@@ -25,7 +25,8 @@ EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forw
            "apml_backward", "apml_backward_ex", "apml_plan_create", "apml_plan_forward",
            "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
            "apml_ctx_destroy",
-           "apml_loss_grad_host", "apml_plan_step_host", "apml_last_error")
+           "apml_loss_grad_host", "apml_plan_step_host", "apml_nvls_create", "apml_nvls_destroy", "apml_nvls_is_multicast",
+           "apml_last_error")
 
 
 class ApmlConfig(C.Structure):
@@ -45,11 +46,13 @@ class ApmlAllocator(C.Structure):
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+GATHER_BYTES_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 
 class ApmlComm(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("allreduce_sum_f32", ALLREDUCE_FN),
-                ("allgather_f32", ALLGATHER_FN), ("user", C.c_void_p)]
+                ("allgather_f32", ALLGATHER_FN), ("user", C.c_void_p),
+                ("allgather_bytes", GATHER_BYTES_FN), ("nvls", C.c_void_p)]
 
 
 class ApmlStats(C.Structure):
@@ -112,11 +115,17 @@ def lib() -> C.CDLL:
         L.apml_loss_grad_host.restype = C.c_int
         L.apml_loss_grad_host.argtypes = [vp, vp, i64, i64, i64, C.POINTER(ApmlConfig),
                                           C.POINTER(ApmlAllocator), vp, vp, vp]
+        L.apml_nvls_create.restype = C.c_int
+        L.apml_nvls_create.argtypes = [C.POINTER(ApmlComm), C.c_size_t, C.POINTER(vp)]
+        L.apml_nvls_is_multicast.restype = C.c_int
+        L.apml_nvls_is_multicast.argtypes = [vp]
+        L.apml_nvls_destroy.restype = None
+        L.apml_nvls_destroy.argtypes = [vp]
         L.apml_plan_step_host.restype = C.c_int
         L.apml_plan_step_host.argtypes = [vp, vp, vp, vp, vp, vp]
         L.apml_last_error.restype = C.c_char_p
         L.apml_last_error.argtypes = []
-        if L.apml_abi_version() != 2:
+        if L.apml_abi_version() != 3:
             raise ImportError("libapml.so ABI version mismatch")
         _lib = L
     return _lib

@@ -22,6 +22,7 @@
 #include "k_dist.cuh"
 #include "k_mega.cuh"
 #include "k_rowshard.cuh"
+#include "nvls_host.cuh"
 
 using namespace apml;
 
@@ -818,6 +819,38 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
   return APML_OK;
 }
 
+// One X3 reduction through the NVLS team (k_nvls.cuh): this rank's column sums of w into its
+// copy of the team buffer, every CTA of every rank counted on the flag, then the column step
+// (kind 0: Eq. (3) forward, 1: its reverse) on the sums over the ranks read by multimem.
+apml_status nvls_colsum_step(apml_ctx* c, const float* w, size_t w_stride, int kind, int l) {
+  apml_nvls* t = c->comm.nvls;
+  const int B = (int)c->B, M = (int)c->M;
+  const size_t need = kNvlsHdr + 2 * sizeof(float) * (size_t)B * M;
+  if (t->size < need) return fail(APML_ERR_INVALID_ARG, "NVLS team buffer smaller than 8 B M + 256 bytes");
+  cudaStream_t s = c->stream;
+  const SparseArgs a = sparse_args(c, nullptr, nullptr, nullptr);
+  const size_t off = kNvlsHdr + (size_t)t->use * sizeof(float) * (size_t)B * M;
+  t->use ^= 1;
+  float* part_uc = reinterpret_cast<float*>(t->uc + off);
+  const float* part_mc = reinterpret_cast<const float*>(t->mcva + off);
+  unsigned* flag_uc = reinterpret_cast<unsigned*>(t->uc);
+  unsigned* flag_mc = reinterpret_cast<unsigned*>(t->mcva);
+  const dim3 gc((M + 255) / 256, B);
+  t->sig += (uint32_t)t->world * gc.x * gc.y;  // every CTA of every rank bumps every flag once
+  if (t->multicast) {
+    k_rs_colsum_nvls<true><<<gc, 256, 0, s>>>(a, w, w_stride, part_uc, flag_mc);
+    if (kind == 0) k_rs_bstep_nvls<true><<<gc, 256, 0, s>>>(a, l, part_mc, flag_uc, t->sig);
+    else k_rs_bwd_colrev_nvls<true><<<gc, 256, 0, s>>>(a, l, part_mc, flag_uc, t->sig);
+  } else {
+    k_rs_colsum_nvls<false><<<gc, 256, 0, s>>>(a, w, w_stride, part_uc, flag_mc);
+    if (kind == 0) k_rs_bstep_nvls<false><<<gc, 256, 0, s>>>(a, l, part_mc, flag_uc, t->sig);
+    else k_rs_bwd_colrev_nvls<false><<<gc, 256, 0, s>>>(a, l, part_mc, flag_uc, t->sig);
+  }
+  c->launches += 2;
+  CK(cudaGetLastError());
+  return APML_OK;
+}
+
 // S4-S7 over this rank's entries; column sums all-reduced.
 apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, L = c->cfg.l_iter;
@@ -842,6 +875,8 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
     if (rs_fused(c)) {  // nothing to all-reduce: column sum + column step fused
       k_rs_colsum_bstep<<<gc256, 256, 0, s>>>(a, l);
       c->launches += 1;
+    } else if (c->comm.nvls) {  // X3 inside the kernels over NVSwitch multicast memory
+      if ((st = nvls_colsum_step(c, c->gvec, 2 * (size_t)(N + M), 0, l)) != APML_OK) return st;
     } else {
       k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
       CK(cudaGetLastError());
@@ -885,6 +920,8 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
       if (rs_fused(c)) {
         k_rs_colsum_colrev<<<gc256, 256, 0, s>>>(a, l);
         c->launches += 1;
+      } else if (c->comm.nvls) {
+        if ((st = nvls_colsum_step(c, c->gvec + N + M, 2 * (size_t)(N + M), 1, l)) != APML_OK) return st;
       } else {
         k_rs_colsum<<<gc256, 256, 0, s>>>(a, c->gvec + N + M, 2 * (size_t)(N + M), c->qbuf, (size_t)M);
         CK(cudaGetLastError());
@@ -946,6 +983,152 @@ apml_status backward_on(apml_ctx* x, const float* grad_loss, float* grad_pred, f
 extern "C" {
 
 int apml_abi_version(void) { return APML_ABI_VERSION; }
+
+apml_status apml_nvls_create(const apml_comm* comm, size_t bytes, apml_nvls** out) {
+  if (!out) return fail(APML_ERR_INVALID_ARG, "out must be non-NULL");
+  *out = nullptr;
+  if (!comm || comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world || bytes == 0)
+    return fail(APML_ERR_INVALID_ARG, "comm needs rank < world; bytes > 0");
+  if (comm->world > 1 && !comm->allgather_bytes)
+    return fail(APML_ERR_INVALID_ARG, "world > 1 needs comm->allgather_bytes for the handle exchange");
+  const NvlsDrv& d = nvls_drv();
+  if (!d.ok) return fail(APML_ERR_CUDA, "driver multicast entry points unavailable");
+  apml_nvls* t = new apml_nvls();
+  t->rank = comm->rank;
+  t->world = comm->world;
+  t->comm = *comm;
+  t->comm.nvls = nullptr;
+  auto bail = [&](const std::string& m) {
+    nvls_release(t);
+    delete t;
+    return fail(APML_ERR_CUDA, "NVLS: " + m);
+  };
+  int devi = 0;
+  if (cudaGetDevice(&devi) != cudaSuccess || d.deviceGet(&t->dev, devi) != CUDA_SUCCESS) return bail("device");
+  int mc_sup = 0;
+  d.deviceGetAttribute(&mc_sup, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, t->dev);
+  if (!mc_sup) return bail("the device has no multicast support");
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)t->world;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t gran = 0;
+  if (d.mcGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !gran) return bail("granularity");
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = devi;
+  size_t agran = 0;
+  if (d.memGetGranularity(&agran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS) return bail("granularity");
+  const size_t g = std::max(gran, agran);
+  t->size = (bytes + g - 1) / g * g;
+  mp.size = t->size;
+  // rendezvous id from rank 0 (names of the ranks' abstract sockets)
+  uint64_t id = 0;
+  if (t->rank == 0) {
+    const int fd = open("/dev/urandom", O_RDONLY);
+    if (fd >= 0) { if (read(fd, &id, sizeof id) != (ssize_t)sizeof id) id = 0; close(fd); }
+    id ^= (uint64_t)getpid() << 20;
+  }
+  int listener = -1;
+  if (t->world > 1) {
+    std::vector<uint64_t> ids((size_t)t->world);
+    if (comm->allgather_bytes(&id, ids.data(), sizeof id, comm->user) != 0) return bail("rendezvous");
+    id = ids[0];
+    if (t->rank > 0) {
+      listener = socket(AF_UNIX, SOCK_STREAM, 0);
+      sockaddr_un a;
+      const socklen_t al = nvls_addr(nvls_sock_name(id, t->rank), &a);
+      if (listener < 0 || bind(listener, (sockaddr*)&a, al) != 0 || listen(listener, 1) != 0) {
+        if (listener >= 0) close(listener);
+        return bail("socket");
+      }
+    }
+    if (!nvls_barrier(t->comm)) { if (listener >= 0) close(listener); return bail("barrier"); }
+  }
+  if (t->rank == 0) {
+    // handle types: an fd to hand to the other ranks; at world 1 nothing is shared and
+    // some drivers accept only another type there (measured: POSIX fd and NONE rejected with
+    // CUDA_ERROR_INVALID_VALUE on a one-GPU box), so the alternatives are tried in turn
+    const CUmemAllocationHandleType types[3] = {CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_FABRIC,
+                                                CU_MEM_HANDLE_TYPE_NONE};
+    CUresult r = CUDA_ERROR_INVALID_VALUE;
+    std::string tried;
+    for (int k = 0; k < (t->world == 1 ? 3 : 1) && r != CUDA_SUCCESS; ++k) {
+      mp.handleTypes = types[k];
+      r = d.mcCreate(&t->mc, &mp);
+      tried += " " + std::to_string((int)types[k]) + ":" + std::to_string((int)r);
+    }
+    if (r != CUDA_SUCCESS && t->world == 1 && env_long("APML_NVLS_STRICT", 0) == 0) {
+      // a one-device team the driver will not build as a multicast object (one-GPU box):
+      // plain device memory, the same kernels with ordinary atomics / loads (k_nvls.cuh kMc)
+      t->multicast = false;
+      void* p = nullptr;
+      if (cudaMalloc(&p, t->size) != cudaSuccess) return bail("allocation");
+      t->uc = t->mcva = reinterpret_cast<CUdeviceptr>(p);
+      if (cudaMemset(p, 0, t->size) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return bail("zero");
+      *out = t;
+      return APML_OK;
+    }
+    if (r != CUDA_SUCCESS)
+      return bail("cuMulticastCreate (handle type:error)" + tried + " size " + std::to_string(t->size) + " gran " +
+                  std::to_string(gran) + "/" + std::to_string(agran) + " numDevices " + std::to_string(mp.numDevices));
+    t->mc_ok = true;
+    if (t->world > 1) {
+      int fd = -1;
+      if (d.exportHandle(&fd, t->mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS) return bail("export");
+      bool ok = true;
+      for (int r = 1; r < t->world; ++r) ok = nvls_send_fd(nvls_sock_name(id, r), fd) && ok;
+      close(fd);
+      if (!ok) return bail("fd hand-over");
+    }
+  } else {
+    const int fd = nvls_recv_fd(listener);
+    close(listener);
+    if (fd < 0) return bail("fd hand-over");
+    const CUresult r = d.importHandle(&t->mc, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+    close(fd);
+    if (r != CUDA_SUCCESS) return bail("import");
+    t->mc_ok = true;
+  }
+  {
+    const CUresult r = d.mcAddDevice(t->mc, t->dev);
+    if (r != CUDA_SUCCESS) return bail("cuMulticastAddDevice error " + std::to_string((int)r));
+  }
+  if (!nvls_barrier(t->comm)) return bail("barrier");  // every device added before any binding
+  if (d.memCreate(&t->mem, t->size, &ap, 0) != CUDA_SUCCESS) return bail("cuMemCreate");
+  t->mem_ok = true;
+  {
+    const CUresult r = d.mcBindMem(t->mc, 0, t->mem, 0, t->size, 0);
+    if (r != CUDA_SUCCESS) return bail("cuMulticastBindMem error " + std::to_string((int)r));
+  }
+  t->bound = true;
+  CUmemAccessDesc acc{};
+  acc.location = ap.location;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.addrReserve(&t->uc, t->size, g, 0, 0) != CUDA_SUCCESS) return bail("reserve");
+  if (d.memMap(t->uc, t->size, 0, t->mem, 0) != CUDA_SUCCESS) return bail("map");
+  t->uc_mapped = true;
+  if (d.memSetAccess(t->uc, t->size, &acc, 1) != CUDA_SUCCESS) return bail("access");
+  if (d.addrReserve(&t->mcva, t->size, g, 0, 0) != CUDA_SUCCESS) return bail("reserve");
+  if (d.memMap(t->mcva, t->size, 0, t->mc, 0) != CUDA_SUCCESS) return bail("map multicast");
+  t->mc_mapped = true;
+  if (d.memSetAccess(t->mcva, t->size, &acc, 1) != CUDA_SUCCESS) return bail("access");
+  if (cudaMemset(reinterpret_cast<void*>(t->uc), 0, t->size) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return bail("zero");
+  if (!nvls_barrier(t->comm)) return bail("barrier");
+  *out = t;
+  return APML_OK;
+}
+
+int apml_nvls_is_multicast(const apml_nvls* t) { return t && t->multicast ? 1 : 0; }
+
+void apml_nvls_destroy(apml_nvls* t) {
+  if (!t) return;
+  cudaDeviceSynchronize();
+  nvls_barrier(t->comm);
+  nvls_release(t);
+  delete t;
+}
 
 void apml_config_default(apml_config* c) {
   if (!c) return;

@@ -9,6 +9,7 @@
 // L_iter column sums P0^T Rbar^l, column softmax reverse sums.  Every kernel is grid-wide
 // (no cluster), reusing the per-line device functions of k_mega.cuh.
 #pragma once
+#include "k_nvls.cuh"
 #include "k_mega.cuh"
 
 namespace apml {
@@ -599,6 +600,43 @@ __global__ void __launch_bounds__(256) k_rs_colsum_colrev(const SparseArgs A, in
 __global__ void k_rs_bwd_colrev(const SparseArgs A, int l, const float* __restrict__ t) {
   const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j < A.M) grp_colrev(A, b, j, l, t[(size_t)b * A.M + j]);
+}
+
+// ---- NVLS variants of the X3 reductions (k_nvls.cuh): the producer writes this rank's
+// column sums into its copy of the team buffer and every CTA bumps every rank's flag once (no
+// early return: the consumer counts all CTAs of all ranks); the consumer waits for the count
+// and reads each sum over the ranks with one multimem.ld_reduce.
+template <bool kMc>
+__global__ void __launch_bounds__(256) k_rs_colsum_nvls(const SparseArgs A, const float* __restrict__ w,
+                                                        size_t w_stride, float* __restrict__ part,
+                                                        unsigned* flag_mc) {
+  __shared__ GrpSmem S;
+  const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * kWWarps + wid) * 32 + lane;
+  if (A.cursor[b] <= A.cap && j - lane < A.M) {  // warp-uniform
+    const float t = grp_colsum(A, b, j, w + (size_t)b * w_stride, S.x[wid], S.y[wid]);
+    if (j < A.M) part[(size_t)b * A.M + j] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) nvls_signal<kMc>(flag_mc);
+}
+// Eq. (3) column step on the sums over the ranks
+template <bool kMc>
+__global__ void k_rs_bstep_nvls(const SparseArgs A, int l, const float* part_mc, const unsigned* flag_uc,
+                                unsigned target) {
+  if (threadIdx.x == 0) nvls_wait(flag_uc, target);
+  __syncthreads();
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < A.M) grp_bstep(A, b, j, l, nvls_ld_sum<kMc>(part_mc + (size_t)b * A.M + j));
+}
+// Reverse column step on t = P0^T Rbar^l summed over the ranks
+template <bool kMc>
+__global__ void k_rs_bwd_colrev_nvls(const SparseArgs A, int l, const float* part_mc, const unsigned* flag_uc,
+                                     unsigned target) {
+  if (threadIdx.x == 0) nvls_wait(flag_uc, target);
+  __syncthreads();
+  const int b = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < A.M) grp_colrev(A, b, j, l, nvls_ld_sum<kMc>(part_mc + (size_t)b * A.M + j));
 }
 
 __global__ void __launch_bounds__(256) k_rs_bwd_rowrev2(const SparseArgs A, int l) {

@@ -83,9 +83,13 @@ def _view(ptr: int, n: int, device) -> torch.Tensor:
 
 class Collectives:
     """The apml_comm callbacks over a torch.distributed group (NCCL for CUDA tensors; with
-    gloo the all-gather goes through host memory because gloo gathers CPU tensors only)."""
+    gloo the all-gather goes through host memory because gloo gathers CPU tensors only).
 
-    def __init__(self, group=None, device="cuda"):
+    nvls_bytes > 0: also an NVLS team (apml_nvls_create, collective): the per-iteration
+    Sinkhorn column sums are then reduced inside the library's kernels over NVSwitch multicast
+    memory (no callback per iteration); needs 8 B M + 256 bytes for B pairs of M gt points."""
+
+    def __init__(self, group=None, device="cuda", nvls_bytes: int = 0):
         from . import _lib as A
         self.group = group
         self.device = torch.device(device)
@@ -96,7 +100,39 @@ class Collectives:
         self.calls = 0  # collective invocations made on behalf of the library
         self._ar = A.ALLREDUCE_FN(self.allreduce)
         self._ag = A.ALLGATHER_FN(self.allgather)
-        self.c = A.ApmlComm(self.rank, self.world, self._ar, self._ag, None)
+        self._gb = A.GATHER_BYTES_FN(self.allgather_bytes)
+        self.c = A.ApmlComm(self.rank, self.world, self._ar, self._ag, None, self._gb, None)
+        self.nvls = None
+        if nvls_bytes > 0:
+            h = C.c_void_p()
+            with torch.cuda.device(self.device):
+                A.check(A.lib().apml_nvls_create(C.byref(self.c), int(nvls_bytes), C.byref(h)))
+            self.nvls = h.value
+            self.c.nvls = h.value
+            self.nvls_multicast = bool(A.lib().apml_nvls_is_multicast(h.value))
+
+    def allgather_bytes(self, send, recv, n, user) -> int:
+        """Host all-gather of n bytes per rank (the NVLS handle rendezvous)."""
+        try:
+            mine = C.string_at(send, n)
+            if self.world == 1:
+                parts = [mine]
+            else:
+                parts = [None] * self.world
+                dist.all_gather_object(parts, mine, group=self.group)
+            C.memmove(recv, b"".join(parts), n * self.world)
+            return 0
+        except Exception as e:
+            self.errors.append(repr(e))
+            return 1
+
+    def close(self):
+        """Release the NVLS team (collective)."""
+        if self.nvls:
+            from . import _lib as A
+            A.lib().apml_nvls_destroy(self.nvls)
+            self.nvls = None
+            self.c.nvls = None
 
     def allreduce(self, buf, n, stream, user) -> int:
         self.calls += 1

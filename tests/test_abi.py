@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_defaults():
     L = A.lib()
-    assert L.apml_abi_version() == 2
+    assert L.apml_abi_version() == 3
     c = A.ApmlConfig()
     L.apml_config_default(C.byref(c))
     assert c.p_min == pytest.approx(0.9) and c.tau == pytest.approx(1e-8)      # R2

@@ -36,6 +36,11 @@ def test_nccl_world1_collectives_match_oracle():
     out = json.loads(r.stdout.strip().splitlines()[-1])
     assert out["backend"] == "nccl" and out["batchshard"] == "ok"
     assert out["rowshard_cull0_calls"] >= 20 and out["rowshard_cull1_calls"] >= 20
+    # the NVLS team ran (a multicast object where the driver builds one for a
+    # one-device team, else the plain-memory team with the same kernels) and matched bitwise
+    assert out["nvls"] == "ok", out["nvls"]
+    print("NVLS multicast object:", out["nvls_multicast"], "host collective calls (NVLS, callbacks):",
+          out["nvls_calls"])
 
 
 @pytest.mark.parametrize("config", ["C2", "C5"])
