@@ -331,7 +331,15 @@ def main():
         x, y = clouds.batch(c["kind"], B, N, M, args.seed)
         r0, r1 = shard_rows(N, rank, world)
         x = np.ascontiguousarray(x[:, r0:r1])
-        comm = Collectives(device=dev)
+        # X3 (the per-iteration column sums) over an NVLS team when the box builds one (in-kernel
+        # multimem reduction), else through the NCCL callbacks
+        x3 = "nccl all-reduce callbacks"
+        try:
+            comm = Collectives(device=dev, nvls_bytes=8 * B * M + 256)
+            x3 = "in-kernel NVLS " + ("multicast" if comm.nvls_multicast else "team in plain memory (one device)")
+        except Exception as e:
+            comm = Collectives(device=dev)
+            x3 += f" (NVLS unavailable: {str(e)[:80]})"
     else:
         x, y = clouds.batch(c["kind"], B, N, M, args.seed + 1000 * rank) if "ragged" not in c else (None, None)
     ns = ms = None
@@ -612,6 +620,7 @@ def main():
                        **({} if ns is None else {"ragged_mean_N": float(np.mean(ns)), "ragged_mean_M": float(np.mean(ms))}),
                        "l_iter": cfg.l_iter, "p_min": cfg.p_min, "grad_mode": args.grad_mode,
                        "global_batch": pairs_per_step, "pairs_per_rank": B,
+                       **({"x3_column_sums": x3} if rowshard else {}),
                        "parallelism": (f"row-shard x{world} (NCCL all-gather + per-iteration column-sum all-reduce)"
                                        if rowshard else f"batch-shard dp{world}" +
                                        (" + NCCL loss all-reduce" if dist_on else "")),
