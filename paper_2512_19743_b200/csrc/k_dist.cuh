@@ -73,6 +73,46 @@ __global__ void k_stage(const float* __restrict__ pts, int n, int np, float sent
   s[k] = x; s[np + k] = y; s[2 * np + k] = z;
 }
 
+// ---- TMA (bulk-copy engine) staging of the streamed tiles: one elected thread issues three
+// 1-D cp.async.bulk copies (x, y, z: 3 x kTQ floats, contiguous in the SoA staging, 512-byte
+// aligned) per tile into a 2-deep shared-memory ring, each completing on the ring slot's
+// mbarrier (expect-tx); the tile after next is issued as soon as every warp has left a slot,
+// so the copy of tile t+1 overlaps the distance work of tile t (north_star (1): "stages gt /
+// pred tiles in shared memory via TMA bulk copies").
+struct TileRing {
+  float v[2][3][kTQ];
+  unsigned long long bar[2];
+};
+__device__ __forceinline__ uint32_t sptr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ring_init(TileRing& r) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sptr(&r.bar[k])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+// (one thread) tile at streamed index j0 into slot k
+__device__ __forceinline__ void ring_issue(TileRing& r, int k, const float* __restrict__ str, int str_np, int j0) {
+  const uint32_t bar = sptr(&r.bar[k]);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(3u * kTQ * 4u) : "memory");
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sptr(&r.v[k][c][0])),
+                 "l"(str + (size_t)c * str_np + j0), "r"(kTQ * 4u), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void ring_wait(TileRing& r, int k, uint32_t parity) {
+  const uint32_t bar = sptr(&r.bar[k]);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+}
+
 // Load one kTQ-point tile of the streamed cloud (SoA) into shared memory.
 __device__ __forceinline__ void load_tile(const float* __restrict__ str, int str_np, int j0,
                                           float* sx, float* sy, float* sz) {
@@ -97,7 +137,13 @@ __device__ __forceinline__ void top2_block(const float* __restrict__ own_soa, in
   const float* own = own_soa + (size_t)b * 3 * own_np;
   const float* str = str_soa + (size_t)b * 3 * str_np;
   const int base = bx * kSweepThreads * R + threadIdx.x;
-  __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ];
+  __shared__ __align__(128) TileRing ring;
+  const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
+  ring_init(ring);
+  if (threadIdx.x == 0) {
+    if (j0 < j1) ring_issue(ring, 0, str, str_np, j0);
+    if (j0 + kTQ < j1) ring_issue(ring, 1, str, str_np, j0 + kTQ);
+  }
 
   f2_t nx[R], ny[R], nz[R];
   // two independent running (min, second) per owned point (streamed points 0,1 / 2,3 of each
@@ -111,14 +157,13 @@ __device__ __forceinline__ void top2_block(const float* __restrict__ own_soa, in
     m[r] = __int_as_float(0x7f800000); s[r] = m[r];
     m2[r] = m[r]; s2[r] = m[r];
   }
-  const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
-  for (int jt = j0; jt < j1; jt += kTQ) {
-    __syncthreads();
-    load_tile(str, str_np, jt, sx, sy, sz);
-    __syncthreads();
-    const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
-    const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
-    const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
+  int t = 0;
+  for (int jt = j0; jt < j1; jt += kTQ, ++t) {
+    const int k = t & 1;
+    ring_wait(ring, k, (uint32_t)(t >> 1) & 1u);
+    const ulonglong2* px = reinterpret_cast<const ulonglong2*>(ring.v[k][0]);
+    const ulonglong2* py = reinterpret_cast<const ulonglong2*>(ring.v[k][1]);
+    const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(ring.v[k][2]);
 #pragma unroll 4
     for (int q = 0; q < kTQ / 4; ++q) {
       const ulonglong2 qx = px[q], qy = py[q], qz = pz[q];
@@ -132,6 +177,10 @@ __device__ __forceinline__ void top2_block(const float* __restrict__ own_soa, in
         top2_pair(m[r], s[r], d0, d1);
         top2_pair(m2[r], s2[r], d2, d3);
       }
+    }
+    if (jt + 2 * kTQ < j1) {  // slot k is refilled with the tile after next once every warp left it
+      __syncthreads();
+      if (threadIdx.x == 0) ring_issue(ring, k, str, str_np, jt + 2 * kTQ);
     }
   }
   float2* out = part + ((size_t)split * B + b) * own_np;
@@ -324,7 +373,8 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
   const float* str = gt_soa + (size_t)b * 3 * mp;
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __shared__ __align__(16) float sx[kTQ], sy[kTQ], sz[kTQ], sR[kTQ], sE[kTQ];
+  __shared__ __align__(128) TileRing ring;  // streamed coordinates (TMA bulk copies)
+  __shared__ __align__(16) float sR[kTQ], sE[kTQ];
   __shared__ uint2 queue_all[kSweepThreads / 32][kLaneQ][32];  // [warp][slot][lane]: conflict-free
   uint2* q = &queue_all[w][0][lane];
   int qn = 0;  // this lane's queued entries
@@ -344,9 +394,19 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
     }
   }
   const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
-  for (int jt = j0; jt < j1; jt += kTQ) {
-    __syncthreads();
-    load_tile(str, mp, jt, sx, sy, sz);
+  ring_init(ring);
+  if (threadIdx.x == 0) {
+    if (j0 < j1) ring_issue(ring, 0, str, mp, j0);
+    if (j0 + kTQ < j1) ring_issue(ring, 1, str, mp, j0 + kTQ);
+  }
+  int tix = 0;
+  for (int jt = j0; jt < j1; jt += kTQ, ++tix) {
+    const int slot = tix & 1;
+    __syncthreads();  // every warp left the previous tile: its slot takes the tile after this one
+    if (tix > 0 && threadIdx.x == 0 && jt + kTQ < j1) ring_issue(ring, slot ^ 1, str, mp, jt + kTQ);
+    const float* sx = ring.v[slot][0];
+    const float* sy = ring.v[slot][1];
+    const float* sz = ring.v[slot][2];
     for (int t = threadIdx.x; t < kTQ; t += kSweepThreads) {
       const int j = jt + t;
       if (j < M) {
@@ -357,6 +417,7 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
       }
     }
     __syncthreads();
+    ring_wait(ring, slot, (uint32_t)(tix >> 1) & 1u);
     const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
     const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
     const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
