@@ -23,6 +23,7 @@
 #include "k_mega.cuh"
 #include "k_rowshard.cuh"
 #include "nvls_host.cuh"
+#include <nvtx3/nvToolsExt.h>
 
 using namespace apml;
 
@@ -150,6 +151,13 @@ struct apml_ctx {
 };
 
 namespace {
+
+// NVTX ranges (domain-less, host-side; visible to Nsight Systems / ncu --nvtx): one per stage
+// of the hot path, named after SURVEY 8(a)'s rows.  No cost without an attached tool.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 // Stage events.  Under CUDA-graph capture they become event-record nodes (External flag), so
 // every replay re-records them and apml_ctx_stage_times reads the last replay.
@@ -596,6 +604,7 @@ void launch_scan(apml_ctx* c, const ScanJob& j0, const ScanJob& j1) {
 // Culled sweeps: Morton-order both clouds, then Pass A over the sorted clouds
 // with tile culling.  Leaves part_r [B][N] and part_c [B][M] (original indices, S = 1).
 apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
+  const Nvtx nvtx_("apml S0-S1 culled Pass A");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   const int bits = c->cell_bits;
@@ -652,6 +661,7 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
 }
 
 apml_status launch_emit_cull(apml_ctx* c) {
+  const Nvtx nvtx_("apml S3 culled emit");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
@@ -672,6 +682,7 @@ apml_status launch_emit_cull(apml_ctx* c) {
 }
 
 apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
+  const Nvtx nvtx_("apml S0-S3 distance sweeps");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   mark(c, 0, s);
@@ -725,6 +736,7 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
 }
 
 apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
+  const Nvtx nvtx_("apml S4-S7 sparse forward");
   const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
   apml_status st = c->fwd2    ? launch_cluster(c, k_sparse_fwd2, a, c->stream, "fwd2", 9)
                    : c->idx16 ? launch_cluster(c, k_sparse_fwd<uint16_t>, a, c->stream, "fwd", 13)
@@ -775,6 +787,7 @@ apml_status coll_gather(apml_ctx* c, const float* send, float* recv, int64_t n) 
 
 // S0-S3 with rows local and the column statistics merged over ranks (X2).
 apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
+  const Nvtx nvtx_("apml S0-S3 sweeps (row-sharded)");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
   mark(c, 0, s);
@@ -853,6 +866,7 @@ apml_status nvls_colsum_step(apml_ctx* c, const float* w, size_t w_stride, int k
 
 // S4-S7 over this rank's entries; column sums all-reduced.
 apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
+  const Nvtx nvtx_("apml S4-S7 sparse forward (grid)");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, L = c->cfg.l_iter;
   cudaStream_t s = c->stream;
   const SparseArgs a = sparse_args(c, loss, nullptr, nullptr);
@@ -901,6 +915,7 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
 }
 
 apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_pred, cudaStream_t s) {
+  const Nvtx nvtx_("apml S8 backward (grid)");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, L = c->cfg.l_iter;
   const SparseArgs a = sparse_args(c, nullptr, grad_loss, grad_pred);
   const dim3 gr((N + kRsThreads - 1) / kRsThreads, B), gc256((M + 255) / 256, B), gr256((N + 255) / 256, B);
@@ -1349,6 +1364,7 @@ apml_status apml_backward_ex(apml_ctx* x, const float* grad_loss, float* grad_pr
 
 namespace {
 apml_status backward_on(apml_ctx* x, const float* grad_loss, float* grad_pred, float* grad_gt, cudaStream_t s) {
+  const Nvtx nvtx_("apml S8 backward");
   mark(x, 7, s);
   x->bwd_timed = x->timing;
   if (x->rs) {
