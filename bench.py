@@ -371,22 +371,62 @@ def main():
     use_graph = not args.no_graph and not rowshard and ns is None
     graph = plan = None
     launches_per_step = 0
-    if use_graph:
-        plan = Plan(B, pred.shape[1], M, cfg, device=dev)
+    pre = None  # the instrumented pre-pass (graph mode)
+
+    def make_graph(cfg_g):
+        p_ = Plan(B, pred.shape[1], M, cfg_g, device=dev)
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
+        nl = 0
         with torch.cuda.stream(side):
             for _ in range(2):
-                l0 = plan.stats()["launches"]
-                plan.forward(pred, gt, loss_buf)
-                plan.backward(ones, out=grad_buf)
-                launches_per_step = plan.stats()["launches"] - l0
+                l0 = p_.stats()["launches"]
+                p_.forward(pred, gt, loss_buf)
+                p_.backward(ones, out=grad_buf)
+                nl = p_.stats()["launches"] - l0
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            plan.forward(pred, gt, loss_buf)
-            plan.backward(ones, out=grad_buf)
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_):
+            p_.forward(pred, gt, loss_buf)
+            p_.backward(ones, out=grad_buf)
+        return p_, g_, nl
+
+    if use_graph:
+        # Every stage mark inside a graph is an event-record node costing a few us of launch
+        # pipelining (all nine: ~40 us on a 306 us C2 step).  So: (1) an instrumented pre-pass
+        # (all marks) gives the stage breakdown and picks the dominant kernel; (2) the same step
+        # without marks is timed for reference; (3) the TIMED graph carries only the two marks
+        # around the dominant kernel, whose live duration the roofline uses.
+        STAGE_MARKS = {"staging": (0, 1), "passA_rows": (1, 3), "line_info": (3, 4), "emit": (4, 5),
+                       "sparse_fwd": (5, 6), "sparse_bwd": (7, 8)}
+        p_i, g_i, _ = make_graph(cfg)
+        pre_st = []
+        for k in range(max(5, args.warmup)):
+            flush.fill_(k & 0xFF)
+            g_i.replay()
+            pre_st.append(p_i.stage_times())
+        pre_med = {k: float(np.median([st[k] for st in pre_st])) for k in pre_st[0]}
+        dom_pre = max(STAGE_MARKS, key=lambda k: pre_med.get(k, 0.0))
+        p_i.close()
+        del g_i
+        p_u, g_u, _ = make_graph(Config(grad_mode=args.grad_mode, sync_check=False))
+        e_u = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+        for k in range(13):
+            flush.fill_(k & 0xFF)
+            if k >= 3:
+                e_u[k - 3][0].record()
+            g_u.replay()
+            if k >= 3:
+                e_u[k - 3][1].record()
+        torch.cuda.synchronize()
+        pre = {"stages_ms": pre_med, "dominant": dom_pre,
+               "uninstrumented_ms_per_step": float(np.median([a.elapsed_time(b) for a, b in e_u]))}
+        p_u.close()
+        del g_u
+        a_, b_ = STAGE_MARKS[dom_pre]
+        cfg = Config(grad_mode=args.grad_mode, sync_check=False, stage_timing=True, stage_marks=(1 << a_) | (1 << b_))
+        plan, graph, launches_per_step = make_graph(cfg)
 
     class _GraphStep:  # the per-step handle the timing loop reads (stage times, stats)
         def stage_times(self):
@@ -448,6 +488,9 @@ def main():
             stages.append(prev.stage_times()); launches += prev.stats()["launches"]; prev.close()
         prev = ctx
     if use_graph:
+        # (the replays run on the current stream, the plan's own stream is the capture stream:
+        # order the counter read after the last replay)
+        torch.cuda.synchronize()
         st0 = _GraphStep().stats()
     else:
         stages.append(prev.stage_times()); st0 = prev.stats(); launches += st0["launches"]; prev.close()
@@ -465,9 +508,14 @@ def main():
     pairs_per_step = B if rowshard else B * world  # = B_global under strong scaling
     value = pairs_per_step / (ms_per_step / 1e3)
 
-    # per-stage medians and the roofline of the dominant kernel
+    # per-stage medians and the roofline of the dominant kernel (graph mode: the dominant
+    # kernel live from the timed region, the other stages from the instrumented pre-pass)
     keys = list(stages[0].keys())
     med = {k: float(np.median([s[k] for s in stages])) for k in keys}
+    if pre is not None:
+        live = med[pre["dominant"]]
+        med = dict(pre["stages_ms"])
+        med[pre["dominant"]] = live
     peaks = _peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
@@ -628,6 +676,11 @@ def main():
                        "cuda_graph": bool(use_graph)},
             "roofline": roof, "roofline_distance_pass": roof_dist,
             "stages_ms": med, "nnz_per_pair": nnz / B, "peak_gb": peak_gb,
+            **({} if pre is None else {
+                "stages_note": (f"{pre['dominant']} timed live over the timed region (two event marks "
+                                "in the graph); the other stages from an instrumented pre-pass with all "
+                                "nine marks (each costs a few us of launch pipelining)"),
+                "ms_per_step_uninstrumented": pre["uninstrumented_ms_per_step"]}),
             "dense_lower_bound_gb": 8 * B * N * M / 1e9,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "gpu_launches": launches,
             "wall_s_timed": t_wall, "step_ms_min": min(step_ms), "step_ms_max": max(step_ms),

@@ -80,6 +80,15 @@ typedef enum {
 #define APML_FLAG_CHECK_FINITE 2u /* scan the inputs for NaN/Inf first (one extra pass + sync) */
 #define APML_FLAG_STAGE_TIMING 4u /* record CUDA events between the stages below (on the launch
                                      stream); read them with apml_ctx_stage_times */
+#define APML_FLAG_MARKS_SHIFT 8  /* bits 8..16: with APML_FLAG_STAGE_TIMING, record only the stage
+                                     marks k whose bit (8 + k) is set (0 = all nine).  Stage s
+                                     (0..5) spans marks s, s+1 (Pass A, both directions in one
+                                     launch: marks 1, 3); the backward spans marks 7, 8.  Each
+                                     mark inside a captured CUDA graph is an event-record node
+                                     that costs a few microseconds of pipelining (measured: all
+                                     nine add ~40 us to a 306 us C2 step), so a timed loop
+                                     brackets only the kernel it needs. */
+#define APML_FLAG_MARKS(mask) ((uint32_t)(mask) << APML_FLAG_MARKS_SHIFT)
 #define APML_FLAG_UNIFORM_FALLBACK 8u /* stability mode of dense APML (the sparse kernel
                                      "writes a uniform distribution over the corresponding row
                                      or column") instead of the gap clamp of CUDA-APML

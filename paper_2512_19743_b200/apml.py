@@ -33,6 +33,7 @@ class Config:
     check_finite: bool = False
     stage_timing: bool = False       # CUDA events between stages (apml_ctx_stage_times)
     stability: str = "clamp"         # "clamp" (CUDA-APML) | "uniform" (P:64 / P:97 fallback)
+    stage_marks: int = 0             # with stage_timing: bit k records stage mark k only (0 = all)
 
     def to_c(self) -> A.ApmlConfig:
         if self.grad_mode not in ("full", "plan_detached"):
@@ -42,7 +43,7 @@ class Config:
         flags = (A.APML_FLAG_UNIFORM_FALLBACK if self.stability == "uniform" else 0) | \
             (A.APML_FLAG_SYNC_CHECK if self.sync_check else 0) | \
             (A.APML_FLAG_CHECK_FINITE if self.check_finite else 0) | \
-            (A.APML_FLAG_STAGE_TIMING if self.stage_timing else 0)
+            (A.APML_FLAG_STAGE_TIMING if self.stage_timing else 0) | ((int(self.stage_marks) & 0x1FF) << 8)
         return A.ApmlConfig(self.p_min, self.tau, self.l_iter, self.eps_stab, self.delta, self.eps_g,
                             self.eps_dist, A.APML_GRAD_FULL if self.grad_mode == "full"
                             else A.APML_GRAD_PLAN_DETACHED, self.capacity, flags)

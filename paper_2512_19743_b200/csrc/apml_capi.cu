@@ -90,6 +90,7 @@ struct apml_ctx {
   size_t zero_off = 0, zero_bytes = 0;  // the counters block zeroed before every forward
   bool timing = false;
   bool bwd_timed = false;
+  uint32_t mark_mask = 0x1FFu;  // which of the 9 stage marks are recorded (APML_FLAG_MARKS)
   cudaEvent_t ev[9] = {};  // 0..6 forward stage boundaries, 7 backward start, 8 backward end
   int64_t launches = 0;
   // sparse-stage launch plan
@@ -152,6 +153,40 @@ struct apml_ctx {
 
 namespace {
 
+// Launch with programmatic dependent launch (common.cuh pdl_trigger / pdl_wait) so that the
+// kernel is scheduled while its predecessor's last CTAs still run; APML_PDL=0 disables it.
+bool pdl_on() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("APML_PDL"); v = (e && e[0] == '0') ? 0 : 1; }
+  return v == 1;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 g, dim3 blk, size_t smem, cudaStream_t s, int cluster,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = g;
+  cfg.blockDim = blk;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_on()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster > 0) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = (unsigned)cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // NVTX ranges (domain-less, host-side; visible to Nsight Systems / ncu --nvtx): one per stage
 // of the hot path, named after SURVEY 8(a)'s rows.  No cost without an attached tool.
 struct Nvtx {
@@ -162,7 +197,7 @@ struct Nvtx {
 // Stage events.  Under CUDA-graph capture they become event-record nodes (External flag), so
 // every replay re-records them and apml_ctx_stage_times reads the last replay.
 void mark(apml_ctx* c, int k, cudaStream_t s) {
-  if (!c->timing) return;
+  if (!c->timing || !((c->mark_mask >> k) & 1u)) return;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
   if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(c->ev[k], s, cudaEventRecordExternal);
@@ -572,13 +607,19 @@ apml_status launch_cluster(const apml_ctx* c, K kernel, const SparseArgs& a0, cu
   cfg.blockDim = dim3(kMegaThreads, 1, 1);
   cfg.dynamicSmemBytes = c->smem_bytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)c->cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (pdl_on() && !dbg) {  // (the phase-timing diagnostics synchronise anyway)
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   CK(cudaLaunchKernelEx(&cfg, kernel, a));
   if (dbg) {
     CK(cudaStreamSynchronize(s));
@@ -711,8 +752,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
                      c->part_r, c->nb_d, c->mb_d};
     const Top2Dir dc{c->gtS, (int)Mp, c->predS, (int)Np, c->chunk_cols, c->S_cols, (int)(Mp / kOwnTile),
                      c->part_c, c->mb_d, c->nb_d};
-    k_line_top2_both<kR><<<dim3(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B),
-                           kSweepThreads, 0, s>>>(dr, dc, B);
+    CK(launch_pdl(k_line_top2_both<kR>, dim3(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B),
+                  dim3(kSweepThreads), 0, s, 0, dr, dc, B));
   }
   c->passA_fused = true;
   mark(c, 2, s);
@@ -721,14 +762,15 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   {
     const LineInfoDir lr_{c->part_r, c->S_rows, (int)Np, N, M, c->lam_r, c->rho_r, c->rowA, c->rowB, c->nb_d, c->mb_d, 0};
     const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2};
-    k_line_info_both<<<dim3((std::max(N, M) + 255) / 256, B, 2), 256, 0, s>>>(lr_, lc_, B, c->cfg.delta, c->cfg.eps_g,
-                                                                             c->clamp, c->lr_d, ufb(c));
+    CK(launch_pdl(k_line_info_both, dim3((std::max(N, M) + 255) / 256, B, 2), dim3(256), 0, s, 0, lr_, lc_, B,
+                  c->cfg.delta, c->cfg.eps_g, c->clamp, (const float*)c->lr_d, ufb(c)));
   }
   mark(c, 4, s);
   // S3 Pass B emit
-  k_emit<kR><<<dim3(Np / kOwnTile, c->S_emit, B), kSweepThreads, 0, s>>>(
-      c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_emit, c->cap_e, c->ebuf, c->cursor,
-      c->aux, c->row_cnt, c->col_cnt, c->nb_d, c->mb_d);
+  CK(launch_pdl(k_emit<kR>, dim3(Np / kOwnTile, c->S_emit, B), dim3(kSweepThreads), 0, s, 0,
+                (const float*)c->predS, Np, N, (const LineA*)c->rowA, (const float*)c->gtS, Mp, M,
+                (const LineA*)c->colA, c->chunk_emit, c->cap_e, c->ebuf, c->cursor, c->aux, c->row_cnt,
+                c->col_cnt, (const int*)c->nb_d, (const int*)c->mb_d));
   mark(c, 5, s);
   c->launches += 4;
   CK(cudaGetLastError());
@@ -1217,6 +1259,7 @@ apml_status apml_forward_ragged(const float* pred, const float* gt, int64_t B, i
     if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
     if (c.flags & APML_FLAG_STAGE_TIMING) {
       x->timing = true;
+      if ((c.flags >> APML_FLAG_MARKS_SHIFT) & 0x1FFu) x->mark_mask = (c.flags >> APML_FLAG_MARKS_SHIFT) & 0x1FFu;
       for (auto& e : x->ev)
         if (cudaEventCreate(&e) != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, "cudaEventCreate"); }
     }
@@ -1294,6 +1337,7 @@ apml_status apml_forward_rowsharded(const float* pred, const float* gt, int64_t 
     if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
     if (c.flags & APML_FLAG_STAGE_TIMING) {
       x->timing = true;
+      if ((c.flags >> APML_FLAG_MARKS_SHIFT) & 0x1FFu) x->mark_mask = (c.flags >> APML_FLAG_MARKS_SHIFT) & 0x1FFu;
       for (auto& e : x->ev)
         if (cudaEventCreate(&e) != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, "cudaEventCreate"); }
     }
@@ -1523,13 +1567,21 @@ apml_status apml_ctx_stage_times(const apml_ctx* x, float* ms, int32_t n) {
   if (!x->timing) return fail(APML_ERR_STATE, "context was created without APML_FLAG_STAGE_TIMING");
   if (!ms || n < APML_NUM_STAGES) return fail(APML_ERR_INVALID_ARG, "ms must hold APML_NUM_STAGES floats");
   for (int k = 0; k < APML_NUM_STAGES; ++k) ms[k] = 0.f;
-  CK(cudaEventSynchronize(x->ev[x->bwd_timed ? 8 : 6]));
-  for (int k = 0; k < 6; ++k) CK(cudaEventElapsedTime(&ms[k], x->ev[k], x->ev[k + 1]));
+  const uint32_t mk = x->mark_mask;
+  auto has = [&](int a, int b) { return ((mk >> a) & 1u) && ((mk >> b) & 1u); };
+  int last = -1;  // the last mark recorded by the last forward (+ backward)
+  for (int k = 0; k <= (x->bwd_timed ? 8 : 6); ++k)
+    if ((mk >> k) & 1u) last = k;
+  if (last < 0) return APML_OK;
+  CK(cudaEventSynchronize(x->ev[last]));
+  for (int k = 0; k < 6; ++k)
+    if (has(k, k + 1)) CK(cudaEventElapsedTime(&ms[k], x->ev[k], x->ev[k + 1]));
   if (x->passA_fused) {  // one launch for both Pass A directions: reported as the rows stage
-    CK(cudaEventElapsedTime(&ms[APML_STAGE_PASSA_ROWS], x->ev[1], x->ev[3]));
+    ms[APML_STAGE_PASSA_ROWS] = 0.f;
+    if (has(1, 3)) CK(cudaEventElapsedTime(&ms[APML_STAGE_PASSA_ROWS], x->ev[1], x->ev[3]));
     ms[APML_STAGE_PASSA_COLS] = 0.f;
   }
-  if (x->bwd_timed) CK(cudaEventElapsedTime(&ms[APML_STAGE_SPARSE_BWD], x->ev[7], x->ev[8]));
+  if (x->bwd_timed && has(7, 8)) CK(cudaEventElapsedTime(&ms[APML_STAGE_SPARSE_BWD], x->ev[7], x->ev[8]));
   return APML_OK;
 }
 
@@ -1561,6 +1613,7 @@ apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apml_config*
   if (alloc) { x->alloc = *alloc; x->has_alloc = true; }
   if (c.flags & APML_FLAG_STAGE_TIMING) {
     x->timing = true;
+    if ((c.flags >> APML_FLAG_MARKS_SHIFT) & 0x1FFu) x->mark_mask = (c.flags >> APML_FLAG_MARKS_SHIFT) & 0x1FFu;
     for (auto& e : x->ev)
       if (cudaEventCreate(&e) != cudaSuccess) { apml_ctx_destroy(x); return fail(APML_ERR_CUDA, "cudaEventCreate"); }
   }

@@ -112,4 +112,12 @@ __device__ __forceinline__ bool pair_overflow(const unsigned* cursor, int b, uin
 
 __device__ __forceinline__ int warp_lane() { return threadIdx.x & 31; }
 
+// Programmatic dependent launch (PDL) along the forward / backward chain: every kernel lets
+// its dependent be scheduled as soon as all of its own CTAs are running (launch_dependents),
+// and a dependent runs its prologue (shared-memory carve-out, mbarrier set-up) before it waits
+// for the whole predecessor grid and its memory (wait).  Both are no-ops for a kernel not
+// launched with the programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace apml

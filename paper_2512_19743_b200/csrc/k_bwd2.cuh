@@ -176,6 +176,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
   const size_t pb = (size_t)b * A.cap;
   const Slice sr = slice_of(N, rank, CL), sc = slice_of(M, rank, CL);
   const int nr = sr.hi - sr.lo, nc = sc.hi - sc.lo;
+  pdl_trigger();
+  pdl_wait();  // the forward's saved state (k_sparse_fwd2)
   if (A.cursor[b] > A.cap) {
     const float nan = __int_as_float(0x7fc00000);
     for (int i = sr.lo + threadIdx.x; i < sr.hi; i += blockDim.x) {

@@ -51,6 +51,7 @@ __global__ void k_stage_both(const float* __restrict__ pred, int N, int Np, floa
                              int M, int Mp, float* __restrict__ gtS, float4* __restrict__ gt4,
                              const int* __restrict__ mb, int B) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_trigger();
   if ((int)blockIdx.z < B) stage_point(pred, N, Np, kPadPred, predS, pred4, nb, blockIdx.z, k);
   else stage_point(gt, M, Mp, kPadGt, gtS, gt4, mb, blockIdx.z - B, k);
 }
@@ -140,6 +141,8 @@ __device__ __forceinline__ void top2_block(const float* __restrict__ own_soa, in
   __shared__ __align__(128) TileRing ring;
   const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
   ring_init(ring);
+  pdl_trigger();
+  pdl_wait();  // the staged SoA clouds (k_stage_both)
   if (threadIdx.x == 0) {
     if (j0 < j1) ring_issue(ring, 0, str, str_np, j0);
     if (j0 + kTQ < j1) ring_issue(ring, 1, str, str_np, j0 + kTQ);
@@ -307,6 +310,8 @@ struct LineInfoDir {
 };
 __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int B, float delta, float eps_g,
                                  unsigned long long* __restrict__ clamp_count, const float* __restrict__ lr, int ufb) {
+  pdl_trigger();
+  pdl_wait();  // Pass A's partials
   const LineInfoDir& d = blockIdx.z ? d1 : d0;
   line_info(d.part, d.S, B, d.own_np, d.n, d.K, d.lam, d.rho, delta, eps_g, d.A, d.Bo, clamp_count, d.nown,
             d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb);
@@ -368,6 +373,8 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
   const int b = blockIdx.z, split = blockIdx.y;
   const uint32_t nreal = nb ? (uint32_t)nb[b] : (uint32_t)N, mreal = mb ? (uint32_t)mb[b] : (uint32_t)M;
   if ((uint32_t)(blockIdx.x * kSweepThreads * R) >= nreal) return;  // a block of padding rows
+  pdl_trigger();
+  pdl_wait();  // the line constants (k_line_info_both)
   const int str_end = min(mp, (int)((mreal + kTQ - 1) / kTQ * kTQ));
   const float* own = pred_soa + (size_t)b * 3 * np;
   const float* str = gt_soa + (size_t)b * 3 * mp;

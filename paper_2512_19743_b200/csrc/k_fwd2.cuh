@@ -375,6 +375,8 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
   const int b = blockIdx.x / CL;
   const int N = A.N, M = A.M, L = A.L;
   const size_t pb = (size_t)b * A.cap;
+  pdl_trigger();
+  pdl_wait();  // the emitted support (k_emit)
   const unsigned total = A.cursor[b];
   if (total > A.cap) {  // overflowed pair: uniform across the cluster, no barrier follows
     if (rank == 0 && threadIdx.x == 0) A.loss[b] = __int_as_float(0x7fc00000);

@@ -877,6 +877,8 @@ __device__ void sinkhorn_fwd(cg::cluster_group& cl, const SparseArgs& A, int b, 
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd(const SparseArgs A) {
+  pdl_trigger();
+  pdl_wait();  // launched with programmatic dependent launch: the emit's output first
   extern __shared__ __align__(16) uint8_t shm[];
   __shared__ unsigned s_tot_r[kMaxCluster], s_tot_c[kMaxCluster];  // one per scan (no reuse race)
   __shared__ unsigned s_warp[32];
@@ -1607,6 +1609,8 @@ __device__ void bwd_init_cols(const SparseArgs& A, int b, Slice s, const LongLis
 
 template <typename IdxT>
 __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd(const SparseArgs A) {
+  pdl_trigger();
+  pdl_wait();  // the forward's saved state first
   extern __shared__ __align__(16) uint8_t shm[];
   cg::cluster_group cl = cg::this_cluster();
   const int CL = cl.num_blocks(), rank = cl.block_rank();
