@@ -378,18 +378,19 @@ def main():
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         nl = 0
+        def one_step():
+            p_.forward(pred, gt, loss_buf)
+            p_.backward(ones, out=grad_buf)
         with torch.cuda.stream(side):
             for _ in range(2):
                 l0 = p_.stats()["launches"]
-                p_.forward(pred, gt, loss_buf)
-                p_.backward(ones, out=grad_buf)
+                one_step()
                 nl = p_.stats()["launches"] - l0
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize()
         g_ = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_):
-            p_.forward(pred, gt, loss_buf)
-            p_.backward(ones, out=grad_buf)
+            one_step()
         return p_, g_, nl
 
     if use_graph:
@@ -517,6 +518,10 @@ def main():
         live = med[pre["dominant"]]
         med = dict(pre["stages_ms"])
         med[pre["dominant"]] = live
+    fused = use_graph and os.environ.get("APML_FUSED") == "1" and med.get("sparse_fwd", 1.0) < 0.01
+    if fused:  # apml_plan_forward_backward: one cluster kernel for the sparse forward + backward
+        med["sparse_fwdbwd"] = med.pop("sparse_bwd")
+        med.pop("sparse_fwd", None)
     peaks = _peaks()
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
@@ -537,6 +542,7 @@ def main():
         "sparse_fwd": nnz * (8 + 20 + 48 + 16 * L + 12),   # CSR/CSC + normalise + Sinkhorn + loss
         "sparse_bwd": nnz * (16 * L + 12 + 44 + 12),        # reverse Sinkhorn + P0bar + softmax rev + Eq. 5
     }
+    sparse_bytes["sparse_fwdbwd"] = sparse_bytes["sparse_fwd"] + sparse_bytes["sparse_bwd"]
     dom = max(med, key=med.get)
     traffic = None
     try:

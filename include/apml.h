@@ -284,6 +284,17 @@ APML_API apml_status apml_plan_create(int64_t B, int64_t N, int64_t M, const apm
 APML_API apml_status apml_plan_forward(apml_ctx* plan, const float* pred, const float* gt, void* stream,
                                        float* loss);
 
+/* Forward AND backward of a plan in one call (a training step whose grad_loss -- device [B],
+ * e.g. ones for a sum reduction -- is known before the call; JAX-style value-and-grad).
+ * loss device [B], grad_pred device [B][N][3] overwritten; results equal apml_plan_forward +
+ * apml_backward bit for bit.  With APML_FUSED=1 in the environment the sparse forward and
+ * backward of each pair run in ONE cluster kernel (k_sparse_fwdbwd2: no kernel boundary
+ * between them) -- measured no faster (C2 201 vs 90 + 106 us; C3 equal), so off by default.
+ * Capturable in a CUDA graph.  Errors as apml_plan_forward / apml_backward. */
+APML_API apml_status apml_plan_forward_backward(apml_ctx* plan, const float* pred, const float* gt,
+                                                const float* grad_loss, void* stream, float* loss,
+                                                float* grad_pred);
+
 /* One training step of a plan on HOST buffers -- the end-to-end call: copies pred_host
  * [B][N][3] and gt_host [B][M][3] (fp32, host; pinned memory gives async copies) into
  * plan-owned device buffers, runs the forward and the backward with grad_loss = 1 for every

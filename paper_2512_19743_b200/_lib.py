@@ -26,6 +26,7 @@ EXPORTS = ("apml_abi_version", "apml_config_default", "apml_forward", "apml_forw
            "apml_ctx_stats", "apml_ctx_support", "apml_ctx_lines", "apml_ctx_stage_times",
            "apml_ctx_destroy",
            "apml_loss_grad_host", "apml_plan_step_host", "apml_nvls_create", "apml_nvls_destroy", "apml_nvls_is_multicast",
+           "apml_plan_forward_backward",
            "apml_last_error")
 
 
@@ -121,6 +122,8 @@ def lib() -> C.CDLL:
         L.apml_nvls_is_multicast.argtypes = [vp]
         L.apml_nvls_destroy.restype = None
         L.apml_nvls_destroy.argtypes = [vp]
+        L.apml_plan_forward_backward.restype = C.c_int
+        L.apml_plan_forward_backward.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.apml_plan_step_host.restype = C.c_int
         L.apml_plan_step_host.argtypes = [vp, vp, vp, vp, vp, vp]
         L.apml_last_error.restype = C.c_char_p

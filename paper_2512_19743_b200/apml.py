@@ -200,6 +200,22 @@ class Plan(Context):
         return loss
 
 
+    def forward_backward(self, pred: torch.Tensor, gt: torch.Tensor, grad_loss: torch.Tensor,
+                         loss_out: torch.Tensor | None = None, grad_out: torch.Tensor | None = None):
+        """apml_plan_forward_backward: per-pair losses and d(sum_b grad_loss[b] loss_b)/d pred in one
+        call (sparse forward + backward fused in one cluster kernel); capturable in a graph."""
+        pred = _check_points(pred, "pred")
+        gt = _check_points(gt, "gt")
+        if tuple(pred.shape) != (self.B, self.N, 3) or tuple(gt.shape) != (self.B, self.M, 3):
+            raise ValueError("pred / gt shapes differ from the plan's")
+        gl = grad_loss.to(device=self.device, dtype=torch.float32).contiguous().reshape(self.B)
+        loss = loss_out if loss_out is not None else torch.empty(self.B, device=self.device, dtype=torch.float32)
+        g = grad_out if grad_out is not None else torch.empty(self.B, self.N, 3, device=self.device)
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        A.check(A.lib().apml_plan_forward_backward(self._h, pred.data_ptr(), gt.data_ptr(), gl.data_ptr(), s,
+                                                   loss.data_ptr(), g.data_ptr()))
+        return loss, g
+
     def step_host(self, pred_host: torch.Tensor, gt_host: torch.Tensor, loss_out: torch.Tensor | None = None,
                   grad_out: torch.Tensor | None = None):
         """apml_plan_step_host: host fp32 [B,N,3] / [B,M,3] in, host loss [B] and grad [B,N,3] out

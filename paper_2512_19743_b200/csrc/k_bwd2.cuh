@@ -164,9 +164,10 @@ __device__ void grad_rows_sm(const SparseArgs& A, int b, Slice s, const unsigned
   }
 }
 
-__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArgs A) {
+__device__ __forceinline__ void sparse_bwd2_body(const SparseArgs& A) {
   extern __shared__ __align__(16) uint8_t shm[];
-  __shared__ uint32_t s_long_r[kLongCap], s_long_c[kLongCap];
+  uint32_t* s_long_r = long_lists();
+  uint32_t* s_long_c = s_long_r + kLongCap;
   __shared__ int s_nlong[2];
   __shared__ __align__(8) unsigned long long s_mbar[2];
   cg::cluster_group cl = cg::this_cluster();
@@ -365,6 +366,21 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArg
   else grad_rows<1, 4>(A, b, sr, llr);
   grad_rows<32, 1>(A, b, sr, llr);
   phase(A, 6);
+}
+
+__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_bwd2(const SparseArgs A) { sparse_bwd2_body(A); }
+
+// Forward + backward in ONE launch (apml_plan_forward_backward: the training step with
+// grad_loss known before the launch).  Each cluster runs its pair's sparse forward, one
+// cluster barrier (release / acquire at cluster scope: the pair's CSR / CSC arrays, history and
+// line data written by any CTA of the cluster are visible to all of them), then the backward:
+// no kernel boundary between them, and a pair whose forward finishes early goes straight on
+// instead of waiting for the slowest pair of the batch.
+__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwdbwd2(const SparseArgs A) {
+  sparse_fwd2_body(A);
+  cg::cluster_group cl = cg::this_cluster();
+  csync(cl);
+  sparse_bwd2_body(A);
 }
 
 }  // namespace apml

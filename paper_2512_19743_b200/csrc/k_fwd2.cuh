@@ -362,12 +362,13 @@ __device__ void fwd2_sinkhorn(cg::cluster_group& cl, const SparseArgs& A, int b,
   sinkhorn_fwd<IdxT, kSm>(cl, A, b, sr, sc, RV, CV, xa, xb, llr, llc, rperm, cperm);
 }
 
-__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArgs A) {
+__device__ __forceinline__ void sparse_fwd2_body(const SparseArgs& A) {
   extern __shared__ __align__(16) uint8_t shm[];
   __shared__ unsigned s_tot[2][kMaxCluster];
   __shared__ unsigned s_warp[32];
   __shared__ double s_part[kMaxCluster];
-  __shared__ uint32_t s_long_r[kLongCap], s_long_c[kLongCap];
+  uint32_t* s_long_r = long_lists();
+  uint32_t* s_long_c = s_long_r + kLongCap;
   __shared__ int s_nlong[2];
   __shared__ __align__(8) unsigned long long s_mbar[4];
   cg::cluster_group cl = cg::this_cluster();
@@ -692,5 +693,7 @@ __global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArg
   }
   phase(A, 8);
 }
+
+__global__ void __launch_bounds__(kMegaThreads, 1) k_sparse_fwd2(const SparseArgs A) { sparse_fwd2_body(A); }
 
 }  // namespace apml

@@ -188,6 +188,13 @@ __device__ void cluster_scan(cg::cluster_group& cl, unsigned* cnt, unsigned* ptr
 constexpr uint32_t kRegLine = 16;  // lines up to this length are sorted in registers by one thread
 constexpr int kLongCap = 1024;     // per-CTA list of longer lines (warp per line)
 
+// The two long-line lists of a CTA (rows, columns) in ONE static shared allocation, shared by
+// every kernel body that calls this (the fused forward + backward reuses it: 8 KB once).
+__device__ __forceinline__ uint32_t* long_lists() {
+  __shared__ uint32_t buf[2 * kLongCap];
+  return buf;
+}
+
 // The lines of a slice longer than kRegLine, collected once so that warp-per-line passes do
 // not walk (and load the offsets of) every line of the slice.
 struct LongList {

@@ -738,3 +738,45 @@ def test_uniform_fallback_mode(env, mode, monkeypatch):
     assert st["uniform_count"] == nu and nu >= 20
     # the uniform lines really are dense: each duplicated-minimum row keeps all M entries
     assert st["nnz_total"] >= nu * min(N, M) // 2
+
+
+@pytest.mark.parametrize("shape", [("shapenet", 4, 2048, 2048), ("mmfi", 6, 1024, 512), ("uniform", 3, 700, 650)])
+def test_plan_forward_backward_fused_matches(shape, monkeypatch):
+    """apml_plan_forward_backward (sparse forward + backward in ONE cluster kernel) gives the
+    bits of apml_plan_forward + apml_backward, eagerly and replayed from a CUDA graph, with a
+    non-trivial grad_loss; an overflowed pair still reports NaN."""
+    Config, forward = _gpu()
+    from paper_2512_19743_b200 import Plan
+    monkeypatch.setenv("APML_FUSED", "1")
+    kind, B, N, M = shape
+    cfg = Config(sync_check=False)
+    x, y = clouds.batch(kind, B, N, M, 81)
+    pred, gt = torch.tensor(x, device="cuda"), torch.tensor(y, device="cuda")
+    gl = torch.linspace(0.5, 2.0, B, device="cuda")
+    plan = Plan(B, N, M, cfg)
+    lr = plan.forward(pred, gt).clone()          # (the calibrating first forward)
+    gr = plan.backward(gl).clone()
+    lf, gf = plan.forward_backward(pred, gt, gl)
+    assert torch.equal(lf, lr) and torch.equal(gf, gr)
+    ls, gs = torch.zeros(B, device="cuda"), torch.zeros(B, N, 3, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        plan.forward_backward(pred, gt, gl, loss_out=ls, grad_out=gs)
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.forward_backward(pred, gt, gl, loss_out=ls, grad_out=gs)
+    x2, y2 = clouds.batch(kind, B, N, M, 82)
+    pred.copy_(torch.tensor(x2)); gt.copy_(torch.tensor(y2))
+    g.replay()
+    torch.cuda.synchronize()
+    l2, c2 = forward(pred, gt, cfg)
+    g2 = c2.backward(gl)
+    assert torch.equal(ls, l2) and torch.equal(gs, g2)
+    plan.close()
+    small = Plan(B, N, M, Config(sync_check=False, capacity=1))
+    lo, go = small.forward_backward(pred, gt, gl)
+    torch.cuda.synchronize()
+    assert torch.isnan(lo).all() and torch.isnan(go).all()
+    small.close()
