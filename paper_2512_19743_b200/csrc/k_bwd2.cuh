@@ -339,12 +339,12 @@ __device__ __forceinline__ void sparse_bwd2_body(const SparseArgs& A) {
     if (fit16) {
       const SliceView<uint16_t> R{roff, r16, rP0, racc};
       const SliceView<uint16_t> C{coff, c16, cP0, nullptr};
-      sinkhorn_bwd<uint16_t, true>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bhs ? nullptr : bls, ahs, bhs, llr, llc,
+      sinkhorn_bwd<uint16_t, true>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, (bhs || M > kPf * (int)blockDim.x) ? nullptr : bls, ahs, bhs, llr, llc,
                                     rperm, cperm);
     } else {
       const SliceView<uint32_t> R{roff, rjf, rP0, racc};
       const SliceView<uint32_t> C{coff, cif, cP0, nullptr};
-      sinkhorn_bwd<uint32_t, false>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, bhs ? nullptr : bls, ahs, bhs, llr, llc);
+      sinkhorn_bwd<uint32_t, false>(cl, A, b, sr, sc, R, C, ab, bb, xr, xq, (bhs || M > kPf * (int)blockDim.x) ? nullptr : bls, ahs, bhs, llr, llc);
     }
   }
   if (fit16)
