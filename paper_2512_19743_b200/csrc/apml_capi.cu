@@ -115,6 +115,7 @@ struct apml_ctx {
   float *gce2 = nullptr, *gfe2 = nullptr;  // largest column emit radius per tile / sub-tile
   float2* gre = nullptr;                   // column (R2, E2) in sorted order
   float* bbpart = nullptr;                 // partial pair boxes [B][kBoxParts][6]
+  float *psb = nullptr, *gsb = nullptr, *gsce2 = nullptr;  // super-tile boxes (32 tiles), gt: + max E2
   // batched scans (CSR/CSC pointers, Morton cells) and the grid-wide loss
   unsigned* tsum = nullptr;
   double* lossp = nullptr;
@@ -474,6 +475,9 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_pfb = k.take<float>(cu ? 6 * B * (c->Np / kSub) : 0), o_gfb = k.take<float>(cu ? 6 * B * (c->Mp / kSub) : 0);
   size_t o_gfe2 = k.take<float>(cu ? B * (c->Mp / kSub) : 0), o_gre = k.take<float2>(cu ? B * c->Mp : 0);
   size_t o_bbpart = k.take<float>(cu ? 6 * B * kBoxParts : 0);
+  const int64_t nst_p = (c->Np / kTQ + kSuper - 1) / kSuper, nst_g = (c->Mp / kTQ + kSuper - 1) / kSuper;
+  size_t o_psb = k.take<float>(cu ? 6 * B * nst_p : 0), o_gsb = k.take<float>(cu ? 6 * B * nst_g : 0);
+  size_t o_gsce2 = k.take<float>(cu ? B * nst_g : 0);
   const int64_t tiles_rc = scan_tiles(N + 1) + scan_tiles(M + 1), tiles_cells = 2 * scan_tiles(cells1);
   size_t o_tsum = k.take<unsigned>(B * std::max(tiles_rc, tiles_cells));
   size_t o_lossp = k.take<double>(B * ((N + kLossThreads - 1) / kLossThreads));
@@ -511,7 +515,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->pfb = (float*)(p + o_pfb); c->gfb = (float*)(p + o_gfb);
   c->gce2 = (float*)(p + o_gce2); c->gfe2 = (float*)(p + o_gfe2); c->gre = (float2*)(p + o_gre);
   c->ipperm = c->relabel ? (int*)(p + o_ipperm) : nullptr;
-  c->bbpart = (float*)(p + o_bbpart); c->tsum = (unsigned*)(p + o_tsum); c->lossp = (double*)(p + o_lossp);
+  c->bbpart = (float*)(p + o_bbpart);
+  c->psb = (float*)(p + o_psb); c->gsb = (float*)(p + o_gsb); c->gsce2 = (float*)(p + o_gsce2); c->tsum = (unsigned*)(p + o_tsum); c->lossp = (double*)(p + o_lossp);
   c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
   c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
   c->pstart = (uint32_t*)(p + o_pstart); c->gstart = (uint32_t*)(p + o_gstart);
@@ -667,6 +672,9 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
       c->ghist, c->gtS, c->gperm, c->relabel ? c->gt4 : nullptr, nullptr);
   k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->pcb, c->pfb);
   k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
+  k_super_box<<<dim3((Np / kTQ + kSuper - 1) / kSuper, B), 32, 0, s>>>(c->pcb, Np / kTQ, c->psb, nullptr, nullptr);
+  k_super_box<<<dim3((Mp / kTQ + kSuper - 1) / kSuper, B), 32, 0, s>>>(c->gcb, Mp / kTQ, c->gsb, nullptr, nullptr);
+  c->launches += 2;
   mark(c, 1, s);
   // both directions in one launch (the stage marks 2 and 3 bracket it together)
   if (env_long("APML_CULL_BOTH", 1)) {
@@ -676,9 +684,9 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
     const long few = (long)B * (Np + Mp) / (kSweepThreads * kRc) < 28L * num_sms();
     const int rc = env_long("APML_CULL_RA", few ? 1 : kRc) == 1 ? 1 : kRc;
     const CullDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gcb, c->gfb, c->part_r, c->clamp + 1,
-                     (int)(Np / (kSweepThreads * rc))};
+                     (int)(Np / (kSweepThreads * rc)), c->gsb};
     const CullDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pcb, c->pfb, c->part_c, c->clamp + 2,
-                     (int)(Mp / (kSweepThreads * rc))};
+                     (int)(Mp / (kSweepThreads * rc)), c->psb};
     if (rc == 1)
       k_line_top2_cull_both<1><<<dim3(std::max(dr.nblk, dc.nblk), B, 2), kSweepThreads, 0, s>>>(dr, dc,
                                                                                              (int)c->relabel);
@@ -690,10 +698,10 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
     c->launches -= 1;
   } else {
     k_line_top2_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
-        c->gtS, Mp, c->gcb, c->gfb, (int)c->relabel, c->part_r, c->clamp + 1);
+        c->gtS, Mp, c->gcb, c->gfb, c->gsb, (int)c->relabel, c->part_r, c->clamp + 1);
     mark(c, 2, s);
     k_line_top2_cull<kRc><<<dim3(Mp / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->gtS, Mp, M, c->gperm,
-        c->predS, Np, c->pcb, c->pfb, (int)c->relabel, c->part_c, c->clamp + 2);
+        c->predS, Np, c->pcb, c->pfb, c->psb, (int)c->relabel, c->part_c, c->clamp + 2);
     c->passA_fused = false;
   }
   c->launches += 11;  // + the scan's own
@@ -707,15 +715,17 @@ apml_status launch_emit_cull(apml_ctx* c) {
   cudaStream_t s = c->stream;
   k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
                                                c->gfe2);
+  k_super_box<<<dim3((Mp / kTQ + kSuper - 1) / kSuper, B), 32, 0, s>>>(c->gcb, Mp / kTQ, c->gsb, c->gce2, c->gsce2);
+  c->launches += 1;
   // kRc groups per warp; APML_EMIT_R=1 (one group per warp, as Pass A at C5) measured slower
   // here: C5 emit 0.532 -> 0.546 ms, C4 0.601 -> 0.648 ms
   if (env_long("APML_EMIT_R", kRc) == 1)
     k_emit_cull<1><<<dim3(Np / kSweepThreads, B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm, c->rowA,
-        c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap_e, c->ebuf,
+        c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->gsb, c->gsce2, c->cap_e, c->ebuf,
         c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
   else
     k_emit_cull<kRc><<<dim3(Np / (kSweepThreads * kRc), B), kSweepThreads, 0, s>>>(c->predS, Np, N, c->pperm,
-        c->rowA, c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->cap_e, c->ebuf,
+        c->rowA, c->gtS, Mp, M, c->gperm, (int)c->relabel, c->gre, c->gcb, c->gfb, c->gce2, c->gfe2, c->gsb, c->gsce2, c->cap_e, c->ebuf,
         c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
   c->launches += 2;
   CK(cudaGetLastError());

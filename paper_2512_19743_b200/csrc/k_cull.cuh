@@ -192,6 +192,37 @@ k_tile_re(const int* __restrict__ gperm, int mp, const LineA* __restrict__ colA,
   }
 }
 
+// Super-tiles of 32 consecutive tiles (4096 sorted points): box = union of the tile boxes and,
+// for the emit, the largest column emit radius of its tiles.  The candidate walks test a
+// super-tile first and only its surviving tiles individually: the flat walk tested every
+// tile of the cloud against every warp (ncu at C5: ~35 % of the culled Pass A samples in the
+// tile-box tests, stalled on their global loads).  grid (ceil(nt / 32), B), 32 threads.
+constexpr int kSuper = 32;
+__global__ void __launch_bounds__(32) k_super_box(const float* __restrict__ cb, int nt, float* __restrict__ sb,
+                                                  const float* __restrict__ ce2, float* __restrict__ sce2) {
+  const int b = blockIdx.y, s = blockIdx.x, lane = threadIdx.x;
+  const int nst = (nt + kSuper - 1) / kSuper;
+  const int t = s * kSuper + lane;
+  float lo[3] = {3e38f, 3e38f, 3e38f}, hi[3] = {-3e38f, -3e38f, -3e38f};
+  float e = -1.f;
+  if (t < nt) {
+    const float* tb = cb + ((size_t)b * nt + t) * 6;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) { lo[d] = tb[d]; hi[d] = tb[3 + d]; }
+    if (ce2) e = ce2[(size_t)b * nt + t];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+      hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+    }
+    e = fmaxf(e, __shfl_xor_sync(0xffffffffu, e, o));
+  }
+  if (lane < 6) sb[((size_t)b * nst + s) * 6 + lane] = lane < 3 ? lo[lane] : hi[lane - 3];
+  if (sce2 && lane == 0) sce2[(size_t)b * nst + s] = e;
+}
+
 __device__ __forceinline__ float box_dist2(const float* a, const float* b) {
   float s = 0.f;
 #pragma unroll
@@ -265,9 +296,9 @@ template <int R>
 __device__ __forceinline__ void top2_cull_block(const float* __restrict__ own_soa, int own_np, int own_n,
                                                 const int* __restrict__ own_perm, const float* __restrict__ str_soa,
                                                 int str_np, const float* __restrict__ str_cb,
-                                                const float* __restrict__ str_fb, int relabel,
-                                                float2* __restrict__ out, unsigned long long* __restrict__ evals,
-                                                const int blk, const int b) {
+                                                const float* __restrict__ str_fb, const float* __restrict__ str_sb,
+                                                int relabel, float2* __restrict__ out,
+                                                unsigned long long* __restrict__ evals, const int blk, const int b) {
   constexpr int kW = kSweepThreads / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* own = own_soa + (size_t)b * 3 * own_np;
@@ -308,12 +339,24 @@ __device__ __forceinline__ void top2_cull_block(const float* __restrict__ own_so
   unsigned nev = 0;
   const int own_base = blk * kSweepThreads * R + w * 32 * R;
   const int t0 = min(nt - 1, (int)((long long)own_base * nt / own_np));
+  // Candidate tiles come from a two-level generator: super-tiles (32 tiles) in a ring around
+  // the warp's own super-tile, each tested against the warp bound with one broadcast box; the
+  // 32 tiles of a surviving super-tile are tested one per lane (one ballot).  Inside the own
+  // super-tile the candidates start at the own tile so the bound tightens first.  The data of
+  // the NEXT candidate (its sub-tile box for this lane's (group, sub-tile) test and its
+  // coordinates) is loaded into registers before the current one is evaluated, so the
+  // dependent global round trips overlap the arithmetic.  A candidate chosen with an older,
+  // larger bound is only a weaker filter: the result is unchanged.
   // Candidate tiles come from a generator (32 ring steps per ballot against the warp bound);
   // the data of the NEXT candidate (its sub-tile box for this lane's (group, sub-tile) test
   // and its coordinates) is loaded into registers before the current one is evaluated, so
   // the two dependent global round trips per tile overlap the arithmetic (the walk was
   // latency-bound: ncu 13 % occupancy, 45 % issue).  A candidate chosen with an older,
-  // larger bound is only a weaker filter: the result is unchanged.
+  // larger bound is only a weaker filter: the result is unchanged.  (A two-level walk over
+  // super-tiles of 32 tiles, str_sb, measured slower here: C5 Pass A 0.57 -> 0.67 ms, C4
+  // 0.88 -> 1.10 ms -- the ring order of single tiles tightens the bound sooner; the emit,
+  // whose bound is fixed, does use it.)
+  (void)str_sb;
   int gbase = 0, gT = -1;
   unsigned gcm = 0u;
   auto next_cand = [&]() -> int {
@@ -404,10 +447,10 @@ template <int R>
 __global__ void __launch_bounds__(kSweepThreads)
 k_line_top2_cull(const float* __restrict__ own_soa, int own_np, int own_n, const int* __restrict__ own_perm,
                  const float* __restrict__ str_soa, int str_np, const float* __restrict__ str_cb,
-                 const float* __restrict__ str_fb, int relabel, float2* __restrict__ out,
-                 unsigned long long* __restrict__ evals) {
-  top2_cull_block<R>(own_soa, own_np, own_n, own_perm, str_soa, str_np, str_cb, str_fb, relabel, out, evals,
-                     blockIdx.x, blockIdx.y);
+                 const float* __restrict__ str_fb, const float* __restrict__ str_sb, int relabel,
+                 float2* __restrict__ out, unsigned long long* __restrict__ evals) {
+  top2_cull_block<R>(own_soa, own_np, own_n, own_perm, str_soa, str_np, str_cb, str_fb, str_sb, relabel, out,
+                     evals, blockIdx.x, blockIdx.y);
 }
 
 // Both culled Pass A directions in ONE launch (grid.z = 2: rows, then columns).  At B = 1
@@ -425,14 +468,15 @@ struct CullDir {
   float2* out;
   unsigned long long* evals;
   int nblk;
+  const float* str_sb;  // super-tile boxes of the streamed cloud (k_super_box)
 };
 template <int R>
 __global__ void __launch_bounds__(kSweepThreads) k_line_top2_cull_both(const CullDir d0, const CullDir d1,
                                                                        int relabel) {
   const CullDir& d = blockIdx.z ? d1 : d0;
   if ((int)blockIdx.x >= d.nblk) return;
-  top2_cull_block<R>(d.own, d.own_np, d.own_n, d.own_perm, d.str, d.str_np, d.str_cb, d.str_fb, relabel, d.out,
-                     d.evals, blockIdx.x, blockIdx.y);
+  top2_cull_block<R>(d.own, d.own_np, d.own_n, d.own_perm, d.str, d.str_np, d.str_cb, d.str_fb, d.str_sb, relabel,
+                     d.out, d.evals, blockIdx.x, blockIdx.y);
 }
 
 // Culled Pass B: as k_emit over the sorted clouds, evaluating only the (group, sub-tile)
@@ -444,6 +488,7 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
             const LineA* __restrict__ rowA, const float* __restrict__ gt_soa, int mp, int M,
             const int* __restrict__ gperm, int relabel, const float2* __restrict__ gre, const float* __restrict__ gcb,
             const float* __restrict__ gfb, const float* __restrict__ gce2, const float* __restrict__ gfe2,
+            const float* __restrict__ gsb, const float* __restrict__ gsce2,
             uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
             unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt, unsigned* __restrict__ col_cnt,
             unsigned long long* __restrict__ evals) {
@@ -499,8 +544,28 @@ k_emit_cull(const float* __restrict__ pred_soa, int np, int N, const int* __rest
   }
   __syncwarp();
   unsigned nev = 0;
-  for (int base = 0; base < nt; base += 32) {
-    const int T = base + lane;
+  // two-level scan: 32 super-tiles per ballot (box + largest column emit radius), then the 32
+  // tiles of each surviving super-tile (one per lane)
+  const int nst = (nt + kSuper - 1) / kSuper;
+  const float* sbx = gsb + (size_t)b * nst * 6;
+  const float* sce = gsce2 + (size_t)b * nst;
+  unsigned scm = 0u;
+  int sbase = 0, ST = -1;
+  for (;;) {
+    while (!scm && sbase < nst) {
+      ST = sbase + lane;
+      bool sc = false;
+      if (ST < nst) {
+        const float lb = box_dist2(wbox, sbx + (size_t)ST * 6) * kCullMargin;
+        sc = lb <= fmaxf(wE, sce[ST]) && lb < 3e38f;
+      }
+      scm = __ballot_sync(0xffffffffu, sc);
+      sbase += 32;
+    }
+    if (!scm) break;
+    const int sl = __ffs(scm) - 1;
+    scm &= scm - 1;
+    const int T = __shfl_sync(0xffffffffu, ST, sl) * kSuper + lane;
     bool cand = false;
     if (T < nt) {
       const float lb = box_dist2(wbox, cb + (size_t)T * 6) * kCullMargin;
