@@ -141,6 +141,7 @@ struct apml_ctx {
   unsigned *row_cnt, *col_cnt, *row_ptr, *col_ptr;
   uint32_t *csr_t, *csc_t, *inv, *csr_jf, *csc_i, *csc_perm;
   uint32_t* csc_if = nullptr;  // CSC-order copies (k_sparse_fwd2 -> k_sparse_bwd2)
+  uint16_t *csr16 = nullptr, *csc16 = nullptr;  // grid path: 16-bit Sinkhorn indices
   float *csc_c = nullptr, *csc_pc = nullptr;
   float *d2s, *cs, *prow, *pcol, *P0, *P0c, *pbar;
   int2 *rowidx, *colidx;
@@ -393,6 +394,8 @@ apml_status alloc_entries(apml_ctx* c, uint32_t cap) {
   size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
   const int64_t E2 = f2 ? E : 0;  // CSC-order copies written by k_sparse_fwd2
   size_t o_csc_if = k.take<uint32_t>(E2), o_csc_c = k.take<float>(E2), o_csc_pc = k.take<float>(E2);
+  const int64_t E3 = (c->rs && c->N <= 65536 && c->M <= 65536 && env_long("APML_RS_IDX16", 1) != 0) ? E : 0;
+  size_t o_csr16 = k.take<uint16_t>(E3), o_csc16 = k.take<uint16_t>(E3);
   c->ebytes = k.off;
   c->ebase = (char*)ctx_alloc(c, c->ebytes);
   if (!c->ebase) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->ebytes) + " bytes failed");
@@ -402,6 +405,8 @@ apml_status alloc_entries(apml_ctx* c, uint32_t cap) {
   c->d2s = (float*)(p + o_d2); c->cs = (float*)(p + o_cs); c->prow = (float*)(p + o_prow); c->pcol = (float*)(p + o_pcol);
   c->P0 = (float*)(p + o_P0); c->P0c = (float*)(p + o_P0c); c->pbar = (float*)(p + o_pbar);
   c->csc_if = (uint32_t*)(p + o_csc_if); c->csc_c = (float*)(p + o_csc_c); c->csc_pc = (float*)(p + o_csc_pc);
+  c->csr16 = E3 ? (uint16_t*)(p + o_csr16) : nullptr;
+  c->csc16 = E3 ? (uint16_t*)(p + o_csc16) : nullptr;
   return APML_OK;
 }
 
@@ -539,6 +544,7 @@ SparseArgs sparse_args(const apml_ctx* c, float* loss, const float* grad_loss, f
   a.row_ptr = c->row_ptr; a.col_ptr = c->col_ptr; a.csr_t = c->csr_t; a.csc_t = c->csc_t; a.inv = c->inv;
   a.csr_jf = c->csr_jf; a.csc_i = c->csc_i; a.csc_perm = c->csc_perm;
   a.csc_if = c->csc_if; a.csc_c = c->csc_c; a.csc_pc = c->csc_pc;
+  a.csr16 = c->csr16; a.csc16 = c->csc16;
   a.d2s = c->d2s; a.cs = c->cs; a.prow = c->prow; a.pcol = c->pcol; a.P0 = c->P0; a.P0c = c->P0c; a.pbar = c->pbar;
   a.rowidx = c->rowidx; a.colidx = c->colidx; a.a_hist = c->a_hist; a.b_hist = c->b_hist; a.gvec = c->gvec;
   a.rowback = c->rowback; a.colback = c->colback;
@@ -934,6 +940,10 @@ apml_status launch_sparse_fwd_rs(apml_ctx* c, float* loss) {
   if ((st = coll_sum(c, c->colred, 3LL * B * M)) != APML_OK) return st;
   if ((st = coll_gather(c, (const float*)c->cand, (float*)c->gcand, 3LL * B * M)) != APML_OK) return st;
   k_rs_cols_b<<<gc, kRsThreads, 0, s>>>(a, c->gcand, c->comm.world);
+  if (c->csr16) {
+    k_rs_idx16<<<dim3((c->cap + 255) / 256, B), 256, 0, s>>>(a);
+    c->launches += 1;
+  }
   k_rs_bstep<<<gc256, 256, 0, s>>>(a, 0, nullptr);
   k_rs_astep<<<gr256, 256, 0, s>>>(a, 0);
   c->launches += 6;  // + the scan's own

@@ -59,6 +59,8 @@ struct SparseArgs {
   uint32_t* csc_i;
   uint32_t* csc_perm;
   uint32_t* csc_if;  // CSC order (k_sparse_fwd2): i | flags, c, P_col
+  uint16_t* csr16;   // grid path, N, M <= 65536: 16-bit other-cloud indices for Sinkhorn (or NULL)
+  uint16_t* csc16;
   float* csc_c;
   float* csc_pc;
   float* d2s;
