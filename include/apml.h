@@ -270,7 +270,7 @@ APML_API apml_status apml_backward_ex(apml_ctx* ctx, const float* grad_loss, flo
  * APML_FLAG_CHECK_FINITE are ignored), so a training step `apml_plan_forward +
  * apml_backward[_ex]` can be captured into a CUDA graph and replayed.  Exception: with
  * cfg->capacity == 0 (the default) the per-entry arrays (CSR / CSC, ~64 B per entry) are
- * sized by the plan's FIRST forward -- 1.5 x the largest per-pair support it emits, one count
+ * sized by the plan's FIRST forward -- 1.25 x the largest per-pair support it emits, one count
  * read-back and one allocation in that call only -- so that memory follows the support, not
  * the emit capacity; if that first forward is itself being captured they take the emit
  * capacity.  A later input whose support exceeds that size is reported like a capacity

@@ -313,7 +313,8 @@ long env_long(const char* name, long dflt) {
   return (e && *e) ? strtol(e, nullptr, 10) : dflt;
 }
 
-void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk, int64_t target_div = 1) {
+void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk, int64_t target_div = 1,
+                int64_t max_s = 1 << 30) {
   const int64_t blocks = own_np / kOwnTile * B;
   // ~16 waves of 4 CTAs / SM (target_div = 2: the two Pass A directions share one launch);
   // measured (APML_SPLIT_TARGET sweep, ms/step): C3 1.274 (4 waves) -> 1.232 (8) / 1.237 (16),
@@ -322,6 +323,7 @@ void plan_split(int64_t own_np, int64_t str_np, int64_t B, int* S, int* chunk, i
   int64_t s = (target + blocks - 1) / blocks;
   const int64_t tiles = str_np / kTQ;
   if (s > tiles) s = tiles;
+  if (s > max_s) s = max_s;
   if (s < 1) s = 1;
   const int64_t ch = ((tiles + s - 1) / s) * kTQ;
   *chunk = (int)ch;
@@ -438,8 +440,11 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   // for k_line_info to merge); the emit sweep keeps the full target.  The row-sharded mode
   // launches the Pass A directions separately.
   const int64_t pa_div = c->rs ? 1 : 2;
-  plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows, pa_div);
-  plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols, pa_div);
+  // Pass A: at most 8 column splits -- each costs 8 bytes per line of partials (C2: 16 -> 8
+  // splits, -8.4 MB, step time unchanged within noise: 0.317 vs 0.320 ms); C3's 4 unaffected
+  const int64_t max_s = env_long("APML_MAX_SPLITS", 8);
+  plan_split(c->Np, c->Mp, B, &c->S_rows, &c->chunk_rows, pa_div, max_s);
+  plan_split(c->Mp, c->Np, B, &c->S_cols, &c->chunk_cols, pa_div, max_s);
   plan_split(c->Np, c->Mp, B, &c->S_emit, &c->chunk_emit);
   plan_sparse(c);
   Carve k;
@@ -1672,7 +1677,7 @@ apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, v
   x->grad_gt = nullptr;
   apml_status st = x->rs ? launch_forward_rs(x, pred, gt) : launch_forward(x, pred, gt);
   if (st == APML_OK && !x->ebase) {
-    // first forward of a calibrating plan: the per-entry arrays at 1.5 x the largest support
+    // first forward of a calibrating plan: the per-entry arrays at 1.25 x the largest support
     // of this forward (one count read-back, this call only); inside a graph capture (no
     // read-back possible) at the emit capacity
     uint32_t cap = x->cap_e;
@@ -1682,7 +1687,7 @@ apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, v
       CK(cudaStreamSynchronize(x->stream));
       unsigned mx = 0;
       for (unsigned v : cnt) mx = v > mx ? v : mx;
-      cap = fitted_cap(mx, x->cap_e, 1.5);
+      cap = fitted_cap(mx, x->cap_e, 1.25);
     }
     st = alloc_entries(x, cap);
   }
