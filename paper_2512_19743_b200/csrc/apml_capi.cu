@@ -137,6 +137,7 @@ struct apml_ctx {
   float2 *part_r, *part_c;
   LineA *rowA, *colA; LineB *rowB, *colB;
   unsigned long long* clamp;  // [0] clamped lines, [1..3] evaluations of the culled sweeps
+  unsigned* icnt = nullptr;    // Pass A + S2 fused: arrivals per (direction, pair, row block)
   uint2* ebuf; unsigned *cursor, *aux;
   unsigned *row_cnt, *col_cnt, *row_ptr, *col_ptr;
   uint32_t *csr_t, *csc_t, *inv, *csr_jf, *csc_i, *csc_perm;
@@ -463,6 +464,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t z0 = k.off;
   size_t o_phist = k.take<uint32_t>(B * cells1), o_ghist = k.take<uint32_t>(B * cells1);
   size_t o_clamp = k.take<unsigned long long>(5);  // clamp count, culled-sweep evaluations [3], uniform lines
+  const int64_t nblk_max = std::max(c->Np, c->Mp) / kOwnTile;
+  size_t o_icnt = k.take<unsigned>(2 * B * nblk_max);  // Pass A + S2 fused: arrivals per row block
   size_t o_cursor = k.take<unsigned>(B), o_aux = k.take<unsigned>(B);
   size_t o_row_cnt = k.take<unsigned>(B * (N + 1)), o_col_cnt = k.take<unsigned>(B * (M + 1));
   size_t z1 = k.off;
@@ -505,6 +508,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->rowA = (LineA*)(p + o_rowA); c->colA = (LineA*)(p + o_colA);
   c->rowB = (LineB*)(p + o_rowB); c->colB = (LineB*)(p + o_colB);
   c->clamp = (unsigned long long*)(p + o_clamp);
+  c->icnt = (unsigned*)(p + o_icnt);
   c->cursor = (unsigned*)(p + o_cursor); c->aux = (unsigned*)(p + o_aux);
   c->row_cnt = (unsigned*)(p + o_row_cnt); c->col_cnt = (unsigned*)(p + o_col_cnt);
   c->row_ptr = (unsigned*)(p + o_row_ptr); c->col_ptr = (unsigned*)(p + o_col_ptr);
@@ -773,18 +777,26 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
                      c->part_r, c->nb_d, c->mb_d};
     const Top2Dir dc{c->gtS, (int)Mp, c->predS, (int)Np, c->chunk_cols, c->S_cols, (int)(Mp / kOwnTile),
                      c->part_c, c->mb_d, c->nb_d};
-    CK(launch_pdl(k_line_top2_both<kR>, dim3(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B),
-                  dim3(kSweepThreads), 0, s, 0, dr, dc, B));
-  }
-  c->passA_fused = true;
-  mark(c, 2, s);
-  mark(c, 3, s);
-  // S2 line constants (rows and columns in one launch)
-  {
     const LineInfoDir lr_{c->part_r, c->S_rows, (int)Np, N, M, c->lam_r, c->rho_r, c->rowA, c->rowB, c->nb_d, c->mb_d, 0};
     const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2};
-    CK(launch_pdl(k_line_info_both, dim3((std::max(N, M) + 255) / 256, B, 2), dim3(256), 0, s, 0, lr_, lc_, B,
-                  c->cfg.delta, c->cfg.eps_g, c->clamp, (const float*)c->lr_d, ufb(c)));
+    const dim3 ga(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B);
+    if (env_long("APML_FUSE_INFO", 1) != 0) {  // S2 in the last CTA of every row block
+      const FusedInfo fi{{lr_, lc_}, c->cfg.delta, c->cfg.eps_g, c->clamp, (const float*)c->lr_d, ufb(c), c->icnt,
+                         (int)(std::max(Np, Mp) / kOwnTile)};
+      CK(launch_pdl(k_line_top2_info<kR>, ga, dim3(kSweepThreads), 0, s, 0, dr, dc, B, fi));
+      c->passA_fused = true;
+      mark(c, 2, s);
+      mark(c, 3, s);
+      c->launches -= 1;
+    } else {
+      CK(launch_pdl(k_line_top2_both<kR>, ga, dim3(kSweepThreads), 0, s, 0, dr, dc, B));
+      c->passA_fused = true;
+      mark(c, 2, s);
+      mark(c, 3, s);
+      // S2 line constants (rows and columns in one launch)
+      CK(launch_pdl(k_line_info_both, dim3((std::max(N, M) + 255) / 256, B, 2), dim3(256), 0, s, 0, lr_, lc_, B,
+                    c->cfg.delta, c->cfg.eps_g, c->clamp, (const float*)c->lr_d, ufb(c)));
+    }
   }
   mark(c, 4, s);
   // S3 Pass B emit

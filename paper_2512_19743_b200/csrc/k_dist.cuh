@@ -317,6 +317,42 @@ __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int
             d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb);
 }
 
+// Pass A with S2 fused (the full sweeps): every CTA of a (direction, pair, row block) writes
+// its partial (min, second) and counts itself in; the LAST of the block's S column splits
+// merges the S partials of its 512 lines into the line constants (line_info), so no separate
+// launch (and no kernel boundary) is needed between Pass A and the emit.  Writers: stores,
+// __threadfence, then the counter; the last CTA fences before reading the other partials.
+struct FusedInfo {
+  LineInfoDir li[2];  // rows, columns
+  float delta, eps_g;
+  unsigned long long* clamp;
+  const float* lr;
+  int ufb;
+  unsigned* cnt;      // [2][B][nblk] arrivals, zeroed before every forward
+  int nblk;           // row-block stride of cnt (the larger direction's)
+};
+template <int R>
+__global__ void __launch_bounds__(kSweepThreads) k_line_top2_info(const Top2Dir d0, const Top2Dir d1, int B,
+                                                                   const FusedInfo fi) {
+  const int dir = blockIdx.z >= (unsigned)B;
+  const Top2Dir& d = dir ? d1 : d0;
+  if ((int)blockIdx.x >= d.nblk || (int)blockIdx.y >= d.S) return;
+  const int b = blockIdx.z - dir * B;
+  top2_block<R>(d.own, d.own_np, d.str, d.str_np, d.chunk, B, d.part, d.nown, d.nstr, blockIdx.x, blockIdx.y, b);
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    s_last = atomicAdd(fi.cnt + ((size_t)dir * B + b) * fi.nblk + blockIdx.x, 1u) == (unsigned)d.S - 1u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const LineInfoDir& L = fi.li[dir];
+  for (int k = threadIdx.x; k < kSweepThreads * R; k += blockDim.x)
+    line_info(L.part, L.S, B, L.own_np, L.n, L.K, L.lam, L.rho, fi.delta, fi.eps_g, L.A, L.Bo, fi.clamp, L.nown,
+              L.kpair, fi.lr, L.lr_off, b, (int)blockIdx.x * kSweepThreads * R + k, fi.ufb);
+}
+
 // Emission (S3).  Counts keep running past the capacity so the host can size a retry;
 // overflowed pairs are skipped downstream; the per-line counts are non-returning reductions.
 // Per-lane emission queues (k_emit, k_emit_cull): every lane appends its own hits to its own slots of a
