@@ -406,6 +406,8 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_FWD2": "0"},                                          # global-memory sparse forward (k_sparse_fwd)
     {"APML_BWD2": "0"},                                          # k_sparse_fwd2 + k_sparse_bwd
     {"APML_SMEM_LIMIT": "60000", "APML_CL": "1"},                # fwd2 / bwd2 slices in global memory
+    {"APML_FUSE_INFO": "0", "APML_PDL": "0"},                    # separate line-info launch, no PDL
+    {"APML_GRID": "1", "APML_RS_IDX16": "0"},                    # grid path with 32-bit Sinkhorn indices
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_sparse_stage_fallback_paths(env, monkeypatch):
     """The plan the library picks depends on N, M, B and shared memory; force every variant at a
