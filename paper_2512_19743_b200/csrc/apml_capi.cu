@@ -79,9 +79,12 @@ struct apml_ctx {
   size_t bytes = 0;
   char* ebase = nullptr;  // the per-entry arrays (stride cap), a second allocation
   size_t ebytes = 0;
+  char* embase = nullptr; // the emit buffer (stride cap_e), a third allocation (re-sized by a
+  size_t embytes = 0;     // calibrating plan once its first forward has consumed it)
   uint32_t cap = 0;       // per-pair stride of the per-entry arrays (sized from the support)
   uint32_t cap_e = 0;     // per-pair stride of the emit buffer (the emit capacity)
   bool calibrate = false; // plan: size the per-entry arrays on the first forward
+  bool ebuf_fitted = false;
   int S_rows = 1, S_cols = 1, chunk_rows = 0, chunk_cols = 0;
   int S_emit = 1, chunk_emit = 0;  // column split of the emit sweep (its own wave target)
   bool backward_done = false;
@@ -235,6 +238,13 @@ void* ctx_alloc(apml_ctx* c, size_t bytes) {
   return p;
 }
 
+void mem_free(apml_ctx* c, char*& p, size_t bytes) {
+  if (!p) return;
+  if (c->has_alloc) c->alloc.free(p, bytes, c->stream, c->alloc.user);
+  else cudaFreeAsync(p, c->stream);
+  p = nullptr;
+}
+
 void ctx_free(apml_ctx* c) {
   for (auto& e : c->ev)
     if (e) { cudaEventDestroy(e); e = nullptr; }
@@ -244,11 +254,8 @@ void ctx_free(apml_ctx* c) {
     else cudaFreeAsync(c->hbuf, c->stream);
     c->hbuf = nullptr;
   }
-  if (c->ebase) {
-    if (c->has_alloc) c->alloc.free(c->ebase, c->ebytes, c->stream, c->alloc.user);
-    else cudaFreeAsync(c->ebase, c->stream);
-    c->ebase = nullptr;
-  }
+  mem_free(c, c->ebase, c->ebytes);
+  mem_free(c, c->embase, c->embytes);
   if (!c->base) return;
   if (c->has_alloc) c->alloc.free(c->base, c->bytes, c->stream, c->alloc.user);
   else cudaFreeAsync(c->base, c->stream);
@@ -470,7 +477,6 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_row_cnt = k.take<unsigned>(B * (N + 1)), o_col_cnt = k.take<unsigned>(B * (M + 1));
   size_t z1 = k.off;
   size_t o_row_ptr = k.take<unsigned>(B * (N + 1)), o_col_ptr = k.take<unsigned>(B * (M + 1));
-  size_t o_ebuf = k.take<uint2>(E);
   size_t o_nb = k.take<int>(c->ragged ? B : 0), o_mb = k.take<int>(c->ragged ? B : 0);
   size_t o_lr = k.take<float>(c->ragged ? 4 * B : 0);
   size_t o_rowidx = k.take<int2>(B * N), o_colidx = k.take<int2>(B * M);
@@ -478,9 +484,11 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_gv = k.take<float>(B * 2 * (N + M));
   size_t o_rowback = k.take<LineBack>(B * N), o_colback = k.take<LineBack>(B * M);
   const int64_t W = c->rs ? c->comm.world : 0;
-  size_t o_colpart = k.take<float2>(c->rs ? B * M : 0), o_gath = k.take<float2>(W * B * M);
+  // world 1 without forced collectives: the "gathered" copies ARE the local arrays
+  const bool w1 = c->rs && c->comm.world == 1 && env_long("APML_RS_COLLECTIVES", 0) == 0;
+  size_t o_colpart = k.take<float2>(c->rs ? B * M : 0), o_gath = k.take<float2>(w1 ? 0 : W * B * M);
   size_t o_colred = k.take<float>(c->rs ? 3 * B * M : 0), o_qbuf = k.take<float>(c->rs ? B * M : 0);
-  size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(3 * W * B * M);
+  size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(w1 ? 0 : 3 * W * B * M);
   size_t o_flag = k.take<float>(16);
   const bool cu = c->cull;
   size_t o_pbb = k.take<float>(cu ? 6 * B : 0), o_pcb = k.take<float>(cu ? 6 * B * (c->Np / kTQ) : 0);
@@ -501,6 +509,10 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->bytes = k.off;
   c->base = (char*)ctx_alloc(c, c->bytes);
   if (!c->base) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->bytes) + " bytes failed");
+  c->embytes = sizeof(uint2) * (size_t)std::max<int64_t>(E, 1);
+  c->embase = (char*)ctx_alloc(c, c->embytes);
+  if (!c->embase) return fail(APML_ERR_OOM, "allocation of the emit buffer failed");
+  c->ebuf = (uint2*)c->embase;
   char* p = c->base;
   c->predS = (float*)(p + o_predS); c->gtS = (float*)(p + o_gtS);
   c->pred4 = (float4*)(p + o_pred4); c->gt4 = (float4*)(p + o_gt4);
@@ -512,7 +524,6 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->cursor = (unsigned*)(p + o_cursor); c->aux = (unsigned*)(p + o_aux);
   c->row_cnt = (unsigned*)(p + o_row_cnt); c->col_cnt = (unsigned*)(p + o_col_cnt);
   c->row_ptr = (unsigned*)(p + o_row_ptr); c->col_ptr = (unsigned*)(p + o_col_ptr);
-  c->ebuf = (uint2*)(p + o_ebuf);
   if (c->ragged) {  // pageable host vectors: the copies are staged before the calls return
     c->nb_d = (int*)(p + o_nb); c->mb_d = (int*)(p + o_mb); c->lr_d = (float*)(p + o_lr);
     CK(cudaMemcpyAsync(c->nb_d, c->nb_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice, c->stream));
@@ -522,9 +533,9 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->rowidx = (int2*)(p + o_rowidx); c->colidx = (int2*)(p + o_colidx);
   c->a_hist = (float*)(p + o_ah); c->b_hist = (float*)(p + o_bh); c->gvec = (float*)(p + o_gv);
   c->rowback = (LineBack*)(p + o_rowback); c->colback = (LineBack*)(p + o_colback);
-  c->colpart = (float2*)(p + o_colpart); c->gath = (float2*)(p + o_gath);
+  c->colpart = (float2*)(p + o_colpart); c->gath = w1 ? c->colpart : (float2*)(p + o_gath);
   c->colred = (float*)(p + o_colred); c->qbuf = (float*)(p + o_qbuf);
-  c->cand = (int*)(p + o_cand); c->gcand = (int*)(p + o_gcand); c->flag = (float*)(p + o_flag);
+  c->cand = (int*)(p + o_cand); c->gcand = w1 ? c->cand : (int*)(p + o_gcand); c->flag = (float*)(p + o_flag);
   c->pbb = (float*)(p + o_pbb); c->pcb = (float*)(p + o_pcb); c->gcb = (float*)(p + o_gcb);
   c->pfb = (float*)(p + o_pfb); c->gfb = (float*)(p + o_gfb);
   c->gce2 = (float*)(p + o_gce2); c->gfe2 = (float*)(p + o_gfe2); c->gre = (float2*)(p + o_gre);
@@ -827,6 +838,7 @@ apml_status launch_sparse_fwd(apml_ctx* c, float* loss) {
 // the sparse stage of choice when there are too few pairs to fill the GPU with clusters.
 int local_allreduce(float*, int64_t, void*, void*) { return 0; }
 int local_allgather(const float* send, float* recv, int64_t n, void* stream, void*) {
+  if (recv == send) return 0;  // (the gathered copy aliases the local array at world 1)
   return cudaMemcpyAsync(recv, send, sizeof(float) * (size_t)n, cudaMemcpyDeviceToDevice,
                          (cudaStream_t)stream) == cudaSuccess ? 0 : 1;
 }
@@ -1703,7 +1715,21 @@ apml_status apml_plan_forward(apml_ctx* x, const float* pred, const float* gt, v
     }
     st = alloc_entries(x, cap);
   }
+  const bool calibrated_now = x->calibrate && x->ebase && !x->ebuf_fitted && !capturing(x->stream);
   if (st == APML_OK) st = x->rs ? launch_sparse_fwd_rs(x, loss) : launch_sparse_fwd(x, loss);
+  if (st == APML_OK && calibrated_now) {
+    // the emit buffer at the per-entry capacity from now on (the first forward's sparse stage,
+    // enqueued above, still reads the old one: the free is stream-ordered after it)
+    x->ebuf_fitted = true;
+    if (x->cap < x->cap_e) {
+      mem_free(x, x->embase, x->embytes);
+      x->cap_e = x->cap;
+      x->embytes = sizeof(uint2) * (size_t)x->B * x->cap_e;
+      x->embase = (char*)ctx_alloc(x, x->embytes);
+      if (!x->embase) return fail(APML_ERR_OOM, "allocation of the emit buffer failed");
+      x->ebuf = (uint2*)x->embase;
+    }
+  }
   if (st == APML_OK) x->forward_done = true;
   return st;
 }
