@@ -96,3 +96,29 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(^|\s)(from|import)\s+oracle\b|liboracle|apml_oracle", txt), f
+
+
+def test_round2_entry_points_validate_on_host():
+    """ABI 3 entry points reject bad arguments before touching the device: NVLS teams need
+    rank < world and, for world > 1, the host all-gather used for the handle rendezvous; plan
+    calls need a plan; the stage-mark mask travels in the config flags."""
+    import ctypes as C
+    L = A.lib()
+    h = C.c_void_p()
+    comm = A.ApmlComm(0, 2, A.ALLREDUCE_FN(lambda *a: 0), A.ALLGATHER_FN(lambda *a: 0), None,
+                      A.GATHER_BYTES_FN(), None)  # world 2, no allgather_bytes
+    assert L.apml_nvls_create(C.byref(comm), 4096, C.byref(h)) == A.APML_ERR_INVALID_ARG
+    assert h.value is None
+    bad = A.ApmlComm(3, 2, A.ALLREDUCE_FN(lambda *a: 0), A.ALLGATHER_FN(lambda *a: 0), None,
+                     A.GATHER_BYTES_FN(), None)  # rank >= world
+    assert L.apml_nvls_create(C.byref(bad), 4096, C.byref(h)) == A.APML_ERR_INVALID_ARG
+    assert L.apml_nvls_is_multicast(None) == 0
+    L.apml_nvls_destroy(None)  # no-op
+    assert L.apml_plan_forward_backward(None, None, None, None, None, None, None) == A.APML_ERR_STATE
+    assert L.apml_plan_step_host(None, None, None, None, None, None) == A.APML_ERR_STATE
+    from paper_2512_19743_b200 import Config
+    c = Config(stage_timing=True, stage_marks=(1 << 7) | (1 << 8)).to_c()
+    assert (c.flags >> 8) & 0x1FF == (1 << 7) | (1 << 8)
+    assert Config(stability="uniform").to_c().flags & A.APML_FLAG_UNIFORM_FALLBACK
+    with pytest.raises(ValueError):
+        Config(stability="dense").to_c()
