@@ -442,7 +442,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   if (c->cull) {
     int lg = 0;
     while ((1LL << lg) < std::max(N, M)) ++lg;
-    c->cell_bits = std::min(7, std::max(2, (lg + 2) / 3));
+    // ~0.5-4 points per Morton cell: the 4 cell arrays cost 16 B per cell (65k: 2^18 -> 2^15 cells)
+    c->cell_bits = std::min(7, std::max(2, (lg + 1) / 3));
   }
   // full sweeps: Pass A rows + columns share one launch (half the target each; fewer partials
   // for k_line_info to merge); the emit sweep keeps the full target.  The row-sharded mode
