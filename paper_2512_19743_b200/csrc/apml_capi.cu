@@ -17,6 +17,7 @@
 #include "../../include/apml.h"
 #include "common.cuh"
 #include "k_cull.cuh"
+#include "k_cells.cuh"
 #include "k_fwd2.cuh"
 #include "k_bwd2.cuh"
 #include "k_dist.cuh"
@@ -113,6 +114,7 @@ struct apml_ctx {
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // spatially culled sweeps (k_cull.cuh)
   bool cull = false;
+  bool cells = false;     // culled sweeps over the Morton cell grid (k_cells.cuh), else the tile walk
   int cell_bits = 0;
   float *pbb = nullptr, *pcb = nullptr, *pfb = nullptr, *gcb = nullptr, *gfb = nullptr;  // tile / sub-tile boxes
   float *gce2 = nullptr, *gfe2 = nullptr;  // largest column emit radius per tile / sub-tile
@@ -439,11 +441,24 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   const long fc = env_long("APML_CULL", -1);
   c->cull = !c->ragged && (fc >= 0 ? fc != 0 : std::min(N, M) >= 4096);
   c->relabel = c->cull && (!c->rs || (c->comm.world == 1 && c->row_offset == 0)) && env_long("APML_RELABEL", 1) != 0;
+  c->cells = c->cull && env_long("APML_CULL_MODE", 1) != 0;
   if (c->cull) {
     int lg = 0;
     while ((1LL << lg) < std::max(N, M)) ++lg;
-    // ~0.5-4 points per Morton cell: the 4 cell arrays cost 16 B per cell (65k: 2^18 -> 2^15 cells)
-    c->cell_bits = std::min(7, std::max(2, (lg + 1) / 3));
+    if (c->cells) {
+      // cell sweeps: cells of a few neighbour spacings on surface-like clouds (points on a few
+      // surfaces in the box: occupied cells ~ G^2), G = 2^((lg - 3) / 2) capped at 64 per axis --
+      // 16384 -> 32 (C4), 262144 -> 64 (C5); measured (ms Pass A + emit): C4 bits 4 / 5:
+      // 1.49 / 1.04, C5 bits 5 / 6 / 7: 0.52 / 0.28 / 0.34.  At most 2^22 cells over the batch
+      // (the four cell arrays cost 16 B per cell).
+      int bits = std::min(6, std::max(2, (lg - 3) / 2));
+      while (bits > 2 && (B << (3 * bits)) > (1LL << 22)) --bits;
+      c->cell_bits = (int)env_long("APML_CELL_BITS", bits);
+      c->cell_bits = std::min(7, std::max(1, c->cell_bits));
+    } else {
+      // ~0.5-4 points per Morton cell: the 4 cell arrays cost 16 B per cell (65k: 2^18 -> 2^15 cells)
+      c->cell_bits = std::min(7, std::max(2, (lg + 1) / 3));
+    }
   }
   // full sweeps: Pass A rows + columns share one launch (half the target each; fewer partials
   // for k_line_info to merge); the emit sweep keeps the full target.  The row-sharded mode
@@ -491,12 +506,12 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_colred = k.take<float>(c->rs ? 3 * B * M : 0), o_qbuf = k.take<float>(c->rs ? B * M : 0);
   size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(w1 ? 0 : 3 * W * B * M);
   size_t o_flag = k.take<float>(16);
-  const bool cu = c->cull;
-  size_t o_pbb = k.take<float>(cu ? 6 * B : 0), o_pcb = k.take<float>(cu ? 6 * B * (c->Np / kTQ) : 0);
+  const bool cu = c->cull && !c->cells;  // tile / sub-tile / super-tile boxes: the tile walk only
+  size_t o_pbb = k.take<float>(c->cull ? 6 * B : 0), o_pcb = k.take<float>(cu ? 6 * B * (c->Np / kTQ) : 0);
   size_t o_gcb = k.take<float>(cu ? 6 * B * (c->Mp / kTQ) : 0), o_gce2 = k.take<float>(cu ? B * (c->Mp / kTQ) : 0);
   size_t o_pfb = k.take<float>(cu ? 6 * B * (c->Np / kSub) : 0), o_gfb = k.take<float>(cu ? 6 * B * (c->Mp / kSub) : 0);
   size_t o_gfe2 = k.take<float>(cu ? B * (c->Mp / kSub) : 0), o_gre = k.take<float2>(cu ? B * c->Mp : 0);
-  size_t o_bbpart = k.take<float>(cu ? 6 * B * kBoxParts : 0);
+  size_t o_bbpart = k.take<float>(c->cull ? 6 * B * kBoxParts : 0);
   const int64_t nst_p = (c->Np / kTQ + kSuper - 1) / kSuper, nst_g = (c->Mp / kTQ + kSuper - 1) / kSuper;
   size_t o_psb = k.take<float>(cu ? 6 * B * nst_p : 0), o_gsb = k.take<float>(cu ? 6 * B * nst_g : 0);
   size_t o_gsce2 = k.take<float>(cu ? B * nst_g : 0);
@@ -504,9 +519,9 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_tsum = k.take<unsigned>(B * std::max(tiles_rc, tiles_cells));
   size_t o_lossp = k.take<double>(B * ((N + kLossThreads - 1) / kLossThreads));
   size_t o_ipperm = k.take<int>(c->relabel ? B * N : 0);
-  size_t o_pkey = k.take<uint32_t>(cu ? B * N : 0), o_gkey = k.take<uint32_t>(cu ? B * M : 0);
+  size_t o_pkey = k.take<uint32_t>(c->cull ? B * N : 0), o_gkey = k.take<uint32_t>(c->cull ? B * M : 0);
   size_t o_pstart = k.take<uint32_t>(B * cells1), o_gstart = k.take<uint32_t>(B * cells1);
-  size_t o_pperm = k.take<int>(cu ? B * c->Np : 0), o_gperm = k.take<int>(cu ? B * c->Mp : 0);
+  size_t o_pperm = k.take<int>(c->cull ? B * c->Np : 0), o_gperm = k.take<int>(c->cull ? B * c->Mp : 0);
   c->bytes = k.off;
   c->base = (char*)ctx_alloc(c, c->bytes);
   if (!c->base) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->bytes) + " bytes failed");
@@ -697,6 +712,25 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
       c->phist, c->predS, c->pperm, c->relabel ? c->pred4 : nullptr, c->ipperm);
   k_cell_scatter<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, bits, c->gkey, c->gstart,
       c->ghist, c->gtS, c->gperm, c->relabel ? c->gt4 : nullptr, nullptr);
+  if (c->cells) {  // Pass A over the cell grid (k_cells.cuh), both directions in one launch
+    const int cw = 32 * kCellWarps;
+    static int stats_on = -1;
+    if (stats_on < 0) {
+      stats_on = env_long("APML_CELL_STATS", 0) != 0;
+      CK(cudaMemcpyToSymbol(g_cell_stats_on, &stats_on, sizeof(int)));
+    }
+    const CellDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gstart, c->part_r, c->clamp + 1,
+                     (int)((Np + cw - 1) / cw)};
+    const CellDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pstart, c->part_c, c->clamp + 2,
+                     (int)((Mp + cw - 1) / cw)};
+    mark(c, 1, s);
+    k_top2_cells<<<dim3(std::max(dr.nblk, dc.nblk), B, 2), cw, 0, s>>>(dr, dc, c->pbb, bits, cells1, (int)c->relabel);
+    c->passA_fused = true;
+    mark(c, 2, s);
+    c->launches += 8;  // bbox x2, count x2, scatter x2, Pass A (+ the scan's own)
+    CK(cudaGetLastError());
+    return APML_OK;
+  }
   k_tile_bbox<<<dim3(Np / kTQ, B), kTQ, 0, s>>>(c->predS, Np, N, c->pcb, c->pfb);
   k_tile_bbox<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gtS, Mp, M, c->gcb, c->gfb);
   k_super_box<<<dim3((Np / kTQ + kSuper - 1) / kSuper, B), 32, 0, s>>>(c->pcb, Np / kTQ, c->psb, nullptr, nullptr);
@@ -740,6 +774,29 @@ apml_status launch_emit_cull(apml_ctx* c) {
   const Nvtx nvtx_("apml S3 culled emit");
   const int B = (int)c->B, N = (int)c->N, M = (int)c->M, Np = (int)c->Np, Mp = (int)c->Mp;
   cudaStream_t s = c->stream;
+  if (c->cells) {  // row pass + column pass over the cell grid (k_cells.cuh)
+    const int bits = c->cell_bits, cells1 = (1 << (3 * bits)) + 1;
+    const int cw = 32 * kCellWarps;
+    const CellEmitDir dr{c->predS, (int)Np, N, c->pperm, c->rowA, c->gtS, (int)Mp, c->gstart, c->gperm, c->colA,
+                         (int)((Np + cw - 1) / cw)};
+    const CellEmitDir dc{c->gtS, (int)Mp, M, c->gperm, c->colA, c->predS, (int)Np, c->pstart, c->pperm, c->rowA,
+                         (int)((Mp + cw - 1) / cw)};
+    k_emit_cells<<<dim3(std::max(dr.nblk, dc.nblk), B, 2), cw, 0, s>>>(dr, dc, c->pbb, bits, cells1, (int)c->relabel,
+        N, M, c->cap_e, c->ebuf, c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
+    c->launches += 1;
+    if (env_long("APML_CELL_STATS", 0)) {  // diagnostics (synchronises): counters of this forward
+      unsigned long long h[16];
+      CK(cudaStreamSynchronize(s));
+      CK(cudaMemcpyFromSymbol(h, g_cell_stats, sizeof h));
+      fprintf(stderr, "[apml cells] bits %d | PassA rounds %llu staged %llu far %llu shells %llu groups %llu warps %llu"
+              " | emit rounds %llu staged %llu far %llu groups %llu warps %llu\n", bits, h[0], h[1], h[2], h[3], h[4],
+              h[5], h[8], h[9], h[10], h[12], h[13]);
+      memset(h, 0, sizeof h);
+      CK(cudaMemcpyToSymbol(g_cell_stats, h, sizeof h));
+    }
+    CK(cudaGetLastError());
+    return APML_OK;
+  }
   k_tile_re<<<dim3(Mp / kTQ, B), kTQ, 0, s>>>(c->gperm, Mp, c->colA, M, (int)c->relabel, c->gre, c->gce2,
                                                c->gfe2);
   k_super_box<<<dim3((Mp / kTQ + kSuper - 1) / kSuper, B), 32, 0, s>>>(c->gcb, Mp / kTQ, c->gsb, c->gce2, c->gsce2);

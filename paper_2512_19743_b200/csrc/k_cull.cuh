@@ -75,6 +75,16 @@ __device__ __forceinline__ uint32_t spread_bits3(uint32_t v) {  // 10-bit v -> e
   return v;
 }
 
+// Cell of one coordinate in a G-cell axis over [lo, hi] (and the fractional coordinate f):
+// ONE definition for the sort (k_cell_count) and the cell sweeps (k_cells.cuh), so a point is
+// always looked up in the cell it was sorted into.
+__device__ __forceinline__ uint32_t cell_axis(float p, float lo, float hi, uint32_t G, float* frac) {
+  const float ext = fmaxf(hi - lo, 1e-30f);
+  const float f = (p - lo) / ext * (float)G;
+  *frac = f;
+  return (uint32_t)fminf(fmaxf(f, 0.f), (float)(G - 1));
+}
+
 // Morton cell key of every point (bits per axis) and the per-pair cell histogram.
 __global__ void k_cell_count(const float* __restrict__ pts, int n, const float* __restrict__ bb, int bits,
                              uint32_t* __restrict__ key, uint32_t* __restrict__ hist) {
@@ -85,12 +95,9 @@ __global__ void k_cell_count(const float* __restrict__ pts, int n, const float* 
   const float* box = bb + b * 6;
   const uint32_t cells_axis = 1u << bits;
   uint32_t c[3];
+  float f;
 #pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const float ext = fmaxf(box[3 + d] - box[d], 1e-30f);
-    float f = (p[d] - box[d]) / ext * (float)cells_axis;
-    c[d] = (uint32_t)fminf(fmaxf(f, 0.f), (float)(cells_axis - 1));
-  }
+  for (int d = 0; d < 3; ++d) c[d] = cell_axis(p[d], box[d], box[3 + d], cells_axis, &f);
   const uint32_t kk = spread_bits3(c[0]) | (spread_bits3(c[1]) << 1) | (spread_bits3(c[2]) << 2);
   key[(size_t)b * n + k] = kk;
   atomicAdd(hist + (size_t)b * ((1u << (3 * bits)) + 1) + kk, 1u);

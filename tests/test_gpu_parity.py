@@ -399,10 +399,13 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_CL": "1"},                                            # one CTA per pair, no DSMEM peers
     {"APML_CL": "2"},
     {"APML_GRID": "1"},                                          # grid-wide kernels (few, large pairs)
-    {"APML_CULL": "1"},                                          # spatially culled sweeps (NEXT-2)
+    {"APML_CULL": "1"},                                          # spatially culled sweeps (NEXT-2): cell grid
     {"APML_CULL": "1", "APML_GRID": "1"},
-    {"APML_CULL": "1", "APML_CULL_RA": "2", "APML_EMIT_R": "1"},  # Pass A 2 groups per warp, emit 1
-    {"APML_CULL": "1", "APML_CULL_BOTH": "0"},                   # culled Pass A, one launch per direction
+    {"APML_CULL": "1", "APML_CELL_BITS": "1"},                   # 2 cells per axis: boxes reach the grid edge
+    {"APML_CULL": "1", "APML_CELL_BITS": "6"},                   # tiny cells: shells, per-cell cubes
+    {"APML_CULL": "1", "APML_CULL_MODE": "0"},                   # tile walk (k_cull.cuh)
+    {"APML_CULL": "1", "APML_CULL_MODE": "0", "APML_CULL_RA": "2", "APML_EMIT_R": "1"},  # 2 groups / warp, emit 1
+    {"APML_CULL": "1", "APML_CULL_MODE": "0", "APML_CULL_BOTH": "0"},  # tile walk, one launch per direction
     {"APML_FWD2": "0"},                                          # global-memory sparse forward (k_sparse_fwd)
     {"APML_BWD2": "0"},                                          # k_sparse_fwd2 + k_sparse_bwd
     {"APML_SMEM_LIMIT": "60000", "APML_CL": "1"},                # fwd2 / bwd2 slices in global memory
