@@ -714,11 +714,6 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
       c->ghist, c->gtS, c->gperm, c->relabel ? c->gt4 : nullptr, nullptr);
   if (c->cells) {  // Pass A over the cell grid (k_cells.cuh), both directions in one launch
     const int cw = 32 * kCellWarps;
-    static int stats_on = -1;
-    if (stats_on < 0) {
-      stats_on = env_long("APML_CELL_STATS", 0) != 0;
-      CK(cudaMemcpyToSymbol(g_cell_stats_on, &stats_on, sizeof(int)));
-    }
     const CellDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gstart, c->part_r, c->clamp + 1,
                      (int)((Np + cw - 1) / cw)};
     const CellDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pstart, c->part_c, c->clamp + 2,
@@ -784,7 +779,7 @@ apml_status launch_emit_cull(apml_ctx* c) {
     k_emit_cells<<<dim3(std::max(dr.nblk, dc.nblk), B, 2), cw, 0, s>>>(dr, dc, c->pbb, bits, cells1, (int)c->relabel,
         N, M, c->cap_e, c->ebuf, c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
     c->launches += 1;
-    if (env_long("APML_CELL_STATS", 0)) {  // diagnostics (synchronises): counters of this forward
+    if (APML_CELL_DIAG && env_long("APML_CELL_STATS", 0)) {  // diagnostics (synchronises)
       unsigned long long h[16];
       CK(cudaStreamSynchronize(s));
       CK(cudaMemcpyFromSymbol(h, g_cell_stats, sizeof h));

@@ -36,12 +36,15 @@ struct CellBox {
   int lo[3], hi[3];
 };
 
-// APML_CELL_STATS=1 (diagnostics): [0] cell rounds, [1] staged points, [2] far lanes, [3] shells,
-// [4] groups, [5] warps -- Pass A in [0, 8), the emit in [8, 16)
+// Diagnostics (a build with -DAPML_CELL_DIAG=1, printed with APML_CELL_STATS=1): [0] cell rounds,
+// [1] staged points, [2] far lanes, [3] shells, [4] groups, [5] warps -- Pass A in [0, 8), the
+// emit in [8, 16).  Compiled out by default (the flag load alone cost ~5 % of the emit).
+#ifndef APML_CELL_DIAG
+#define APML_CELL_DIAG 0
+#endif
 __device__ unsigned long long g_cell_stats[16];
-__device__ int g_cell_stats_on;
 __device__ __forceinline__ void cell_stat(int k, unsigned long long v) {
-  if (g_cell_stats_on && (threadIdx.x & 31) == 0 && v) atomicAdd(&g_cell_stats[k], v);
+  if (APML_CELL_DIAG && (threadIdx.x & 31) == 0 && v) atomicAdd(&g_cell_stats[k], v);
 }
 
 __device__ __forceinline__ uint32_t morton3(uint32_t x, uint32_t y, uint32_t z) {
@@ -122,10 +125,11 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
   // small-integer division by ex, ex * ey in fp32 (exact for V < 2^17: the quotient's true value
   // is at least 0.5 / ex away from an integer)
   const float rx = 1.0f / (float)ex, rxy = 1.0f / (float)exy;
-  for (int base = 0; base < V; base += 32) {
-    cell_stat(8 * kEmit + 0, 1);
-    const int idx = base + lane;
-    uint32_t cst = 0, cnt = 0;
+  // the cell starts of the NEXT round are loaded before this round's points are staged and
+  // evaluated (their latency overlaps the work)
+  auto cell_of = [&](int idx, uint32_t& cst, uint32_t& cnt) {
+    cst = 0;
+    cnt = 0;
     if (idx < V) {
       const int qz = (int)(((float)idx + 0.5f) * rxy), rem = idx - qz * exy;
       const int qy = (int)(((float)rem + 0.5f) * rx), qx = rem - qy * ex;
@@ -135,9 +139,16 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
       if (!skip) {
         const uint32_t key = morton3((uint32_t)ix, (uint32_t)iy, (uint32_t)iz);
         cst = __ldg(start + key);
-        cnt = __ldg(start + key + 1) - cst;
+        cnt = __ldg(start + key + 1);
       }
     }
+  };
+  uint32_t ncst, ncnt;
+  cell_of(lane, ncst, ncnt);
+  for (int base = 0; base < V; base += 32) {
+    cell_stat(8 * kEmit + 0, 1);
+    const uint32_t cst = ncst, cnt = ncnt - ncst;
+    if (base + 32 < V) cell_of(base + 32 + lane, ncst, ncnt);
     uint32_t inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -147,33 +158,47 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
     const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
     cell_stat(8 * kEmit + 1, T);
     const uint32_t bse = cst - (inc - cnt);  // sorted position of round slot s of this lane's cell: bse + s
-    for (uint32_t sb = 0; sb < T; sb += 32) {
-      if (filled > kCellBuf - 32) {
-        __syncwarp();
-        eval(filled);
-        filled = 0;
-      }
-      const uint32_t s = sb + (uint32_t)lane;
+    auto src_of = [&](uint32_t s) {
       int l = 0;
 #pragma unroll
       for (int wd = 16; wd; wd >>= 1) {
         const uint32_t v = __shfl_sync(0xffffffffu, inc, l + wd - 1);
         if (v <= s) l += wd;
       }
-      const uint32_t src = __shfl_sync(0xffffffffu, bse, l & 31) + s;
-      const uint32_t n = min(32u, T - sb);
-      if ((uint32_t)lane < n) {
-        const int dst = filled + lane;
-        st.x[dst] = __ldg(str + src);
-        st.y[dst] = __ldg(str + str_np + src);
-        st.z[dst] = __ldg(str + 2 * (size_t)str_np + src);
-        if (kEmit) {
-          const int o = relabel ? (int)src : __ldg(perm + src);
-          st.id[dst] = o;
-          st.r2[dst] = __ldg(r2src + 4 * (size_t)o);  // a field of the LineA at o
-        }
+      return __shfl_sync(0xffffffffu, bse, l & 31) + s;
+    };
+    for (uint32_t sb = 0; sb < T; sb += 64) {  // two slots per lane per step: 64 loads in flight
+      if (filled > kCellBuf - 64) {
+        __syncwarp();
+        eval(filled);
+        filled = 0;
       }
-      filled += (int)n;
+      const uint32_t s0 = sb + (uint32_t)lane, s1 = s0 + 32;
+      const uint32_t src0 = src_of(s0), src1 = src_of(s1);
+      const bool v0 = s0 < T, v1 = s1 < T;
+      float x0 = 0.f, y0 = 0.f, z0 = 0.f, x1 = 0.f, y1 = 0.f, z1 = 0.f, r0 = 0.f, r1 = 0.f;
+      int o0 = 0, o1 = 0;
+      if (v0) {
+        x0 = __ldg(str + src0); y0 = __ldg(str + str_np + src0); z0 = __ldg(str + 2 * (size_t)str_np + src0);
+        if (kEmit) { o0 = relabel ? (int)src0 : __ldg(perm + src0); }
+      }
+      if (v1) {
+        x1 = __ldg(str + src1); y1 = __ldg(str + str_np + src1); z1 = __ldg(str + 2 * (size_t)str_np + src1);
+        if (kEmit) { o1 = relabel ? (int)src1 : __ldg(perm + src1); }
+      }
+      if (kEmit) {
+        if (v0) r0 = __ldg(r2src + 4 * (size_t)o0);  // a field of the LineA at o
+        if (v1) r1 = __ldg(r2src + 4 * (size_t)o1);
+      }
+      if (v0) {
+        st.x[filled + lane] = x0; st.y[filled + lane] = y0; st.z[filled + lane] = z0;
+        if (kEmit) { st.id[filled + lane] = o0; st.r2[filled + lane] = r0; }
+      }
+      if (v1) {
+        st.x[filled + 32 + lane] = x1; st.y[filled + 32 + lane] = y1; st.z[filled + 32 + lane] = z1;
+        if (kEmit) { st.id[filled + 32 + lane] = o1; st.r2[filled + 32 + lane] = r1; }
+      }
+      filled += (int)min(64u, T - sb);
     }
   }
 }

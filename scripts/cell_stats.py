@@ -1,4 +1,6 @@
-"""Diagnostics of the cell sweeps (APML_CELL_STATS=1): counters of one forward per (config, bits)."""
+"""Diagnostics of the cell sweeps: counters of one forward per (config, bits).  Needs a build with
+APML_CELL_DIAG: python -c "from paper_2512_19743_b200.build import build; build(True, defines=['APML_CELL_DIAG=1'])"
+then APML_CELL_STATS=1 python scripts/cell_stats.py C5 C4:4 ..."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
