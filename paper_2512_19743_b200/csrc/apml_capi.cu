@@ -128,6 +128,7 @@ struct apml_ctx {
   // sorted positions from Pass A on; ipperm [B][N] = sorted position of each original pred
   bool relabel = false;
   int* ipperm = nullptr;
+  uint32_t *prank = nullptr, *grank = nullptr;  // rank of each point in its cell
   uint32_t *pkey = nullptr, *gkey = nullptr, *phist = nullptr, *ghist = nullptr, *pstart = nullptr, *gstart = nullptr;
   int *pperm = nullptr, *gperm = nullptr;
   // row-sharded mode
@@ -520,6 +521,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_lossp = k.take<double>(B * ((N + kLossThreads - 1) / kLossThreads));
   size_t o_ipperm = k.take<int>(c->relabel ? B * N : 0);
   size_t o_pkey = k.take<uint32_t>(c->cull ? B * N : 0), o_gkey = k.take<uint32_t>(c->cull ? B * M : 0);
+  size_t o_prank = k.take<uint32_t>(c->cull ? B * N : 0), o_grank = k.take<uint32_t>(c->cull ? B * M : 0);
   size_t o_pstart = k.take<uint32_t>(B * cells1), o_gstart = k.take<uint32_t>(B * cells1);
   size_t o_pperm = k.take<int>(c->cull ? B * c->Np : 0), o_gperm = k.take<int>(c->cull ? B * c->Mp : 0);
   c->bytes = k.off;
@@ -559,6 +561,7 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->bbpart = (float*)(p + o_bbpart);
   c->psb = (float*)(p + o_psb); c->gsb = (float*)(p + o_gsb); c->gsce2 = (float*)(p + o_gsce2); c->tsum = (unsigned*)(p + o_tsum); c->lossp = (double*)(p + o_lossp);
   c->pkey = (uint32_t*)(p + o_pkey); c->gkey = (uint32_t*)(p + o_gkey);
+  c->prank = (uint32_t*)(p + o_prank); c->grank = (uint32_t*)(p + o_grank);
   c->phist = (uint32_t*)(p + o_phist); c->ghist = (uint32_t*)(p + o_ghist);
   c->pstart = (uint32_t*)(p + o_pstart); c->gstart = (uint32_t*)(p + o_gstart);
   c->pperm = (int*)(p + o_pperm); c->gperm = (int*)(p + o_gperm);
@@ -703,15 +706,15 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   }
   k_pair_bbox_part<<<dim3(kBoxParts, B), kBoxThreads, 0, s>>>(pred, N, gt, M, c->bbpart);
   k_pair_bbox_fin<<<B, 32, 0, s>>>(c->bbpart, kBoxParts, c->pbb);
-  k_cell_count<<<dim3((N + 255) / 256, B), 256, 0, s>>>(pred, N, c->pbb, bits, c->pkey, c->phist);
-  k_cell_count<<<dim3((M + 255) / 256, B), 256, 0, s>>>(gt, M, c->pbb, bits, c->gkey, c->ghist);
   const int cells1 = (1 << (3 * bits)) + 1;
+  const CellCloud cp{pred, N, (int)Np, kPadPred, c->pkey, c->phist, c->prank, c->pstart, c->predS, c->pperm,
+                     c->relabel ? c->pred4 : nullptr, c->ipperm};
+  const CellCloud cgt{gt, M, (int)Mp, kPadGt, c->gkey, c->ghist, c->grank, c->gstart, c->gtS, c->gperm,
+                     c->relabel ? c->gt4 : nullptr, nullptr};
+  k_cell_count_both<<<dim3((std::max(N, M) + 255) / 256, B, 2), 256, 0, s>>>(cp, cgt, c->pbb, bits);
   launch_scan(c, scan_job(c->phist, c->pstart, cells1, cells1, c->tsum),
               scan_job(c->ghist, c->gstart, cells1, cells1, c->tsum + (size_t)B * scan_tiles(cells1)));
-  k_cell_scatter<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, bits, c->pkey, c->pstart,
-      c->phist, c->predS, c->pperm, c->relabel ? c->pred4 : nullptr, c->ipperm);
-  k_cell_scatter<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, bits, c->gkey, c->gstart,
-      c->ghist, c->gtS, c->gperm, c->relabel ? c->gt4 : nullptr, nullptr);
+  k_cell_scatter_both<<<dim3((std::max(Np, Mp) + 255) / 256, B, 2), 256, 0, s>>>(cp, cgt, bits);
   if (c->cells) {  // Pass A over the cell grid (k_cells.cuh), both directions in one launch
     const int cw = 32 * kCellWarps;
     const CellDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gstart, c->part_r, c->clamp + 1,
@@ -722,7 +725,7 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
     k_top2_cells<<<dim3(std::max(dr.nblk, dc.nblk), B, 2), cw, 0, s>>>(dr, dc, c->pbb, bits, cells1, (int)c->relabel);
     c->passA_fused = true;
     mark(c, 2, s);
-    c->launches += 8;  // bbox x2, count x2, scatter x2, Pass A (+ the scan's own)
+    c->launches += 5;  // bbox x2, count, scatter, Pass A (+ the scan's own)
     CK(cudaGetLastError());
     return APML_OK;
   }
@@ -760,7 +763,7 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
         c->predS, Np, c->pcb, c->pfb, c->psb, (int)c->relabel, c->part_c, c->clamp + 2);
     c->passA_fused = false;
   }
-  c->launches += 11;  // + the scan's own
+  c->launches += 9;  // + the scan's own
   CK(cudaGetLastError());
   return APML_OK;
 }

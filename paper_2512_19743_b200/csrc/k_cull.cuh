@@ -85,11 +85,11 @@ __device__ __forceinline__ uint32_t cell_axis(float p, float lo, float hi, uint3
   return (uint32_t)fminf(fmaxf(f, 0.f), (float)(G - 1));
 }
 
-// Morton cell key of every point (bits per axis) and the per-pair cell histogram.
-__global__ void k_cell_count(const float* __restrict__ pts, int n, const float* __restrict__ bb, int bits,
-                             uint32_t* __restrict__ key, uint32_t* __restrict__ hist) {
-  const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// Morton cell key of every point (bits per axis), its rank in the cell (returning atomic: the
+// scatter then needs no atomics) and the per-pair cell histogram.
+__device__ void cell_count_body(const float* __restrict__ pts, int n, const float* __restrict__ bb, int bits,
+                                uint32_t* __restrict__ key, uint32_t* __restrict__ hist, uint32_t* __restrict__ rank,
+                                int b, int k) {
   if (k >= n) return;
   const float* p = pts + ((size_t)b * n + k) * 3;
   const float* box = bb + b * 6;
@@ -100,18 +100,40 @@ __global__ void k_cell_count(const float* __restrict__ pts, int n, const float* 
   for (int d = 0; d < 3; ++d) c[d] = cell_axis(p[d], box[d], box[3 + d], cells_axis, &f);
   const uint32_t kk = spread_bits3(c[0]) | (spread_bits3(c[1]) << 1) | (spread_bits3(c[2]) << 2);
   key[(size_t)b * n + k] = kk;
-  atomicAdd(hist + (size_t)b * ((1u << (3 * bits)) + 1) + kk, 1u);
+  rank[(size_t)b * n + k] = atomicAdd(hist + (size_t)b * ((1u << (3 * bits)) + 1) + kk, 1u);
 }
+__global__ void k_cell_count(const float* __restrict__ pts, int n, const float* __restrict__ bb, int bits,
+                             uint32_t* __restrict__ key, uint32_t* __restrict__ hist, uint32_t* __restrict__ rank) {
+  cell_count_body(pts, n, bb, bits, key, hist, rank, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
+}
+
+// Both clouds in one launch each (grid.z = 2: pred, gt).
+struct CellCloud {
+  const float* pts;
+  int n, np;
+  float sentinel;
+  uint32_t *key, *hist, *rank;
+  const uint32_t* start;
+  float* soa;
+  int* perm;
+  float4* p4;
+  int* iperm;
+};
+__device__ void cell_count_body(const float* __restrict__ pts, int n, const float* __restrict__ bb, int bits,
+                                uint32_t* __restrict__ key, uint32_t* __restrict__ hist, uint32_t* __restrict__ rank,
+                                int b, int k);
+__device__ void cell_scatter_body(const float* __restrict__ pts, int n, int np, float sentinel, int bits,
+                                  const uint32_t* __restrict__ key, const uint32_t* __restrict__ start,
+                                  const uint32_t* __restrict__ rank, float* __restrict__ soa, int* __restrict__ perm,
+                                  float4* __restrict__ p4, int* __restrict__ iperm, int b, int k);
 
 // Place every point at its sorted position: SoA coordinates (pads = sentinel) + perm.
 // Relabelled mode (p4 != NULL): also the float4 copy and the inverse permutation (original
 // -> sorted) at sorted positions.
-__global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, float sentinel, int bits,
-                               const uint32_t* __restrict__ key, const uint32_t* __restrict__ start,
-                               uint32_t* __restrict__ fill, float* __restrict__ soa, int* __restrict__ perm,
-                               float4* __restrict__ p4, int* __restrict__ iperm) {
-  const int b = blockIdx.y;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+__device__ void cell_scatter_body(const float* __restrict__ pts, int n, int np, float sentinel, int bits,
+                                  const uint32_t* __restrict__ key, const uint32_t* __restrict__ start,
+                                  const uint32_t* __restrict__ rank, float* __restrict__ soa, int* __restrict__ perm,
+                                  float4* __restrict__ p4, int* __restrict__ iperm, int b, int k) {
   if (k >= np) return;
   float* s = soa + (size_t)b * 3 * np;
   if (k >= n) {  // pads occupy the sorted positions [n, np)
@@ -121,7 +143,7 @@ __global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, flo
   }
   const size_t hb = (size_t)b * ((1u << (3 * bits)) + 1);
   const uint32_t kk = key[(size_t)b * n + k];
-  const uint32_t pos = start[hb + kk] + atomicAdd(fill + hb + kk, 1u);
+  const uint32_t pos = start[hb + kk] + rank[(size_t)b * n + k];
   const float* p = pts + ((size_t)b * n + k) * 3;
   s[pos] = p[0]; s[np + pos] = p[1]; s[2 * np + pos] = p[2];
   perm[(size_t)b * np + pos] = k;
@@ -129,6 +151,22 @@ __global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, flo
     p4[(size_t)b * n + pos] = make_float4(p[0], p[1], p[2], 0.f);
     if (iperm) iperm[(size_t)b * n + k] = (int)pos;
   }
+}
+__global__ void k_cell_scatter(const float* __restrict__ pts, int n, int np, float sentinel, int bits,
+                               const uint32_t* __restrict__ key, const uint32_t* __restrict__ start,
+                               const uint32_t* __restrict__ rank, float* __restrict__ soa, int* __restrict__ perm,
+                               float4* __restrict__ p4, int* __restrict__ iperm) {
+  cell_scatter_body(pts, n, np, sentinel, bits, key, start, rank, soa, perm, p4, iperm, blockIdx.y,
+                    blockIdx.x * blockDim.x + threadIdx.x);
+}
+__global__ void k_cell_count_both(const CellCloud c0, const CellCloud c1, const float* __restrict__ bb, int bits) {
+  const CellCloud& c = blockIdx.z ? c1 : c0;
+  cell_count_body(c.pts, c.n, bb, bits, c.key, c.hist, c.rank, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
+}
+__global__ void k_cell_scatter_both(const CellCloud c0, const CellCloud c1, int bits) {
+  const CellCloud& c = blockIdx.z ? c1 : c0;
+  cell_scatter_body(c.pts, c.n, c.np, c.sentinel, bits, c.key, c.start, c.rank, c.soa, c.perm, c.p4, c.iperm,
+                    blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // Bounding boxes of every kTQ-point tile (cb[b][t]) and of its kSub-point sub-tiles
