@@ -453,7 +453,9 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
       // 1.49 / 1.04, C5 bits 5 / 6 / 7: 0.52 / 0.28 / 0.34.  At most 2^22 cells over the batch
       // (the four cell arrays cost 16 B per cell).
       int bits = std::min(6, std::max(2, (lg - 3) / 2));
-      while (bits > 2 && (B << (3 * bits)) > (1LL << 22)) --bits;
+      // no more cells than points (the cell arrays stay a small part of the per-point memory:
+      // 65536 -> 32 per axis) and at most 2^22 cells over the batch
+      while (bits > 2 && ((1LL << (3 * bits)) > N + M || (B << (3 * bits)) > (1LL << 22))) --bits;
       c->cell_bits = (int)env_long("APML_CELL_BITS", bits);
       c->cell_bits = std::min(7, std::max(1, c->cell_bits));
     } else {

@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--max-n", type=int, default=262144)
     ap.add_argument("--batch", type=int, default=0, help="pairs per call (0 = auto)")
     ap.add_argument("--oracle-max-n", type=int, default=1024)
+    ap.add_argument("--min-n", type=int, default=64)
+    ap.add_argument("--no-write", action="store_true", help="print only (profiles/ untouched)")
     args = ap.parse_args()
 
     import numpy as np
@@ -37,7 +39,7 @@ def main():
 
     dev = torch.device("cuda")
     rows = []
-    n = 64
+    n = args.min_n
     while n <= args.max_n:
         trials = args.trials if n <= 65536 else max(1, args.trials // 10)
         per_call = args.batch or max(1, min(trials, (1 << 24) // (n * n) + 1, 64))
@@ -75,6 +77,8 @@ def main():
                          oracle_max_abs_nnz_diff=check, seconds=el))
         print(rows[-1], flush=True)
         n *= 2
+    if args.no_write:
+        return
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     import csv
     with open(os.path.join(ROOT, "profiles", "fig2_nnz.csv"), "w", newline="") as f:
