@@ -207,11 +207,11 @@ struct LongList {
   __device__ __forceinline__ int line(int k) const { return all ? lo + k : (int)idx[k]; }
 };
 
-__device__ LongList collect_long(const unsigned* ptr, Slice s, uint32_t* list, int* cnt) {
+__device__ LongList collect_long(const unsigned* ptr, Slice s, uint32_t* list, int* cnt, uint32_t th = kRegLine) {
   if (threadIdx.x == 0) *cnt = 0;
   __syncthreads();
   for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x)
-    if (ptr[i + 1] - ptr[i] > kRegLine) {
+    if (ptr[i + 1] - ptr[i] > th) {
       const int k = atomicAdd(cnt, 1);
       if (k < kLongCap) list[k] = (uint32_t)i;
     }
@@ -228,8 +228,8 @@ __device__ LongList collect_long(const unsigned* ptr, Slice s, uint32_t* list, i
        _k < _n; _k += (G == 1 ? (int)blockDim.x : (int)(blockDim.x >> 5)))                         \
     if (const int var = (G == 1 ? (s).lo + _k : (ll).line(_k)); true)
 
-// Warp per line rank sort of the lines longer than kRegLine (keys inside a line are distinct).
-template <bool kRows>
+// Warp per line rank sort of the lines longer than TH (keys inside a line are distinct).
+template <bool kRows, uint32_t TH = kRegLine>
 __device__ void sort_lines(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const size_t pb = (size_t)b * A.cap;
   const int n = kRows ? A.N : A.M;
@@ -240,7 +240,7 @@ __device__ void sort_lines(const SparseArgs& A, int b, Slice s, const LongList& 
   (void)nw;
   APML_FOR_LINES(32, s, ll, line) {
     const uint32_t beg = ptr[line], end = ptr[line + 1], L = end - beg;
-    if (L <= kRegLine) continue;
+    if (L <= TH) continue;
     auto key_of = [&](uint32_t t) -> uint32_t {  // ORIGINAL index of the other cloud
       return kRows ? orig_col(A, b, e[t].y & kIdxMask) : orig_row(A, b, e[t].x);
     };
@@ -297,6 +297,7 @@ __device__ __forceinline__ void first_two(unsigned bal_m, unsigned bal_s, int& k
 
 // Row softmax on the kept support for rows longer than kRegLine: one warp per row, 32
 // entries per step (the short rows are done in registers by row_sort_norm_regs).
+template <uint32_t TH = kRegLine>
 __device__ void row_norm(const SparseArgs& A, int b, Slice s, const LongList& ll) {
   const int N = A.N, M = A.M;
   const size_t pb = (size_t)b * A.cap;
@@ -304,7 +305,7 @@ __device__ void row_norm(const SparseArgs& A, int b, Slice s, const LongList& ll
   const int lane = threadIdx.x & 31;
   APML_FOR_LINES(32, s, ll, i) {
     const uint32_t beg = rp[i], end = rp[i + 1];
-    if (end - beg <= kRegLine) continue;
+    if (end - beg <= TH) continue;
     const float4 x = A.pred4[(size_t)b * N + i];
     const LineA la = A.rowA[(size_t)b * N + i];
     const LineB lb = A.rowB[(size_t)b * N + i];
@@ -395,41 +396,42 @@ __device__ void col_norm(const SparseArgs& A, int b, Slice s, const LongList& ll
 //           first matches, R12).
 
 // Row softmax on the kept support (S5) + CSR order by j.
+template <uint32_t TH = kRegLine>
 __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
   const int N = A.N, M = A.M;
   const size_t pb = (size_t)b * A.cap;
   const unsigned* rp = A.row_ptr + (size_t)b * (N + 1);
   for (int i = s.lo + threadIdx.x; i < s.hi; i += blockDim.x) {
     const uint32_t beg = rp[i], L = rp[i + 1] - beg;
-    if (L > kRegLine) continue;
+    if (L > TH) continue;
     const float4 x = A.pred4[(size_t)b * N + i];
     const LineA la = A.rowA[(size_t)b * N + i];
     const LineB lb = A.rowB[(size_t)b * N + i];
     {
-      uint32_t t[kRegLine], jf[kRegLine], ok[kRegLine];
+      uint32_t t[TH], jf[TH], ok[TH];
 #pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
+      for (uint32_t k = 0; k < TH; ++k) t[k] = k < L ? A.csr_t[pb + beg + k] : 0u;
 #pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) jf[k] = k < L ? ebuf_of(A, b)[t[k]].y : 0u;
+      for (uint32_t k = 0; k < TH; ++k) jf[k] = k < L ? ebuf_of(A, b)[t[k]].y : 0u;
 #pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) ok[k] = k < L ? orig_col(A, b, jf[k] & kIdxMask) : 0xffffffffu;
+      for (uint32_t k = 0; k < TH; ++k) ok[k] = k < L ? orig_col(A, b, jf[k] & kIdxMask) : 0xffffffffu;
 #pragma unroll
-      for (uint32_t k = 0; k < kRegLine; ++k) {
+      for (uint32_t k = 0; k < TH; ++k) {
         uint32_t r = 0;
 #pragma unroll
-        for (uint32_t f = 0; f < kRegLine; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
+        for (uint32_t f = 0; f < TH; ++f) r += (ok[f] < ok[k]) ? 1u : 0u;
         if (k < L) {  // padded entries (key = ~0) never precede a real key
           A.csr_jf[pb + beg + r] = jf[k];
           A.inv[pb + t[k]] = beg + r;
         }
       }
     }
-    uint32_t sj[kRegLine];
+    uint32_t sj[TH];
 #pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) sj[r] = r < L ? A.csr_jf[pb + beg + r] : 0u;
-    float d2v[kRegLine], cv[kRegLine];
+    for (uint32_t r = 0; r < TH; ++r) sj[r] = r < L ? A.csr_jf[pb + beg + r] : 0u;
+    float d2v[TH], cv[TH];
 #pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) {
+    for (uint32_t r = 0; r < TH; ++r) {
       if (r < L) {
         const float4 y = A.gt4[(size_t)b * M + (sj[r] & kIdxMask)];
         d2v[r] = dist2(x.x, x.y, x.z, y.x, y.y, y.z);
@@ -439,7 +441,7 @@ __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
     int ia = -1, ib = -1;
     float Z = 0.f;
 #pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r) {
+    for (uint32_t r = 0; r < TH; ++r) {
       if (r < L) {
         const int j = (int)(sj[r] & kIdxMask);
         if (ia < 0 && d2v[r] == la.m2) ia = j;
@@ -456,7 +458,7 @@ __device__ void row_sort_norm_regs(const SparseArgs& A, int b, Slice s) {
     }
     const float iz = 1.f / Z;
 #pragma unroll
-    for (uint32_t r = 0; r < kRegLine; ++r)
+    for (uint32_t r = 0; r < TH; ++r)
       if (r < L) A.prow[pb + beg + r] = cv[r] * iz;
     A.rowidx[(size_t)b * N + i] = make_int2(ia, ib);
   }

@@ -172,23 +172,53 @@ __device__ __forceinline__ Slice block_slice(int n) {
 }
 
 // Rows: sort by j + row softmax (everything row-local).
-__global__ void __launch_bounds__(kRsThreads) k_rs_rows(const SparseArgs A) {
+__global__ void __launch_bounds__(kRsThreads, 2) k_rs_rows(const SparseArgs A) {
   __shared__ uint32_t s_long[kLongCap];
   __shared__ int s_n;
   const int b = blockIdx.y;
   if (A.cursor[b] > A.cap) return;
   const Slice s = block_slice(A.N);
-  const LongList ll = collect_long(A.row_ptr + (size_t)b * (A.N + 1), s, s_long, &s_n);
-  row_sort_norm_regs(A, b, s);
+  // rows of up to 8 entries by a thread in registers (64 registers: two CTAs per SM), longer
+  // ones by a warp (C4 / C5: ~4 entries per row)
+  constexpr uint32_t kTh = 8;
+  const LongList ll = collect_long(A.row_ptr + (size_t)b * (A.N + 1), s, s_long, &s_n, kTh);
+  row_sort_norm_regs<kTh>(A, b, s);
   __syncthreads();
-  sort_lines<true>(A, b, s, ll);
+  sort_lines<true, kTh>(A, b, s, ll);
   __syncthreads();
-  row_norm(A, b, s, ll);
+  row_norm<kTh>(A, b, s, ll);
 }
 
 // Columns, pass 1: sort by i; partial column-softmax sum over this rank's entries and this
 // rank's argmin / second-argmin candidates (global row indices, or -1):
 //   cand = {first entry with d2 == m2, second entry with d2 == m2, first entry with d2 == s2}.
+// CSC order of one short column by ORIGINAL row index (R12): csc_i and the CSR position of each
+// entry (csc_perm), from the unsorted emit ids of the column (csc_t).
+template <uint32_t KR>
+__device__ __forceinline__ void col_rank_sort(const SparseArgs& A, int b, uint32_t beg, uint32_t L) {
+  const size_t pb = (size_t)b * A.cap;
+  uint32_t t[KR], ex[KR], key[KR], pp[KR];
+#pragma unroll
+  for (uint32_t k = 0; k < KR; ++k) t[k] = k < L ? A.csc_t[pb + beg + k] : 0u;
+#pragma unroll
+  for (uint32_t k = 0; k < KR; ++k) {
+    ex[k] = k < L ? ebuf_of(A, b)[t[k]].x : 0u;
+    pp[k] = k < L ? A.inv[pb + t[k]] : 0u;
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < KR; ++k) key[k] = k < L ? orig_row(A, b, ex[k]) : 0xffffffffu;
+#pragma unroll
+  for (uint32_t k = 0; k < KR; ++k) {
+    uint32_t r = 0;
+#pragma unroll
+    for (uint32_t f = 0; f < KR; ++f) r += (key[f] < key[k]) ? 1u : 0u;
+    if (k < L) {
+      A.csc_i[pb + beg + r] = ex[k];
+      A.csc_perm[pb + beg + r] = pp[k];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
   __shared__ uint32_t s_long[kLongCap];
   __shared__ int s_n;
@@ -202,23 +232,10 @@ __global__ void __launch_bounds__(kRsThreads) k_rs_cols_a(const SparseArgs A) {
   for (int j = s.lo + threadIdx.x; j < s.hi; j += blockDim.x) {
     const uint32_t beg = cp[j], end = cp[j + 1];
     if (end - beg > kRegLine) continue;
-    // insertion sort by i of the (t) ids, in place in csc_t (short column, thread-private)
-    const size_t pb = (size_t)b * A.cap;
-    for (uint32_t q = beg + 1; q < end; ++q) {
-      const uint32_t t = A.csc_t[pb + q];
-      const uint32_t key = orig_row(A, b, ebuf_of(A, b)[t].x);
-      uint32_t r = q;
-      while (r > beg && orig_row(A, b, ebuf_of(A, b)[A.csc_t[pb + r - 1]].x) > key) {
-        A.csc_t[pb + r] = A.csc_t[pb + r - 1];
-        --r;
-      }
-      A.csc_t[pb + r] = t;
-    }
-    for (uint32_t q = beg; q < end; ++q) {
-      const uint32_t t = A.csc_t[pb + q];
-      A.csc_i[pb + q] = ebuf_of(A, b)[t].x;
-      A.csc_perm[pb + q] = A.inv[pb + t];
-    }
+    // rank sort by (original) i in registers (all loads of the column in flight at once; an
+    // in-place insertion sort through global memory chained two dependent loads per step)
+    if (end - beg <= 8) col_rank_sort<8>(A, b, beg, end - beg);
+    else col_rank_sort<kRegLine>(A, b, beg, end - beg);
   }
   __syncthreads();
   sort_lines<false>(A, b, s, ll);
@@ -740,7 +757,7 @@ __global__ void k_rs_col_soft_fin(const SparseArgs A) {
   A.colback[(size_t)b * M + j] = out;
 }
 
-__global__ void __launch_bounds__(kRsThreads) k_rs_grad(const SparseArgs A) {
+__global__ void __launch_bounds__(kRsThreads, 2) k_rs_grad(const SparseArgs A) {
   __shared__ uint32_t s_long[kLongCap];
   __shared__ int s_n;
   const int b = blockIdx.y;
