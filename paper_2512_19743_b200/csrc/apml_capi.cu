@@ -719,6 +719,12 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
   k_cell_scatter_both<<<dim3((std::max(Np, Mp) + 255) / 256, B, 2), 256, 0, s>>>(cp, cgt, bits);
   if (c->cells) {  // Pass A over the cell grid (k_cells.cuh), both directions in one launch
     const int cw = 32 * kCellWarps;
+    static long maxblock = -1;
+    if (maxblock < 0) {
+      maxblock = env_long("APML_CELL_MAXBLOCK", kCellMaxBlock);
+      const int v = (int)maxblock;
+      CK(cudaMemcpyToSymbol(g_cell_maxblock, &v, sizeof v));
+    }
     const CellDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gstart, c->part_r, c->clamp + 1,
                      (int)((Np + cw - 1) / cw)};
     const CellDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pstart, c->part_c, c->clamp + 2,

@@ -31,6 +31,7 @@ namespace apml {
 constexpr int kCellWarps = 4;        // warps per CTA (independent; no CTA barrier)
 constexpr int kCellBuf = 256;        // staged points per warp
 constexpr int kCellMaxBlock = 216;   // largest grown warp box (cells) scanned for all lanes at once
+__constant__ int g_cell_maxblock = kCellMaxBlock;  // (tuning: APML_CELL_MAXBLOCK)
 
 struct CellBox {
   int lo[3], hi[3];
@@ -303,7 +304,7 @@ __device__ __forceinline__ void for_groups(const CellOwn& o, unsigned lanes, con
       const unsigned m = seg & ~done;
       if (!m) continue;
       const CellBox W = unite(m);
-      if (box_cells(W) <= kCellMaxBlock || len == 1) {
+      if (box_cells(W) <= g_cell_maxblock || len == 1) {
         body(m, W);
         done |= m;
       }
