@@ -528,7 +528,8 @@ def main():
     alu_peak = sms * 128 * f_max / 1e12  # FP32 lane-ops/s (FMA = 1), DESIGN.md "Roofline"
     dist_stages = ("passA_rows", "passA_cols", "emit")
     # algorithmic (i, j) evaluations per sweep on this rank: B N M for the full sweeps; the
-    # spatially culled sweeps (C4, C5) count on the device the 32 x 32 blocks they evaluate
+    # spatially culled sweeps (C4, C5) count on the device the (own point, other point) pairs they
+    # evaluate (k_cells.cuh: staged points x active lanes; the tile walk: 32 x 32 blocks)
     # (apml_stats.sweep_evals), capped at B N M
     full_evals = B * pred.shape[1] * M if ns is None else int(sum(a * b for a, b in zip(ns, ms)))
     evals_by = {k: min(int(e), full_evals) for k, e in zip(dist_stages, st0["sweep_evals"])}
@@ -567,7 +568,9 @@ def main():
                  f"FFMA {fp32_meas.get('ffma_lane_tops', 0):.1f} T lane-op/s")
     if dom in dist_stages:
         ach = LANE_OPS_PER_EVAL * alg_by[dom] / (med[dom] / 1e3) / 1e12
-        kname = ("k_line_top2_cull/k_emit_cull" if culled else "k_line_top2/k_emit") + f" ({dom})"
+        cells = os.environ.get("APML_CULL_MODE", "1") != "0"
+        kname = (("k_top2_cells/k_emit_cells" if cells else "k_line_top2_cull/k_emit_cull") if culled
+                 else "k_line_top2/k_emit") + f" ({dom})"
         roof = {"bound": "alu", "kernel": kname, "achieved": ach, "peak": alu_peak,
                 "unit": "TFLOP/s", "frac": ach / alu_peak, "traffic": traffic, "evals": alg_by[dom],
                 "executed_evals": evals_by[dom],

@@ -74,8 +74,8 @@ def main():
         for d in raw(rep):
             k = d["kernel"].split("(")[0].replace("void ", "")
             lines.append(f"| {k} | " + " | ".join(f"{d.get(x, ''):.4g}" if isinstance(d.get(x), float) else str(d.get(x, "")) for x in keys) + " |")
-            stage = {"k_line_top2": "passA_rows", "k_emit": "emit", "k_sparse_fwd": "sparse_fwd",
-                     "k_sparse_bwd": "sparse_bwd"}
+            stage = {"k_line_top2": "passA_rows", "k_top2_cells": "passA_rows", "k_emit": "emit",
+                     "k_sparse_fwd": "sparse_fwd", "k_sparse_bwd": "sparse_bwd"}
             for pre, st in stage.items():
                 if pre in k and isinstance(d.get("dram_read"), float):
                     traffic.setdefault(cfg, {})[st] = d["dram_read"] + d.get("dram_write", 0.0)
