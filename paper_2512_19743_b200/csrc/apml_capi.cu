@@ -113,6 +113,7 @@ struct apml_ctx {
   float* lr_d = nullptr;
   float lam_r = 0, lam_c = 0, rho_r = 0, rho_c = 0;
   // spatially culled sweeps (k_cull.cuh)
+  float *colR2s = nullptr, *colE2s = nullptr;  // column radii SoA [B][Mp] (full-sweep emit)
   bool cull = false;
   bool cells = false;     // culled sweeps over the Morton cell grid (k_cells.cuh), else the tile walk
   int cell_bits = 0;
@@ -485,6 +486,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   size_t o_part_c = k.take<float2>(parts_c);
   size_t o_rowA = k.take<LineA>(B * N), o_colA = k.take<LineA>(B * M);
   size_t o_rowB = k.take<LineB>(B * N), o_colB = k.take<LineB>(B * M);
+  // SoA copies of the column radii for the full-sweep emit's tile copies (pads: NaN, never a hit)
+  size_t o_cR2 = k.take<float>(c->cull ? 0 : B * c->Mp), o_cE2 = k.take<float>(c->cull ? 0 : B * c->Mp);
   const int64_t cells1 = c->cull ? ((int64_t)1 << (3 * c->cell_bits)) + 1 : 0;
   // counters in one contiguous zeroed block
   size_t z0 = k.off;
@@ -539,6 +542,11 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   c->part_r = (float2*)(p + o_part_r); c->part_c = (float2*)(p + o_part_c);
   c->rowA = (LineA*)(p + o_rowA); c->colA = (LineA*)(p + o_colA);
   c->rowB = (LineB*)(p + o_rowB); c->colB = (LineB*)(p + o_colB);
+  if (!c->cull) {
+    c->colR2s = (float*)(p + o_cR2);
+    c->colE2s = (float*)(p + o_cE2);
+    CK(cudaMemsetAsync(c->colR2s, 0xff, 2 * sizeof(float) * (size_t)(o_cE2 - o_cR2) / sizeof(float), c->stream));
+  }
   c->clamp = (unsigned long long*)(p + o_clamp);
   c->icnt = (unsigned*)(p + o_icnt);
   c->cursor = (unsigned*)(p + o_cursor); c->aux = (unsigned*)(p + o_aux);
@@ -853,7 +861,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     const Top2Dir dc{c->gtS, (int)Mp, c->predS, (int)Np, c->chunk_cols, c->S_cols, (int)(Mp / kOwnTile),
                      c->part_c, c->mb_d, c->nb_d};
     const LineInfoDir lr_{c->part_r, c->S_rows, (int)Np, N, M, c->lam_r, c->rho_r, c->rowA, c->rowB, c->nb_d, c->mb_d, 0};
-    const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2};
+    const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2,
+                          c->colR2s, c->colE2s, (int)Mp};
     const dim3 ga(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B);
     if (env_long("APML_FUSE_INFO", 1) != 0) {  // S2 in the last CTA of every row block
       const FusedInfo fi{{lr_, lc_}, c->cfg.delta, c->cfg.eps_g, c->clamp, (const float*)c->lr_d, ufb(c), c->icnt,
@@ -878,7 +887,8 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
   CK(launch_pdl(k_emit<kR>, dim3(Np / kOwnTile, c->S_emit, B), dim3(kSweepThreads), 0, s, 0,
                 (const float*)c->predS, Np, N, (const LineA*)c->rowA, (const float*)c->gtS, Mp, M,
                 (const LineA*)c->colA, c->chunk_emit, c->cap_e, c->ebuf, c->cursor, c->aux, c->row_cnt,
-                c->col_cnt, (const int*)c->nb_d, (const int*)c->mb_d));
+                c->col_cnt, (const int*)c->nb_d, (const int*)c->mb_d, (const float*)c->colR2s,
+                (const float*)c->colE2s));
   mark(c, 5, s);
   c->launches += 4;
   CK(cudaGetLastError());
@@ -968,14 +978,15 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
     k_line_info<<<dim3((N + 255) / 256, B), 256, 0, s>>>(c->part_r, c->S_rows, B, Np, N, M, c->lam_r,
         c->rho_r, c->cfg.delta, c->cfg.eps_g, c->rowA, c->rowB, c->clamp, c->nb_d, c->mb_d, c->lr_d, 0, ufb(c));
   k_line_info<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->gath, c->comm.world, B, M, M, (int)c->N_global,
-      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2, ufb(c));
+      c->lam_c, c->rho_c, c->cfg.delta, c->cfg.eps_g, c->colA, c->colB, c->clamp, c->mb_d, c->nb_d, c->lr_d, 2, ufb(c),
+      c->colR2s, c->colE2s, (int)Mp);
   mark(c, 4, s);
   if (c->cull) {
     if ((st = launch_emit_cull(c)) != APML_OK) return st;
   } else {
     k_emit<kR><<<dim3(Np / kOwnTile, c->S_rows, B), kSweepThreads, 0, s>>>(
         c->predS, Np, N, c->rowA, c->gtS, Mp, M, c->colA, c->chunk_rows, c->cap_e, c->ebuf, c->cursor,
-        c->aux, c->row_cnt, c->col_cnt, nullptr, nullptr);
+        c->aux, c->row_cnt, c->col_cnt, nullptr, nullptr, (const float*)c->colR2s, (const float*)c->colE2s);
   }
   mark(c, 5, s);
   c->launches += 5;

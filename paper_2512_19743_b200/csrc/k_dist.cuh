@@ -114,6 +114,42 @@ __device__ __forceinline__ void ring_wait(TileRing& r, int k, uint32_t parity) {
                  : "memory");
 }
 
+// The emit's ring: the streamed coordinates AND the streamed columns' radii (R'^2, E'^2: SoA
+// copies written by line_info) per tile, five bulk copies completing on one mbarrier.
+struct TileRing5 {
+  float v[2][5][kTQ];
+  unsigned long long bar[2];
+};
+__device__ __forceinline__ void ring5_init(TileRing5& r) {
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sptr(&r.bar[k])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void ring5_issue(TileRing5& r, int k, const float* __restrict__ str, int str_np,
+                                            const float* __restrict__ R2s, const float* __restrict__ E2s, int j0) {
+  const uint32_t bar = sptr(&r.bar[k]);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(5u * kTQ * 4u) : "memory");
+  const float* src[5] = {str + j0, str + (size_t)str_np + j0, str + 2 * (size_t)str_np + j0, R2s + j0, E2s + j0};
+#pragma unroll
+  for (int c = 0; c < 5; ++c)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sptr(&r.v[k][c][0])),
+                 "l"(src[c]), "r"(kTQ * 4u), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void ring5_wait(TileRing5& r, int k, uint32_t parity) {
+  const uint32_t bar = sptr(&r.bar[k]);
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(bar), "r"(parity)
+                 : "memory");
+}
+
 // Load one kTQ-point tile of the streamed cloud (SoA) into shared memory.
 __device__ __forceinline__ void load_tile(const float* __restrict__ str, int str_np, int j0,
                                           float* sx, float* sy, float* sz) {
@@ -236,13 +272,16 @@ __device__ __forceinline__ void line_info(const float2* __restrict__ part, int S
                                           LineA* __restrict__ A, LineB* __restrict__ Bo,
                                           unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
                                           const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off,
-                                          int b, int k, int ufb) {
+                                          int b, int k, int ufb, float* __restrict__ R2s = nullptr,
+                                          float* __restrict__ E2s = nullptr, int re_np = 0) {
+  // R2s / E2s (or NULL): SoA copies of the radii at [b][re_np] for the emit's tile copies
   if (k >= n) return;
   if (nown) {
     if (k >= nown[b]) {
       const float inf = __int_as_float(0x7f800000);
       A[(size_t)b * n + k] = LineA{inf, inf, -1.f, -1.f};
       Bo[(size_t)b * n + k] = LineB{0.f, 0.f, 0.f, 0};
+      if (R2s) { R2s[(size_t)b * re_np + k] = -1.f; E2s[(size_t)b * re_np + k] = -1.f; }
       return;
     }
     K = kpair[b];
@@ -286,15 +325,17 @@ __device__ __forceinline__ void line_info(const float2* __restrict__ part, int S
   }
   A[(size_t)b * n + k] = a;
   Bo[(size_t)b * n + k] = o;
+  if (R2s) { R2s[(size_t)b * re_np + k] = a.R2; E2s[(size_t)b * re_np + k] = a.E2; }
 }
 
 __global__ void k_line_info(const float2* __restrict__ part, int S, int B, int own_np, int n,
                             int K, float lam, float rho, float delta, float eps_g,
                             LineA* __restrict__ A, LineB* __restrict__ Bo,
                             unsigned long long* __restrict__ clamp_count, const int* __restrict__ nown,
-                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off, int ufb) {
+                            const int* __restrict__ kpair, const float* __restrict__ lr, int lr_off, int ufb,
+                            float* __restrict__ R2s = nullptr, float* __restrict__ E2s = nullptr, int re_np = 0) {
   line_info(part, S, B, own_np, n, K, lam, rho, delta, eps_g, A, Bo, clamp_count, nown, kpair, lr, lr_off,
-            blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb);
+            blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb, R2s, E2s, re_np);
 }
 
 // Rows and columns in ONE launch (grid.z = 2: rows, columns; grid.y = pair).
@@ -307,6 +348,9 @@ struct LineInfoDir {
   const int* nown;
   const int* kpair;
   int lr_off;
+  float* R2s = nullptr;  // SoA radii copies (columns of the full sweeps: the emit's tile copies)
+  float* E2s = nullptr;
+  int re_np = 0;         // their per-pair stride
 };
 __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int B, float delta, float eps_g,
                                  unsigned long long* __restrict__ clamp_count, const float* __restrict__ lr, int ufb) {
@@ -314,7 +358,7 @@ __global__ void k_line_info_both(const LineInfoDir d0, const LineInfoDir d1, int
   pdl_wait();  // Pass A's partials
   const LineInfoDir& d = blockIdx.z ? d1 : d0;
   line_info(d.part, d.S, B, d.own_np, d.n, d.K, d.lam, d.rho, delta, eps_g, d.A, d.Bo, clamp_count, d.nown,
-            d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb);
+            d.kpair, lr, d.lr_off, blockIdx.y, blockIdx.x * blockDim.x + threadIdx.x, ufb, d.R2s, d.E2s, d.re_np);
 }
 
 // Pass A with S2 fused (the full sweeps): every CTA of a (direction, pair, row block) writes
@@ -350,7 +394,7 @@ __global__ void __launch_bounds__(kSweepThreads) k_line_top2_info(const Top2Dir 
   const LineInfoDir& L = fi.li[dir];
   for (int k = threadIdx.x; k < kSweepThreads * R; k += blockDim.x)
     line_info(L.part, L.S, B, L.own_np, L.n, L.K, L.lam, L.rho, fi.delta, fi.eps_g, L.A, L.Bo, fi.clamp, L.nown,
-              L.kpair, fi.lr, L.lr_off, b, (int)blockIdx.x * kSweepThreads * R + k, fi.ufb);
+              L.kpair, fi.lr, L.lr_off, b, (int)blockIdx.x * kSweepThreads * R + k, fi.ufb, L.R2s, L.E2s, L.re_np);
 }
 
 // Emission (S3).  Counts keep running past the capacity so the host can size a retry;
@@ -405,7 +449,8 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
        const float* __restrict__ gt_soa, int mp, int M, const LineA* __restrict__ colA,
        int chunk, uint32_t cap, uint2* __restrict__ ebuf, unsigned* __restrict__ cursor,
        unsigned* __restrict__ aux_cnt, unsigned* __restrict__ row_cnt,
-       unsigned* __restrict__ col_cnt, const int* __restrict__ nb, const int* __restrict__ mb) {
+       unsigned* __restrict__ col_cnt, const int* __restrict__ nb, const int* __restrict__ mb,
+       const float* __restrict__ colR2s, const float* __restrict__ colE2s) {
   const int b = blockIdx.z, split = blockIdx.y;
   const uint32_t nreal = nb ? (uint32_t)nb[b] : (uint32_t)N, mreal = mb ? (uint32_t)mb[b] : (uint32_t)M;
   if ((uint32_t)(blockIdx.x * kSweepThreads * R) >= nreal) return;  // a block of padding rows
@@ -416,11 +461,12 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
   const float* str = gt_soa + (size_t)b * 3 * mp;
   const int base = blockIdx.x * kSweepThreads * R + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __shared__ __align__(128) TileRing ring;  // streamed coordinates (TMA bulk copies)
-  __shared__ __align__(16) float sR[kTQ], sE[kTQ];
+  __shared__ __align__(128) TileRing5 ring;  // streamed coordinates + column radii (TMA bulk copies)
   __shared__ uint2 queue_all[kSweepThreads / 32][kLaneQ][32];  // [warp][slot][lane]: conflict-free
   uint2* q = &queue_all[w][0][lane];
   int qn = 0;  // this lane's queued entries
+  const float* cR2 = colR2s + (size_t)b * mp;
+  const float* cE2 = colE2s + (size_t)b * mp;
 
   f2_t nx[R], ny[R], nz[R];
   float rR2[R], rE2[R];
@@ -437,30 +483,20 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
     }
   }
   const int j0 = split * chunk, j1 = min(str_end, j0 + chunk);
-  ring_init(ring);
+  ring5_init(ring);
   if (threadIdx.x == 0) {
-    if (j0 < j1) ring_issue(ring, 0, str, mp, j0);
-    if (j0 + kTQ < j1) ring_issue(ring, 1, str, mp, j0 + kTQ);
+    if (j0 < j1) ring5_issue(ring, 0, str, mp, cR2, cE2, j0);
+    if (j0 + kTQ < j1) ring5_issue(ring, 1, str, mp, cR2, cE2, j0 + kTQ);
   }
   int tix = 0;
   for (int jt = j0; jt < j1; jt += kTQ, ++tix) {
     const int slot = tix & 1;
-    __syncthreads();  // every warp left the previous tile: its slot takes the tile after this one
-    if (tix > 0 && threadIdx.x == 0 && jt + kTQ < j1) ring_issue(ring, slot ^ 1, str, mp, jt + kTQ);
+    ring5_wait(ring, slot, (uint32_t)(tix >> 1) & 1u);
     const float* sx = ring.v[slot][0];
     const float* sy = ring.v[slot][1];
     const float* sz = ring.v[slot][2];
-    for (int t = threadIdx.x; t < kTQ; t += kSweepThreads) {
-      const int j = jt + t;
-      if (j < M) {
-        const LineA a = colA[(size_t)b * M + j];
-        sR[t] = a.R2; sE[t] = a.E2;
-      } else {
-        sR[t] = -1.f; sE[t] = -1.f;
-      }
-    }
-    __syncthreads();
-    ring_wait(ring, slot, (uint32_t)(tix >> 1) & 1u);
+    const float* sR = ring.v[slot][3];
+    const float* sE = ring.v[slot][4];
     const ulonglong2* px = reinterpret_cast<const ulonglong2*>(sx);
     const ulonglong2* py = reinterpret_cast<const ulonglong2*>(sy);
     const ulonglong2* pz = reinterpret_cast<const ulonglong2*>(sz);
@@ -525,6 +561,10 @@ k_emit(const float* __restrict__ pred_soa, int np, int N, const LineA* __restric
           }
         }
       }
+    }
+    if (jt + 2 * kTQ < j1) {  // slot refilled with the tile after next once every warp left it
+      __syncthreads();
+      if (threadIdx.x == 0) ring5_issue(ring, slot, str, mp, cR2, cE2, jt + 2 * kTQ);
     }
   }
   __syncwarp();
