@@ -275,6 +275,23 @@ def test_full_size_C4_pcn_sampled():
     _full_size("shapenet", 64, 16384, 16384, [0, 63], seed=300)
 
 
+@pytest.mark.parametrize("kind,N,M,bits", [("uniform", 8192, 6000, ""), ("uniform", 5000, 5000, "6"),
+                                             ("scene", 12000, 9000, ""), ("mmfi", 4096, 4096, "5")])
+def test_cell_sweeps_whole_pair(kind, N, M, bits, monkeypatch):
+    """The cell-grid culled sweeps (k_cells.cuh; the default for min(N, M) >= 4096) on volume
+    data (Fig. 2's uniform clouds: Pass A shells and coarse far scans), surface scenes and
+    human-pose clouds, unequal sizes, default and forced cell sizes: the whole per-pair bar
+    against the oracle (support set and flags outside the band, line statistics, P0, v, loss,
+    gradient)."""
+    Config, _ = _gpu()
+    if bits:
+        monkeypatch.setenv("APML_CELL_BITS", bits)
+    x, y = clouds.batch(kind, 1, N, M, 41)
+    cfg = Config()
+    lg, gg, ctx = _run(x, y, cfg)
+    _check_pair(x, y, cfg, lg, gg, ctx, 0)
+
+
 def test_full_size_C5_scene_sampled_lines():
     """configs[4] on one GPU: B = 1, N = M = 262144 (culled sweeps, Morton relabelling, grid
     sparse stage), in bench.py's launch configuration.  The whole oracle is out of reach here
