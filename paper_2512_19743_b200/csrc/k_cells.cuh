@@ -44,6 +44,19 @@ struct CellBox {
 #define APML_CELL_DIAG 0
 #endif
 __device__ unsigned long long g_cell_stats[16];
+// Bounds checks of the cell kernels (a build with -DAPML_CELL_CHECKS=1; compute-sanitizer is
+// not available on the GPU pool): every staged slot, sorted position, cell key, queue slot and
+// output index is checked, a violation traps the kernel (the test then fails loudly).
+#ifndef APML_CELL_CHECKS
+#define APML_CELL_CHECKS 0
+#endif
+#define CELL_CHECK(cond)                                                                        \
+  do {                                                                                          \
+    if (APML_CELL_CHECKS && !(cond)) {                                                          \
+      printf("apml cell check failed: %s (%s:%d)\n", #cond, __FILE__, __LINE__);              \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
 __device__ __forceinline__ void cell_stat(int k, unsigned long long v) {
   if (APML_CELL_DIAG && (threadIdx.x & 31) == 0 && v) atomicAdd(&g_cell_stats[k], v);
 }
@@ -139,8 +152,10 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
                         iz >= S->lo[2] && iz <= S->hi[2];
       if (!skip) {
         const uint32_t key = morton3((uint32_t)ix, (uint32_t)iy, (uint32_t)iz);
+        CELL_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && ix < 1024 && iy < 1024 && iz < 1024);
         cst = __ldg(start + key);
         cnt = __ldg(start + key + 1);
+        CELL_CHECK(cnt >= cst && cnt <= (uint32_t)str_np);
       }
     }
   };
@@ -179,6 +194,8 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
       const bool v0 = s0 < T, v1 = s1 < T;
       float x0 = 0.f, y0 = 0.f, z0 = 0.f, x1 = 0.f, y1 = 0.f, z1 = 0.f, r0 = 0.f, r1 = 0.f;
       int o0 = 0, o1 = 0;
+      CELL_CHECK(!v0 || (src0 < (uint32_t)str_np && filled + lane < kCellBuf));
+      CELL_CHECK(!v1 || (src1 < (uint32_t)str_np && filled + 32 + lane < kCellBuf));
       if (v0) {
         x0 = __ldg(str + src0); y0 = __ldg(str + str_np + src0); z0 = __ldg(str + 2 * (size_t)str_np + src0);
         if (kEmit) { o0 = relabel ? (int)src0 : __ldg(perm + src0); }
@@ -363,8 +380,10 @@ __device__ __forceinline__ void far_scan(const CellFrame& F, int bits, const uin
       keep = all || d2 * (1.0f - 1e-5f) <= r2;
       if (keep) {
         const uint32_t key = morton3((uint32_t)c[0], (uint32_t)c[1], (uint32_t)c[2]);
+        CELL_CHECK(((key + 1) << sh) <= (1u << (3 * bits)));
         a0 = __ldg(start + (key << sh));
         a1 = __ldg(start + ((key + 1) << sh));
+        CELL_CHECK(a1 >= a0);
         keep = a1 > a0;
       }
     }
@@ -488,6 +507,7 @@ __device__ __forceinline__ void top2_cells_warp(const CellDir& d, const float* b
     }
     if (lane == l) { m = fm; s = fs; }
   }
+  CELL_CHECK(!o.valid || relabel || (d.own_perm[(size_t)b * d.own_np + k] >= 0 && d.own_perm[(size_t)b * d.own_np + k] < d.own_n));
   if (o.valid) d.out[(size_t)b * d.own_n + (relabel ? k : d.own_perm[(size_t)b * d.own_np + k])] = make_float2(m, s);
   nev += __reduce_add_sync(0xffffffffu, (unsigned)min(nfar, 0xffffffffull));
   if (d.evals && lane == 0 && nev) atomicAdd(d.evals, nev);
@@ -568,6 +588,7 @@ __device__ __forceinline__ void emit_cells_warp(const CellEmitDir& d, int dir, c
   const unsigned near = __ballot_sync(0xffffffffu, active && ok);
   unsigned far = __ballot_sync(0xffffffffu, active && !ok);
   auto queue_hit = [&](int j, float d2, float r2o) {  // (r2o: the other point's R'^2, row pass)
+    CELL_CHECK(qn < kLaneQ && j >= 0 && j < (dir ? N : M) && oi >= 0 && oi < (dir ? M : N));
     if (dir == 0) {
       const uint32_t fl = (d2 <= oR2 ? kFlagRow : 0u) | (d2 <= r2o ? kFlagCol : 0u);
       qp[qn * 32] = make_uint2((uint32_t)oi, (uint32_t)j | fl);
@@ -684,6 +705,7 @@ __device__ __forceinline__ void emit_cells_warp(const CellEmitDir& d, int dir, c
         }
       }
       flush_if_full();
+      CELL_CHECK(!hit || (qn < kLaneQ && j >= 0 && j < (dir ? N : M)));
       if (hit) {
         if (dir == 0) {
           const uint32_t fl2 = (d2 <= R2l ? kFlagRow : 0u) | (d2 <= r2o ? kFlagCol : 0u);

@@ -30,13 +30,19 @@ run KIND=shapenet B=4 NN=1024 MM=1024 PLAN=1
 run KIND=mmfi B=2 NN=1024 MM=512 APML_CL=1
 run KIND=mmfi B=3 NN=700 MM=520 RAGGED=1
 run KIND=uniform B=2 NN=4500 MM=4200 APML_CULL=1
+run KIND=scene B=1 NN=9000 MM=8000
+run KIND=uniform B=2 NN=4500 MM=4200 APML_CULL=1 APML_CULL_MODE=0
+run KIND=uniform B=1 NN=5000 MM=5000 APML_CELL_BITS=6
 run KIND=uniform B=2 NN=700 MM=650 APML_FWD2=0
 run KIND=uniform B=2 NN=700 MM=650 UNIFORM=1
 run KIND=uniform B=2 NN=700 MM=650 APML_GRID=1 APML_RS_COLLECTIVES=1
 echo "== racecheck (shared memory), fwd2/bwd2 CL=1"
 env REPO=$PWD KIND=mmfi B=1 NN=512 MM=256 APML_CL=1 compute-sanitizer --tool racecheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -6
+echo "== racecheck (shared memory), the cell-grid sweeps (k_cells.cuh) + grid sparse stage"
+env REPO=$PWD KIND=scene B=1 NN=5000 MM=5000 compute-sanitizer --tool racecheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -6
 echo "== synccheck (barrier / cluster-barrier divergence), fwd2/bwd2 CL=4 and the grid path"
 env REPO=$PWD KIND=shapenet B=2 NN=1024 MM=1024 APML_CL=4 compute-sanitizer --tool synccheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -4
 env REPO=$PWD KIND=uniform B=2 NN=700 MM=650 APML_GRID=1 compute-sanitizer --tool synccheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -4
 echo "== initcheck (reads of uninitialised device memory), default path + plan"
 env REPO=$PWD KIND=shapenet B=2 NN=1024 MM=1024 PLAN=1 compute-sanitizer --tool initcheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -4
+env REPO=$PWD KIND=scene B=1 NN=5000 MM=5000 compute-sanitizer --tool initcheck --print-limit 5 python /tmp/san2.py 2>&1 | tail -4
