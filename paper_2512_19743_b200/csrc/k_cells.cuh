@@ -134,11 +134,20 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
                                          const int* __restrict__ perm, int relabel, const CellStage& st, int& filled,
                                          Eval&& eval) {
   const int lane = threadIdx.x & 31;
-  const int ex = B.hi[0] - B.lo[0] + 1, ey = B.hi[1] - B.lo[1] + 1, ez = B.hi[2] - B.lo[2] + 1;
+  // the box is enumerated in x-PAIRS of cells (2 px, 2 px + 1): x is the lowest bit of the
+  // Morton key, so the two cells of a pair are consecutive keys and their points one contiguous
+  // range -- one start lookup and one lane per pair (about half the rounds); a pair half outside
+  // the box (or inside the skip box S) contributes its other cell only
+  const int px0 = B.lo[0] >> 1;
+  const int ex = (B.hi[0] >> 1) - px0 + 1, ey = B.hi[1] - B.lo[1] + 1, ez = B.hi[2] - B.lo[2] + 1;
   const int exy = ex * ey, V = exy * ez;
   // small-integer division by ex, ex * ey in fp32 (exact for V < 2^17: the quotient's true value
   // is at least 0.5 / ex away from an integer)
   const float rx = 1.0f / (float)ex, rxy = 1.0f / (float)exy;
+  auto in_skip = [&](int ix, int iy, int iz) {
+    return S && ix >= S->lo[0] && ix <= S->hi[0] && iy >= S->lo[1] && iy <= S->hi[1] && iz >= S->lo[2] &&
+           iz <= S->hi[2];
+  };
   // the cell starts of the NEXT round are loaded before this round's points are staged and
   // evaluated (their latency overlaps the work)
   auto cell_of = [&](int idx, uint32_t& cst, uint32_t& cnt) {
@@ -147,14 +156,14 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
     if (idx < V) {
       const int qz = (int)(((float)idx + 0.5f) * rxy), rem = idx - qz * exy;
       const int qy = (int)(((float)rem + 0.5f) * rx), qx = rem - qy * ex;
-      const int ix = B.lo[0] + qx, iy = B.lo[1] + qy, iz = B.lo[2] + qz;
-      const bool skip = S && ix >= S->lo[0] && ix <= S->hi[0] && iy >= S->lo[1] && iy <= S->hi[1] &&
-                        iz >= S->lo[2] && iz <= S->hi[2];
-      if (!skip) {
-        const uint32_t key = morton3((uint32_t)ix, (uint32_t)iy, (uint32_t)iz);
-        CELL_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && ix < 1024 && iy < 1024 && iz < 1024);
+      const int x0 = 2 * (px0 + qx), iy = B.lo[1] + qy, iz = B.lo[2] + qz;
+      const bool in0 = x0 >= B.lo[0] && !in_skip(x0, iy, iz);
+      const bool in1 = x0 + 1 <= B.hi[0] && !in_skip(x0 + 1, iy, iz);
+      if (in0 || in1) {
+        const uint32_t key = morton3((uint32_t)(in0 ? x0 : x0 + 1), (uint32_t)iy, (uint32_t)iz);
+        CELL_CHECK(x0 >= 0 && iy >= 0 && iz >= 0 && x0 < 1024 && iy < 1024 && iz < 1024);
         cst = __ldg(start + key);
-        cnt = __ldg(start + key + 1);
+        cnt = __ldg(start + key + ((in0 && in1) ? 2u : 1u));
         CELL_CHECK(cnt >= cst && cnt <= (uint32_t)str_np);
       }
     }

@@ -1,5 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q -k "fallback_paths or C4 or C5 or rowshard or grad_gt_every" 2>&1 | tail -15 > gpurun_out/pytest_cells.txt
 for c in C5 C4; do python bench.py --config $c --steps 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_${c,,}.json 2>&1; done
 python scripts/summ.py c5 c4 > gpurun_out/summary_cells.txt 2>&1
