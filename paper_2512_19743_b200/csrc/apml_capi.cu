@@ -1123,7 +1123,7 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
     k_rs_col_soft_fin<<<gc256, 256, 0, s>>>(a);
     c->launches += 4;
   }
-  k_rs_grad<<<gr, kRsThreads, 0, s>>>(a);
+  k_rs_grad<<<gr256, 256, 0, s>>>(a);
   c->launches += 1;
   CK(cudaGetLastError());
   return APML_OK;

@@ -757,7 +757,7 @@ __global__ void k_rs_col_soft_fin(const SparseArgs A) {
   A.colback[(size_t)b * M + j] = out;
 }
 
-__global__ void __launch_bounds__(kRsThreads, 2) k_rs_grad(const SparseArgs A) {
+__global__ void __launch_bounds__(256, 3) k_rs_grad(const SparseArgs A) {
   __shared__ uint32_t s_long[kLongCap];
   __shared__ int s_n;
   const int b = blockIdx.y;
