@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--oracle-max-n", type=int, default=1024)
     ap.add_argument("--min-n", type=int, default=64)
     ap.add_argument("--no-write", action="store_true", help="print only (profiles/ untouched)")
+    ap.add_argument("--all-large", action="store_true", help="--trials also at N > 65536 (else a tenth)")
     args = ap.parse_args()
 
     import numpy as np
@@ -41,7 +42,7 @@ def main():
     rows = []
     n = args.min_n
     while n <= args.max_n:
-        trials = args.trials if n <= 65536 else max(1, args.trials // 10)
+        trials = args.trials if (n <= 65536 or args.all_large) else max(1, args.trials // 10)
         per_call = args.batch or max(1, min(trials, (1 << 24) // (n * n) + 1, 64))
         nnz = []
         peak = 0
