@@ -150,7 +150,9 @@ typedef struct {
     int64_t sweep_evals[3]; /* (i, j) distance evaluations executed by the sweeps of the last
                                forward: [0] Pass A rows, [1] Pass A columns, [2] emit.  Full
                                sweeps: every padded pair (B Np Mp); spatially culled sweeps:
-                               counted on the device (32 x 32 blocks actually evaluated) */
+                               counted on the device (cell-grid sweeps: the (own point, staged
+                               point) pairs evaluated, both emit passes in [2]; the tile walk,
+                               APML_CULL_MODE=0: the 32 x 32 blocks evaluated) */
     int64_t uniform_count;  /* lines given the uniform fallback (APML_FLAG_UNIFORM_FALLBACK) */
 } apml_stats;
 
