@@ -12,5 +12,5 @@ ncu --set full --clock-control none --import-source on -k regex:"k_line_top2|k_e
 ncu --set full --clock-control none --import-source on -k regex:"k_rs_colsum_bstep|k_rs_bwd_rowrev2_rowrev" -s 20 -c 2 -o gpurun_out/full_c4 $B --no-graph --config C4 > gpurun_out/ncu_full_c4.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_top2_cells|k_emit_cells" -s 2 -c 2 -o gpurun_out/full_c4cells python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-graph --config C4 > gpurun_out/ncu_full_c4cells.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"k_top2_cells|k_emit_cells" -s 2 -c 2 -o gpurun_out/full_c5 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-graph --config C5 > gpurun_out/ncu_full_c5.log 2>&1
-timeout 900 python scripts/fig2.py --trials 50 > gpurun_out/fig2.log 2>&1
+timeout 900 python scripts/fig2.py --trials 500 --all-large > gpurun_out/fig2.log 2>&1
 cp profiles/fig2_nnz.csv profiles/fig2_nnz.md gpurun_out/ 2>/dev/null
