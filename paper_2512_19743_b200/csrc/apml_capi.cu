@@ -480,7 +480,10 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   // culled sweeps leave one (min, second) partial per line ([B][n], S = 1)
   const int64_t parts_r = c->cull ? B * N : (int64_t)c->S_rows * B * c->Np;
   const int64_t parts_c = c->cull ? B * M : (int64_t)c->S_cols * B * c->Mp;
-  size_t o_predS = k.take<float>(B * 3 * c->Np), o_gtS = k.take<float>(B * 3 * c->Mp);
+  // the SoA copies of the clouds (full sweeps, tile walk; the cell sweeps of relabelled clouds
+  // read the float4 copies in sorted order instead)
+  const bool soa = !(c->cells && c->relabel);
+  size_t o_predS = k.take<float>(soa ? B * 3 * c->Np : 0), o_gtS = k.take<float>(soa ? B * 3 * c->Mp : 0);
   size_t o_pred4 = k.take<float4>(B * N), o_gt4 = k.take<float4>(B * M);
   size_t o_part_r = k.take<float2>(parts_r);
   size_t o_part_c = k.take<float2>(parts_c);
@@ -537,7 +540,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   if (!c->embase) return fail(APML_ERR_OOM, "allocation of the emit buffer failed");
   c->ebuf = (uint2*)c->embase;
   char* p = c->base;
-  c->predS = (float*)(p + o_predS); c->gtS = (float*)(p + o_gtS);
+  c->predS = soa ? (float*)(p + o_predS) : nullptr;
+  c->gtS = soa ? (float*)(p + o_gtS) : nullptr;
   c->pred4 = (float4*)(p + o_pred4); c->gt4 = (float4*)(p + o_gt4);
   c->part_r = (float2*)(p + o_part_r); c->part_c = (float2*)(p + o_part_c);
   c->rowA = (LineA*)(p + o_rowA); c->colA = (LineA*)(p + o_colA);
@@ -733,10 +737,12 @@ apml_status launch_passA_cull(apml_ctx* c, const float* pred, const float* gt) {
       const int v = (int)maxblock;
       CK(cudaMemcpyToSymbol(g_cell_maxblock, &v, sizeof v));
     }
+    const float4* p4 = c->relabel ? c->pred4 : nullptr;
+    const float4* g4 = c->relabel ? c->gt4 : nullptr;
     const CellDir dr{c->predS, (int)Np, N, c->pperm, c->gtS, (int)Mp, c->gstart, c->part_r, c->clamp + 1,
-                     (int)((Np + cw - 1) / cw)};
+                     (int)((Np + cw - 1) / cw), p4, g4, M};
     const CellDir dc{c->gtS, (int)Mp, M, c->gperm, c->predS, (int)Np, c->pstart, c->part_c, c->clamp + 2,
-                     (int)((Mp + cw - 1) / cw)};
+                     (int)((Mp + cw - 1) / cw), g4, p4, N};
     mark(c, 1, s);
     k_top2_cells<<<dim3(std::max(dr.nblk, dc.nblk), B, 2), cw, 0, s>>>(dr, dc, c->pbb, bits, cells1, (int)c->relabel);
     c->passA_fused = true;
@@ -791,10 +797,12 @@ apml_status launch_emit_cull(apml_ctx* c) {
   if (c->cells) {  // row pass + column pass over the cell grid (k_cells.cuh)
     const int bits = c->cell_bits, cells1 = (1 << (3 * bits)) + 1;
     const int cw = 32 * kCellWarps;
+    const float4* p4 = c->relabel ? c->pred4 : nullptr;
+    const float4* g4 = c->relabel ? c->gt4 : nullptr;
     const CellEmitDir dr{c->predS, (int)Np, N, c->pperm, c->rowA, c->gtS, (int)Mp, c->gstart, c->gperm, c->colA,
-                         (int)((Np + cw - 1) / cw)};
+                         (int)((Np + cw - 1) / cw), p4, g4, M};
     const CellEmitDir dc{c->gtS, (int)Mp, M, c->gperm, c->colA, c->predS, (int)Np, c->pstart, c->pperm, c->rowA,
-                         (int)((Mp + cw - 1) / cw)};
+                         (int)((Mp + cw - 1) / cw), g4, p4, N};
     k_emit_cells<<<dim3(std::max(dr.nblk, dc.nblk), B, 2), cw, 0, s>>>(dr, dc, c->pbb, bits, cells1, (int)c->relabel,
         N, M, c->cap_e, c->ebuf, c->cursor, c->aux, c->row_cnt, c->col_cnt, c->clamp + 3);
     c->launches += 1;

@@ -132,7 +132,9 @@ template <bool kEmit, typename Eval>
 __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, const uint32_t* __restrict__ start,
                                          const float* __restrict__ str, int str_np, const float* __restrict__ r2src,
                                          const int* __restrict__ perm, int relabel, const CellStage& st, int& filled,
-                                         Eval&& eval) {
+                                         Eval&& eval, const float4* __restrict__ s4 = nullptr) {
+  // s4 (relabelled clouds): the float4 copy in sorted order -- one 16-byte load per point
+  // instead of three from the SoA copy (which is then not written at all)
   const int lane = threadIdx.x & 31;
   // the box is enumerated in x-PAIRS of cells (2 px, 2 px + 1): x is the lowest bit of the
   // Morton key, so the two cells of a pair are consecutive keys and their points one contiguous
@@ -205,11 +207,19 @@ __device__ __forceinline__ void scan_box(const CellBox& B, const CellBox* S, con
       int o0 = 0, o1 = 0;
       CELL_CHECK(!v0 || (src0 < (uint32_t)str_np && filled + lane < kCellBuf));
       CELL_CHECK(!v1 || (src1 < (uint32_t)str_np && filled + 32 + lane < kCellBuf));
-      if (v0) {
+      if (v0 && s4) {
+        const float4 q = __ldg(s4 + src0);
+        x0 = q.x; y0 = q.y; z0 = q.z;
+        if (kEmit) { o0 = relabel ? (int)src0 : __ldg(perm + src0); }
+      } else if (v0) {
         x0 = __ldg(str + src0); y0 = __ldg(str + str_np + src0); z0 = __ldg(str + 2 * (size_t)str_np + src0);
         if (kEmit) { o0 = relabel ? (int)src0 : __ldg(perm + src0); }
       }
-      if (v1) {
+      if (v1 && s4) {
+        const float4 q = __ldg(s4 + src1);
+        x1 = q.x; y1 = q.y; z1 = q.z;
+        if (kEmit) { o1 = relabel ? (int)src1 : __ldg(perm + src1); }
+      } else if (v1) {
         x1 = __ldg(str + src1); y1 = __ldg(str + str_np + src1); z1 = __ldg(str + 2 * (size_t)str_np + src1);
         if (kEmit) { o1 = relabel ? (int)src1 : __ldg(perm + src1); }
       }
@@ -254,12 +264,17 @@ struct CellOwn {
   bool valid;
 };
 __device__ __forceinline__ CellOwn cell_own(const float* __restrict__ own, int own_np, int own_n, int k,
-                                            const CellFrame& F) {
+                                            const CellFrame& F, const float4* __restrict__ own4 = nullptr) {
   CellOwn o;
   o.valid = k < own_n;
-  o.x = o.valid ? __ldg(own + k) : 0.f;
-  o.y = o.valid ? __ldg(own + own_np + k) : 0.f;
-  o.z = o.valid ? __ldg(own + 2 * (size_t)own_np + k) : 0.f;
+  if (own4) {
+    const float4 q = o.valid ? __ldg(own4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    o.x = q.x; o.y = q.y; o.z = q.z;
+  } else {
+    o.x = o.valid ? __ldg(own + k) : 0.f;
+    o.y = o.valid ? __ldg(own + own_np + k) : 0.f;
+    o.z = o.valid ? __ldg(own + 2 * (size_t)own_np + k) : 0.f;
+  }
   const float p[3] = {o.x, o.y, o.z};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
@@ -420,6 +435,9 @@ struct CellDir {
   float2* out;                // (min2, second2) at the output index
   unsigned long long* evals;
   int nblk;
+  const float4* own4 = nullptr;  // relabelled clouds: the float4 copies in sorted order [B][n]
+  const float4* str4 = nullptr;  // (the SoA copies own / str are then NULL)
+  int str_n = 0;
 };
 
 __device__ __forceinline__ void top2_cells_warp(const CellDir& d, const float* bb, int bits, int cells1,
@@ -428,11 +446,18 @@ __device__ __forceinline__ void top2_cells_warp(const CellDir& d, const float* b
   __shared__ __align__(16) float s_buf[kCellWarps][3][kCellBuf + 4];
   const CellStage st{s_buf[w][0], s_buf[w][1], s_buf[w][2], nullptr, nullptr};
   const CellFrame F = cell_frame(bb + 6 * b, bits);
-  const float* own = d.own + (size_t)b * 3 * d.own_np;
-  const float* str = d.str + (size_t)b * 3 * d.str_np;
+  const float* own = d.own ? d.own + (size_t)b * 3 * d.own_np : nullptr;
+  const float* str = d.str ? d.str + (size_t)b * 3 * d.str_np : nullptr;
+  const float4* own4 = d.own4 ? d.own4 + (size_t)b * d.own_n : nullptr;
+  const float4* str4 = d.str4 ? d.str4 + (size_t)b * d.str_n : nullptr;
+  // a point of the streamed cloud at sorted position t (float4 copy or SoA)
+  auto str_pt = [&](uint32_t t) {
+    if (str4) return __ldg(str4 + t);
+    return make_float4(__ldg(str + t), __ldg(str + d.str_np + t), __ldg(str + 2 * (size_t)d.str_np + t), 0.f);
+  };
   const uint32_t* start = d.str_start + (size_t)b * cells1;
   const int k = k0 + lane;
-  const CellOwn o = cell_own(own, d.own_np, d.own_n, k, F);
+  const CellOwn o = cell_own(own, d.own_np, d.own_n, k, F, own4);
   const f2_t nx = f2_pack(-o.x, -o.x), ny = f2_pack(-o.y, -o.y), nz = f2_pack(-o.z, -o.z);
   const float inf = __int_as_float(0x7f800000);
   float m = inf, s = inf, m2 = inf, s2 = inf;
@@ -466,7 +491,7 @@ __device__ __forceinline__ void top2_cells_warp(const CellDir& d, const float* b
       }
       __syncwarp();  // the buffer is refilled next
     };
-    scan_box<false>(Bx, nullptr, start, str, d.str_np, nullptr, nullptr, relabel, st, filled, eval);
+    scan_box<false>(Bx, nullptr, start, str, d.str_np, nullptr, nullptr, relabel, st, filled, eval, str4);
     if (filled) { __syncwarp(); eval(filled); filled = 0; }
     for (;;) {
       float mm = m, ss = s;
@@ -480,7 +505,7 @@ __device__ __forceinline__ void top2_cells_warp(const CellDir& d, const float* b
       }
       cell_stat(3, 1);
       const CellBox Nb = box_grow(Bx, F.G);
-      scan_box<false>(Nb, &Bx, start, str, d.str_np, nullptr, nullptr, relabel, st, filled, eval);
+      scan_box<false>(Nb, &Bx, start, str, d.str_np, nullptr, nullptr, relabel, st, filled, eval, str4);
       if (filled) { __syncwarp(); eval(filled); filled = 0; }
       Bx = Nb;
     }
@@ -500,8 +525,8 @@ __device__ __forceinline__ void top2_cells_warp(const CellDir& d, const float* b
     float fm = inf, fs = inf;
     far_scan(F, bits, start, fl, r2, [&](uint32_t t, bool v) {
       if (!v) return;
-      const float dx = __fadd_rn(__ldg(str + t), xl), dy = __fadd_rn(__ldg(str + d.str_np + t), yl),
-                  dz = __fadd_rn(__ldg(str + 2 * (size_t)d.str_np + t), zl);
+      const float4 q = str_pt(t);
+      const float dx = __fadd_rn(q.x, xl), dy = __fadd_rn(q.y, yl), dz = __fadd_rn(q.z, zl);
       float d2 = __fmul_rn(dx, dx);
       d2 = __fmaf_rn(dy, dy, d2);
       d2 = __fmaf_rn(dz, dz, d2);
@@ -547,6 +572,9 @@ struct CellEmitDir {
   const int* str_perm;
   const LineA* strA;          // the other cloud's line constants at the output index
   int nblk;
+  const float4* own4 = nullptr;  // relabelled clouds: the float4 copies in sorted order [B][n]
+  const float4* str4 = nullptr;
+  int str_n = 0;
 };
 
 __device__ __forceinline__ void emit_cells_warp(const CellEmitDir& d, int dir, const float* bb, int bits,
@@ -564,14 +592,21 @@ __device__ __forceinline__ void emit_cells_warp(const CellEmitDir& d, int dir, c
   uint2* qp = &queue_all[w][0][lane];
   int qn = 0;
   const CellFrame F = cell_frame(bb + 6 * b, bits);
-  const float* own = d.own + (size_t)b * 3 * d.own_np;
-  const float* str = d.str + (size_t)b * 3 * d.str_np;
+  const float* own = d.own ? d.own + (size_t)b * 3 * d.own_np : nullptr;
+  const float* str = d.str ? d.str + (size_t)b * 3 * d.str_np : nullptr;
+  const float4* own4 = d.own4 ? d.own4 + (size_t)b * d.own_n : nullptr;
+  const float4* str4 = d.str4 ? d.str4 + (size_t)b * d.str_n : nullptr;
+  // a point of the streamed cloud at sorted position t (float4 copy or SoA)
+  auto str_pt = [&](uint32_t t) {
+    if (str4) return __ldg(str4 + t);
+    return make_float4(__ldg(str + t), __ldg(str + d.str_np + t), __ldg(str + 2 * (size_t)d.str_np + t), 0.f);
+  };
   const uint32_t* start = d.str_start + (size_t)b * cells1;
   const int* sperm = d.str_perm + (size_t)b * d.str_np;
   const LineA* strA = d.strA + (size_t)b * (dir ? N : M);
   const float* r2src = reinterpret_cast<const float*>(strA) + (dir ? 3 : 2);
   const int k = k0 + lane;
-  const CellOwn o = cell_own(own, d.own_np, d.own_n, k, F);
+  const CellOwn o = cell_own(own, d.own_np, d.own_n, k, F, own4);
   const int oi = o.valid ? (relabel ? k : d.own_perm[(size_t)b * d.own_np + k]) : -1;
   float oR2 = -1.f, oE2 = -1.f;
   if (oi >= 0) {
@@ -681,7 +716,7 @@ __device__ __forceinline__ void emit_cells_warp(const CellEmitDir& d, int dir, c
       }
       __syncwarp();  // the buffer is refilled next
     };
-    scan_box<true>(Bx, nullptr, start, str, d.str_np, r2src, sperm, relabel, st, filled, eval);
+    scan_box<true>(Bx, nullptr, start, str, d.str_np, r2src, sperm, relabel, st, filled, eval, str4);
     if (filled) { __syncwarp(); eval(filled); filled = 0; }
   });
   // far lanes, one at a time, all lanes cooperating (the hits go to the queue of the lane that
@@ -701,8 +736,8 @@ __device__ __forceinline__ void emit_cells_warp(const CellEmitDir& d, int dir, c
       float d2 = 0.f, r2o = 0.f;
       int j = -1;
       if (v) {
-        const float dx = __fadd_rn(__ldg(str + t), xl), dy = __fadd_rn(__ldg(str + d.str_np + t), yl),
-                    dz = __fadd_rn(__ldg(str + 2 * (size_t)d.str_np + t), zl);
+        const float4 q = str_pt(t);
+        const float dx = __fadd_rn(q.x, xl), dy = __fadd_rn(q.y, yl), dz = __fadd_rn(q.z, zl);
         d2 = __fmul_rn(dx, dx);
         d2 = __fmaf_rn(dy, dy, d2);
         d2 = __fmaf_rn(dz, dz, d2);

@@ -135,9 +135,9 @@ __device__ void cell_scatter_body(const float* __restrict__ pts, int n, int np, 
                                   const uint32_t* __restrict__ rank, float* __restrict__ soa, int* __restrict__ perm,
                                   float4* __restrict__ p4, int* __restrict__ iperm, int b, int k) {
   if (k >= np) return;
-  float* s = soa + (size_t)b * 3 * np;
+  float* s = soa ? soa + (size_t)b * 3 * np : nullptr;  // (NULL: the cell sweeps read the float4 copy)
   if (k >= n) {  // pads occupy the sorted positions [n, np)
-    s[k] = sentinel; s[np + k] = sentinel; s[2 * np + k] = sentinel;
+    if (s) { s[k] = sentinel; s[np + k] = sentinel; s[2 * np + k] = sentinel; }
     perm[(size_t)b * np + k] = -1;
     return;
   }
@@ -145,7 +145,7 @@ __device__ void cell_scatter_body(const float* __restrict__ pts, int n, int np, 
   const uint32_t kk = key[(size_t)b * n + k];
   const uint32_t pos = start[hb + kk] + rank[(size_t)b * n + k];
   const float* p = pts + ((size_t)b * n + k) * 3;
-  s[pos] = p[0]; s[np + pos] = p[1]; s[2 * np + pos] = p[2];
+  if (s) { s[pos] = p[0]; s[np + pos] = p[1]; s[2 * np + pos] = p[2]; }
   perm[(size_t)b * np + pos] = k;
   if (p4) {
     p4[(size_t)b * n + pos] = make_float4(p[0], p[1], p[2], 0.f);
