@@ -405,11 +405,15 @@ apml_status alloc_entries(apml_ctx* c, uint32_t cap) {
   size_t o_csr_t = k.take<uint32_t>(E1), o_csc_t = k.take<uint32_t>(E1), o_inv = k.take<uint32_t>(E);
   size_t o_csr_jf = k.take<uint32_t>(E), o_csc_i = k.take<uint32_t>(E), o_csc_perm = k.take<uint32_t>(E);
   size_t o_d2 = k.take<float>(E1), o_cs = k.take<float>(E), o_prow = k.take<float>(E), o_pcol = k.take<float>(E);
-  size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(E);
+  // grid-wide path: the emit-index arrays csr_t / csc_t are dead once the columns are sorted
+  // (k_rs_cols_a); the backward's P0bar and the Sinkhorn's 16-bit index copies (written by
+  // k_rs_idx16 after k_rs_cols_b) live in them -- 8 bytes per entry less
+  const bool rs_alias = c->rs && E1 == E && env_long("APML_RS_ALIAS", 1) != 0;
+  size_t o_P0 = k.take<float>(E), o_P0c = k.take<float>(E), o_pbar = k.take<float>(rs_alias ? 0 : E);
   const int64_t E2 = f2 ? E : 0;  // CSC-order copies written by k_sparse_fwd2
   size_t o_csc_if = k.take<uint32_t>(E2), o_csc_c = k.take<float>(E2), o_csc_pc = k.take<float>(E2);
   const int64_t E3 = (c->rs && c->N <= 65536 && c->M <= 65536 && env_long("APML_RS_IDX16", 1) != 0) ? E : 0;
-  size_t o_csr16 = k.take<uint16_t>(E3), o_csc16 = k.take<uint16_t>(E3);
+  size_t o_csr16 = k.take<uint16_t>(rs_alias ? 0 : E3), o_csc16 = k.take<uint16_t>(rs_alias ? 0 : E3);
   c->ebytes = k.off;
   c->ebase = (char*)ctx_alloc(c, c->ebytes);
   if (!c->ebase) return fail(APML_ERR_OOM, "allocation of " + std::to_string(c->ebytes) + " bytes failed");
@@ -421,6 +425,11 @@ apml_status alloc_entries(apml_ctx* c, uint32_t cap) {
   c->csc_if = (uint32_t*)(p + o_csc_if); c->csc_c = (float*)(p + o_csc_c); c->csc_pc = (float*)(p + o_csc_pc);
   c->csr16 = E3 ? (uint16_t*)(p + o_csr16) : nullptr;
   c->csc16 = E3 ? (uint16_t*)(p + o_csc16) : nullptr;
+  if (rs_alias) {
+    c->pbar = reinterpret_cast<float*>(c->csc_t);
+    c->csr16 = E3 ? reinterpret_cast<uint16_t*>(c->csr_t) : nullptr;
+    c->csc16 = E3 ? reinterpret_cast<uint16_t*>(c->csr_t) + E : nullptr;
+  }
   return APML_OK;
 }
 
