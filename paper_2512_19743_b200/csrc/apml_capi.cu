@@ -520,7 +520,8 @@ apml_status build_ctx(apml_ctx* c, uint32_t cap, bool entries = true) {
   const int64_t W = c->rs ? c->comm.world : 0;
   // world 1 without forced collectives: the "gathered" copies ARE the local arrays
   const bool w1 = c->rs && c->comm.world == 1 && env_long("APML_RS_COLLECTIVES", 0) == 0;
-  size_t o_colpart = k.take<float2>(c->rs ? B * M : 0), o_gath = k.take<float2>(w1 ? 0 : W * B * M);
+  // (one GPU with culled sweeps: the line constants read Pass A's column partials directly)
+  size_t o_colpart = k.take<float2>((c->rs && !(c->cull && w1)) ? B * M : 0), o_gath = k.take<float2>(w1 ? 0 : W * B * M);
   size_t o_colred = k.take<float>(c->rs ? 3 * B * M : 0), o_qbuf = k.take<float>(c->rs ? B * M : 0);
   size_t o_cand = k.take<int>(c->rs ? 3 * B * M : 0), o_gcand = k.take<int>(w1 ? 0 : 3 * W * B * M);
   size_t o_flag = k.take<float>(16);
@@ -970,9 +971,12 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
   cudaStream_t s = c->stream;
   mark(c, 0, s);
   apml_status st;
+  // one GPU with culled sweeps: the column partials are final ([B][M], S = 1) and nothing is
+  // gathered, so both line-constant passes run in one launch straight from Pass A's output
+  const bool w1_cull = c->cull && rs_fused(c);
   if (c->cull) {
     if ((st = launch_passA_cull(c, pred, gt)) != APML_OK) return st;
-    k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, c->colpart);
+    if (!w1_cull) k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, 1, B, M, M, c->colpart);
   } else {
     k_stage<<<dim3((Np + 255) / 256, B), 256, 0, s>>>(pred, N, Np, kPadPred, c->predS, c->pred4, nullptr);
     k_stage<<<dim3((Mp + 255) / 256, B), 256, 0, s>>>(gt, M, Mp, kPadGt, c->gtS, c->gt4, nullptr);
@@ -985,6 +989,19 @@ apml_status launch_forward_rs(apml_ctx* c, const float* pred, const float* gt) {
     k_top2_collapse<<<dim3((M + 255) / 256, B), 256, 0, s>>>(c->part_c, c->S_cols, B, Mp, M, c->colpart);
   }
   CK(cudaGetLastError());
+  if (w1_cull) {
+    mark(c, 3, s);
+    const LineInfoDir lr_{c->part_r, 1, N, N, M, c->lam_r, c->rho_r, c->rowA, c->rowB, c->nb_d, c->mb_d, 0};
+    const LineInfoDir lc_{c->part_c, 1, M, M, (int)c->N_global, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2};
+    k_line_info_both<<<dim3((std::max(N, M) + 255) / 256, B, 2), 256, 0, s>>>(lr_, lc_, B, c->cfg.delta, c->cfg.eps_g,
+                                                                             c->clamp, (const float*)c->lr_d, ufb(c));
+    mark(c, 4, s);
+    if ((st = launch_emit_cull(c)) != APML_OK) return st;
+    mark(c, 5, s);
+    c->launches += 2;
+    CK(cudaGetLastError());
+    return APML_OK;
+  }
   st = coll_gather(c, (const float*)c->colpart, (float*)c->gath, 2LL * B * M);
   if (st != APML_OK) return st;
   mark(c, 3, s);
