@@ -1144,7 +1144,7 @@ apml_status launch_backward_rs(apml_ctx* c, const float* grad_loss, float* grad_
         k_rs_bwd_colrev<<<gc256, 256, 0, s>>>(a, l, c->qbuf);
         c->launches += 2;
       }
-      k_rs_bwd_rowrev2_rowrev<<<gr256, 256, 0, s>>>(a, l);
+      k_rs_bwd_rowrev2_rowrev<<<gr256, 256, 0, s>>>(a, l, (int)env_long("APML_RS_FUSED_REV", 1));
       c->launches += 1;
     }
     k_rs_row_soft<<<gr, kRsThreads, 0, s>>>(a);

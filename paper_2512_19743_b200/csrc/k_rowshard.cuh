@@ -485,9 +485,52 @@ __device__ __forceinline__ void grp_rowrev2(const SparseArgs& A, int b, int i, i
   if (i < N) ab[i] += t;
 }
 
+// Row step 2 of reverse iteration l (abar += P0 Qbar^l, P0bar += Qbar^l_j a^{l-1}_i) fused with
+// the row step of iteration l - 1 (Rbar^{l-1} = -abar (a^{l-1})^2, P0bar += Rbar^{l-1}_i
+// b^{l-1}_j), l > 1: a first walk folds the row sums, a second one applies BOTH P0bar terms in
+// one read-modify-write (the two walks of grp_rowrev2 + grp_rowrev each rewrote P0bar).
+__device__ __forceinline__ void grp_rowrev2_fused(const SparseArgs& A, int b, int i, int l, float* sx, float* sy,
+                                                  float* sv, float* sv2, unsigned char* own) {
+  const int N = A.N, M = A.M, L = A.L, lane = threadIdx.x & 31;
+  const size_t pb = (size_t)b * A.cap;
+  float* ab = A.gvec + (size_t)b * 2 * (N + M);
+  float* rcur = ab + N + M;
+  const float* qcur = ab + N + M + N;
+  const float alm = i < N ? A.a_hist[((size_t)b * (L + 1) + l - 1) * N + i] : 0.f;  // a^{l-1}
+  const WarpLines wl = warp_lines(A.row_ptr + (size_t)b * (N + 1), i, N);
+  float t = 0.f;
+  warp_walk(wl, nullptr,
+            [&](int k, uint32_t q) { sx[k] = qcur[rs_ridx(A, pb, q)]; sy[k] = A.P0[pb + q]; },
+            [&](int k) { t = __fmaf_rn(sx[k], sy[k], t); }, NoPost{});
+  float Rb = 0.f;
+  if (i < N) {
+    const float abi = ab[i] + t;
+    const float almm = A.a_hist[((size_t)b * (L + 1) + l - 2) * N + i];  // a^{l-2}
+    const float r = alm / almm;
+    Rb = -abi * alm * alm;
+    ab[i] = abi * A.eps * r * r;
+    rcur[i] = Rb;
+  }
+  sv[lane] = alm;
+  sv2[lane] = Rb;
+  const float* bprev = A.b_hist + ((size_t)b * (L + 1) + l - 1) * M;  // b^{l-1}
+  __syncwarp();
+  warp_walk(wl, own,
+            [&](int k, uint32_t q) {
+              const uint32_t j = rs_ridx(A, pb, q);
+              sx[k] = qcur[j];
+              sy[k] = bprev[j];
+            },
+            [&](int) {},
+            [&](int k, uint32_t q) {
+              const float p1 = __fmaf_rn(sx[k], sv[own[k]], A.pbar[pb + q]);
+              A.pbar[pb + q] = __fmaf_rn(sv2[own[k]], sy[k], p1);
+            });
+}
+
 // Shared memory of one 256-thread block of the group kernels.
 struct GrpSmem {
-  float x[kWWarps][kWChunk], y[kWWarps][kWChunk], v[kWWarps][32];
+  float x[kWWarps][kWChunk], y[kWWarps][kWChunk], v[kWWarps][32], v2[kWWarps][32];
   unsigned char own[kWWarps][kWChunk];
 };
 
@@ -685,11 +728,15 @@ __global__ void __launch_bounds__(256) k_rs_bwd_rowrev2(const SparseArgs A, int 
 
 // Row step 2 of reverse iteration l fused with the row step of iteration l - 1 (both touch
 // only the warp's own rows; no collective between them): one launch per iteration fewer.
-__global__ void __launch_bounds__(256) k_rs_bwd_rowrev2_rowrev(const SparseArgs A, int l) {
+__global__ void __launch_bounds__(256) k_rs_bwd_rowrev2_rowrev(const SparseArgs A, int l, int env_fused_rowrev) {
   __shared__ GrpSmem S;
   const int b = blockIdx.y, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = (blockIdx.x * kWWarps + wid) * 32 + lane;
   if (A.cursor[b] > A.cap || i - lane >= A.N) return;  // warp-uniform
+  if (l > 1 && env_fused_rowrev) {
+    grp_rowrev2_fused(A, b, i, l, S.x[wid], S.y[wid], S.v[wid], S.v2[wid], S.own[wid]);
+    return;
+  }
   grp_rowrev2(A, b, i, l, S.x[wid], S.y[wid], S.v[wid], S.own[wid]);
   if (l > 1) {
     __syncwarp();  // P0bar entries and the warp's scratch are shared by the lanes of both walks

@@ -428,6 +428,7 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_SMEM_LIMIT": "60000", "APML_CL": "1"},                # fwd2 / bwd2 slices in global memory
     {"APML_FUSE_INFO": "0", "APML_PDL": "0"},                    # separate line-info launch, no PDL
     {"APML_GRID": "1", "APML_RS_IDX16": "0"},                    # grid path with 32-bit Sinkhorn indices
+    {"APML_GRID": "1", "APML_RS_FUSED_REV": "0", "APML_RS_ALIAS": "0"},  # grid path: two P0bar walks, no aliasing
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
 def test_sparse_stage_fallback_paths(env, monkeypatch):
     """The plan the library picks depends on N, M, B and shared memory; force every variant at a
