@@ -882,7 +882,11 @@ apml_status launch_forward(apml_ctx* c, const float* pred, const float* gt) {
     const LineInfoDir lc_{c->part_c, c->S_cols, (int)Mp, M, N, c->lam_c, c->rho_c, c->colA, c->colB, c->mb_d, c->nb_d, 2,
                           c->colR2s, c->colE2s, (int)Mp};
     const dim3 ga(std::max(dr.nblk, dc.nblk), std::max(c->S_rows, c->S_cols), 2 * B);
-    if (env_long("APML_FUSE_INFO", 1) != 0) {  // S2 in the last CTA of every row block
+    // S2 in the last CTA of every row block when it has few column splits to merge (C3: one
+    // launch less, 1.193 -> 1.190 ms); with many (C2: 8) the separate, fully parallel
+    // k_line_info_both is faster (0.319 -> 0.317 ms).  APML_FUSE_INFO=0/1 forces either.
+    const long fuse = env_long("APML_FUSE_INFO", -1);
+    if (fuse > 0 || (fuse < 0 && std::max(c->S_rows, c->S_cols) <= 4)) {
       const FusedInfo fi{{lr_, lc_}, c->cfg.delta, c->cfg.eps_g, c->clamp, (const float*)c->lr_d, ufb(c), c->icnt,
                          (int)(std::max(Np, Mp) / kOwnTile)};
       CK(launch_pdl(k_line_top2_info<kR>, ga, dim3(kSweepThreads), 0, s, 0, dr, dc, B, fi));

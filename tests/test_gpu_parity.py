@@ -427,6 +427,7 @@ def test_sharded_loss_single_rank_equals_plain_sum():
     {"APML_BWD2": "0"},                                          # k_sparse_fwd2 + k_sparse_bwd
     {"APML_SMEM_LIMIT": "60000", "APML_CL": "1"},                # fwd2 / bwd2 slices in global memory
     {"APML_FUSE_INFO": "0", "APML_PDL": "0"},                    # separate line-info launch, no PDL
+    {"APML_FUSE_INFO": "1"},                                     # line constants fused into Pass A
     {"APML_GRID": "1", "APML_RS_IDX16": "0"},                    # grid path with 32-bit Sinkhorn indices
     {"APML_GRID": "1", "APML_RS_FUSED_REV": "0", "APML_RS_ALIAS": "0"},  # grid path: two P0bar walks, no aliasing
 ], ids=lambda e: ",".join(f"{k[5:]}={v}" for k, v in e.items()))
